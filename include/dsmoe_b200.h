@@ -1,0 +1,203 @@
+/* dsmoe_b200 — B200 (sm_100a) device path for the DualSparse-MoE MoE-module
+ * forward.  C ABI: plain pointers, sizes and status codes; no C++ or torch
+ * types cross it.  Status codes and the thread-local last-error convention are
+ * the reference's (/root/reference/proj/include/dsmoe.h:16-24, capi.cpp:35-58):
+ * every entry point returns DSMOE_OK (0) or a DSMOE_E_* code and never lets an
+ * exception escape.
+ *
+ * Pointers documented "device" are CUDA global-memory addresses; "host"
+ * pointers are ordinary memory.  `stream` is a cudaStream_t passed as void*
+ * (NULL = the legacy default stream).  Layers are immutable after their
+ * weights are set; calls on distinct contexts may run concurrently.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/proj):
+ *   dsmoe_b200_layer_*          MoeLayer<T> (include/dsmoe/moe.hpp:73-120)
+ *   dsmoe_b200_route            route_and_drop (include/dsmoe/dropping.hpp:248),
+ *                               i.e. gate_scores moe.hpp:170, topk_route :181,
+ *                               replay_routing :277, ensure_normalized
+ *                               dropping.hpp:75, drop_1t :133 / drop_2t :141
+ *   dsmoe_b200_route_logits     the same on caller-supplied fp32 logits
+ *   dsmoe_b200_moe_forward      moe_forward (include/dsmoe/moe.hpp:239)
+ *   dsmoe_b200_forward          route_and_drop + drop_stats + moe_forward, the
+ *                               per-layer body of model_forward_dropped
+ *                               (dropping.hpp:263-274) and of dsmoe_infer
+ *                               (include/dsmoe.h:67, src/capi.cpp:328)
+ *   dsmoe_b200_drop_stats       drop_stats (include/dsmoe/dropping.hpp:171)
+ *   dsmoe_b200_profile_importance  profile_importance (reconstruct.hpp:99)
+ *   dsmoe_b200_reconstruct      build_reconstruction_map + reconstruct_experts
+ *                               (reconstruct.hpp:151, :196)
+ *   dsmoe_b200_load_aware_thresholds  load_aware_thresholds (ep_sim.hpp:76)
+ */
+#ifndef DSMOE_B200_H
+#define DSMOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef DSMOE_OK
+#define DSMOE_OK 0
+#define DSMOE_E_INVALID_ARGUMENT 1
+#define DSMOE_E_SHAPE_MISMATCH 2
+#define DSMOE_E_INVALID_STATE 3
+#define DSMOE_E_IO 4
+#define DSMOE_E_BAD_MAGIC 5
+#define DSMOE_E_TRUNCATED 6
+#define DSMOE_E_SCHEMA 7
+#define DSMOE_E_INTERNAL 8
+#endif
+
+#define DSMOE_B200_F32 0  /* element types */
+#define DSMOE_B200_BF16 1
+
+#define DSMOE_B200_DROP_NONE 0 /* DropPolicy::Kind (dropping.hpp:13) */
+#define DSMOE_B200_DROP_1T 1
+#define DSMOE_B200_DROP_2T 2
+
+#define DSMOE_B200_LOGITS_TENSOR 0 /* gate logits on tcgen05 (bf16 layers) */
+#define DSMOE_B200_LOGITS_EXACT 1  /* serial-k fp32, bit-equal to matmul (matrix.hpp:47) */
+
+#define DSMOE_B200_METRIC_GATE 0 /* Metric (reconstruct.hpp:13) */
+#define DSMOE_B200_METRIC_ABS_GATE 1
+#define DSMOE_B200_METRIC_GATE_UP 2
+#define DSMOE_B200_METRIC_ABS_GATE_UP 3
+
+typedef struct dsmoe_b200_layer dsmoe_b200_layer;
+typedef struct dsmoe_b200_ctx dsmoe_b200_ctx;
+
+/* MoeConfig (moe.hpp:17-36) + the layer state that shapes the blocks:
+ * replay_factor P (moe.hpp:79), block widths (E*P entries, block e*P+p is
+ * slice p of expert e) and shared-expert widths (S entries). */
+typedef struct {
+  int d_model;
+  int d_ffn;
+  int num_experts;
+  int top_k;
+  int num_shared_experts;
+  int gate_prenormalized;
+  int replay_factor;
+  int dtype; /* DSMOE_B200_F32 | DSMOE_B200_BF16: storage + compute type */
+  const int32_t* block_widths;  /* host, E*P entries; NULL -> d_ffn / P each */
+  const int32_t* shared_widths; /* host, S entries; NULL -> d_ffn each */
+} dsmoe_b200_layer_config;
+
+/* DropPolicy (dropping.hpp:12-56) as the policy JSON of capi.cpp:96-112 maps
+ * it: for 2T the caller supplies t_major/t_minor (default t_drop -/+ 0.01).
+ * normalize < 0 selects the default (!gate_prenormalized).
+ * t_unit (device, optional, num_experts doubles) overrides the threshold per
+ * original expert: t_major = t_unit[e] + (t_major - t_drop), t_minor =
+ * t_unit[e] + (t_minor - t_drop) — the owner-device thresholds of
+ * simulate_step (ep_sim.hpp:133-149). */
+typedef struct {
+  int kind;
+  double t_drop;
+  double t_major;
+  double t_minor;
+  int keep_top1;
+  int normalize;
+  const double* t_unit;
+} dsmoe_b200_policy;
+
+/* RoutingDecision (moe.hpp:142-167) on the device, T x (K*P) slots in the
+ * reference's copy-major order.  Any field may be NULL. */
+typedef struct {
+  int32_t* indices;
+  float* raw;        /* raw score; the reference's double raw is exactly this float */
+  double* normalized;
+  uint8_t* fraction; /* 0 -> 0.0, 1 -> 0.5, 2 -> 1.0 */
+} dsmoe_b200_routing;
+
+/* DropStats (dropping.hpp:156-166), same fields and arithmetic. */
+typedef struct {
+  long num_tokens;
+  double total_routed_units;
+  double dropped_units;
+  double shared_units;
+  double drop_rate;
+  double total_flops;
+  double saved_flops;
+  double retained_flops;
+} dsmoe_b200_drop_stats_t;
+
+const char* dsmoe_b200_version(void);
+const char* dsmoe_b200_last_error(void);
+/* number of kernels the last dsmoe_b200_forward / _moe_forward launched */
+int dsmoe_b200_last_launch_count(void);
+
+/* ---- layers ------------------------------------------------------------ */
+int dsmoe_b200_layer_create(const dsmoe_b200_layer_config* cfg, dsmoe_b200_layer** out);
+void dsmoe_b200_layer_free(dsmoe_b200_layer* layer);
+/* gate: d_model x num_experts row-major (moe.hpp:75).  src_dtype is the
+ * element type of the source; src_on_device says where it lives. */
+int dsmoe_b200_layer_set_gate(dsmoe_b200_layer* layer, const void* gate, int src_dtype,
+                              int src_on_device, void* stream);
+/* physical block b (Expert<T>, moe.hpp:39-45): w1, w3 d x width; w2 width x d. */
+int dsmoe_b200_layer_set_block(dsmoe_b200_layer* layer, int block, const void* w1, const void* w3,
+                               const void* w2, int src_dtype, int src_on_device, void* stream);
+int dsmoe_b200_layer_set_shared(dsmoe_b200_layer* layer, int s, const void* w1, const void* w3,
+                                const void* w2, int src_dtype, int src_on_device, void* stream);
+/* shape query: out8 = d, ffn, E, K, S, P, dtype, prenorm */
+int dsmoe_b200_layer_info(const dsmoe_b200_layer* layer, int32_t* out8);
+
+/* ---- execution contexts (stream + workspace) ---------------------------- */
+int dsmoe_b200_ctx_create(void* stream, dsmoe_b200_ctx** out);
+void dsmoe_b200_ctx_free(dsmoe_b200_ctx* ctx);
+/* synchronise the context's stream and report any device-side error flag
+ * raised since the last check (zero-sum normalisation, non-canonical routing) */
+int dsmoe_b200_ctx_check(dsmoe_b200_ctx* ctx);
+
+/* Per-stage device timing for dsmoe_b200_forward (CUDA events on the
+ * context's stream; each profiled call synchronises).  Stages: 0 gate logits,
+ * 1 router, 2 permute + tile plan, 3 gather, 4 grouped GEMM1 ([W1|W3] +
+ * SwiGLU), 5 grouped GEMM2 (W2 + score), 6 combine.  ms receives the summed
+ * milliseconds per stage since profiling was (re)enabled. */
+int dsmoe_b200_ctx_set_profiling(dsmoe_b200_ctx* ctx, int on);
+int dsmoe_b200_ctx_profile(const dsmoe_b200_ctx* ctx, double* ms, int n, long* calls);
+
+/* ---- the forward path --------------------------------------------------- */
+/* route_and_drop on device x (T x d_model, layer dtype).  `logits_in`
+ * (device, T x E fp32, optional) bypasses the gate matmul.  `logits_out`
+ * (device, optional) receives the logits used.  stats (host, optional)
+ * forces a stream sync and is filled like drop_stats(pre, post, config). */
+int dsmoe_b200_route(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
+                     const dsmoe_b200_policy* policy, int logits_mode, const float* logits_in,
+                     float* logits_out, const dsmoe_b200_routing* out,
+                     dsmoe_b200_drop_stats_t* stats);
+/* moe_forward with a caller routing (device arrays, T x K*P): out (device,
+ * T x d_model, layer dtype) = sum over kept slots of raw * block(x) + shared. */
+int dsmoe_b200_moe_forward(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x,
+                           int T, const int32_t* indices, const double* raw,
+                           const double* fraction, void* out);
+/* route + drop + forward in one launch sequence (no host sync unless stats
+ * is non-NULL).  The timed hot path. */
+int dsmoe_b200_forward(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
+                       const dsmoe_b200_policy* policy, int logits_mode, void* out,
+                       dsmoe_b200_drop_stats_t* stats);
+
+/* drop_stats from host fraction arrays (n = T*K*P doubles each). */
+int dsmoe_b200_drop_stats(const double* pre_fraction, const double* post_fraction, long n,
+                          int replay_factor, int num_shared, long num_tokens, int d_model,
+                          int d_ffn, dsmoe_b200_drop_stats_t* out);
+
+/* ---- offline partition + reconstruction (north-star item 1) ------------- */
+/* profile_importance: x (device, T x d, layer dtype), indices (device, T x K,
+ * an unsplit layer's routing); values (device, E x d_ffn doubles). */
+int dsmoe_b200_profile_importance(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x,
+                                  int T, const int32_t* indices, int metric, double* values);
+/* reconstruct_experts: stable descending order of each expert's importance
+ * (order: device, E x d_ffn int32, optional), then a new layer with P = 2
+ * (major = first ceil(d_ffn/2) neurons of the order). */
+int dsmoe_b200_reconstruct(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const double* values,
+                           int32_t* order, dsmoe_b200_layer** out);
+
+/* ---- expert parallelism policy (ep_sim.hpp) ----------------------------- */
+/* host arrays; same arithmetic as load_aware_thresholds (ep_sim.hpp:76-89) */
+int dsmoe_b200_load_aware_thresholds(const double* loads, int devices, double t_max, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSMOE_B200_H */

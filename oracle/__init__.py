@@ -232,6 +232,41 @@ def route_from_logits(logits, K, P=1, kind="none", t_drop=0.0, t_major=None, t_m
                    pre.reshape(sh), K, P)
 
 
+def topk(scores, K):
+    """topk_route (moe.hpp:181-206) restated: (idx int32 T x K, raw f64 T x K)."""
+    scores = np.ascontiguousarray(scores, np.float32)
+    T, E = scores.shape
+    idx = np.empty((T, K), np.int32)
+    raw = np.empty((T, K), np.float64)
+    L = lib()
+    L.orc_topk.argtypes = [f32p, C.c_int, C.c_int, C.c_int, i32p, f64p]
+    _chk(L.orc_topk(scores, T, E, K, idx, raw))
+    return idx, raw
+
+
+def normalize(raw, K, P=1):
+    """normalize_topk (dropping.hpp:60-72) on copy-major T x K*P raw scores."""
+    raw = np.ascontiguousarray(raw, np.float64)
+    T = raw.shape[0]
+    out = np.empty_like(raw)
+    L = lib()
+    L.orc_normalize.argtypes = [f64p, C.c_int, C.c_int, C.c_int, f64p]
+    _chk(L.orc_normalize(raw, T, K, P, out))
+    return out
+
+
+def apply_bands(norm, K, P, t_major, t_minor, keep_top1=True):
+    """apply_bands_fn (dropping.hpp:93-122) on copy-major T x K*P scores."""
+    norm = np.ascontiguousarray(norm, np.float64)
+    T = norm.shape[0]
+    frac = np.ones_like(norm)
+    L = lib()
+    L.orc_apply_bands.argtypes = [f64p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p,
+                                  C.c_void_p, C.c_int, f64p]
+    L.orc_apply_bands(norm, T, K, P, t_major, t_minor, None, None, int(keep_top1), frac)
+    return frac
+
+
 def drop_stats(pre_frac, post_frac, P, S, T, d, ffn) -> dict:
     pre = np.ascontiguousarray(pre_frac, np.float64).ravel()
     post = np.ascontiguousarray(post_frac, np.float64).ravel()

@@ -109,55 +109,52 @@ static inline float swishf(float x) { return x / (1.0f + expf(-x)); } /* matrix.
 
 /* ------------------------------------------------------- moe.hpp / dropping */
 
-int orc_route_from_logits(const float* logits, int T, int E, int K, int P, int kind, double t_drop,
-                          double t_major, double t_minor, int keep_top1, int normalize,
-                          const double* t_major_slot, const double* t_minor_slot, int32_t* idx,
-                          double* raw, double* norm, double* frac, double* pre_frac) {
-  if (K < 1 || K > E) return ST_INVALID_ARGUMENT; /* moe.hpp:182-184 */
-  if (P < 1) return ST_INVALID_ARGUMENT;
-  if (kind == ORC_2T) {
-    if (!(t_major <= t_minor)) return ST_INVALID_ARGUMENT; /* dropping.hpp:145-146 */
-    if (P != 2) return ST_INVALID_STATE;                   /* dropping.hpp:147-148 */
+/* topk_route, moe.hpp:181-206: K argmax rounds, strict >, lower index wins
+ * ties; raw = (double)score.  scores is one row of E floats. */
+static void topk_row(const float* row, int E, int K, char* taken, int32_t* sel, double* sraw) {
+  memset(taken, 0, (size_t)E);
+  for (int j = 0; j < K; ++j) {
+    int best = -1;
+    for (int e = 0; e < E; ++e)
+      if (!taken[e] && (best < 0 || row[e] > row[best])) best = e;
+    taken[best] = 1;
+    sel[j] = best;
+    sraw[j] = (double)row[best];
   }
-  if (kind == ORC_1T) t_major = t_minor = t_drop; /* drop_1t, dropping.hpp:136 */
-  const int k = K * P;
-  float* row = (float*)malloc(sizeof(float) * (size_t)E);
+}
+
+int orc_topk(const float* scores, int T, int E, int K, int32_t* idx, double* raw) {
+  if (K < 1 || K > E) return ST_INVALID_ARGUMENT; /* moe.hpp:182-184 */
   char* taken = (char*)malloc((size_t)E);
-  int32_t* sel = (int32_t*)malloc(sizeof(int32_t) * (size_t)K);
-  double* sraw = (double*)malloc(sizeof(double) * (size_t)K);
-  int st = ST_OK;
-  for (int t = 0; t < T && st == ST_OK; ++t) {
-    memcpy(row, logits + (size_t)t * E, sizeof(float) * (size_t)E);
-    softmax_row(row, E);
-    /* topk_route, moe.hpp:193-205: strict >, lower index wins ties */
-    memset(taken, 0, (size_t)E);
-    for (int j = 0; j < K; ++j) {
-      int best = -1;
-      for (int e = 0; e < E; ++e)
-        if (!taken[e] && (best < 0 || row[e] > row[best])) best = e;
-      taken[best] = 1;
-      sel[j] = best;
-      sraw[j] = (double)row[best];
-    }
-    /* normalize_topk, dropping.hpp:60-72 (sum over base_k in slot order) */
+  for (int t = 0; t < T; ++t)
+    topk_row(scores + (size_t)t * E, E, K, taken, idx + (size_t)t * K, raw + (size_t)t * K);
+  free(taken);
+  return ST_OK;
+}
+
+/* normalize_topk, dropping.hpp:60-72: per token, sum of the first base_k raw
+ * scores in slot order (double), then raw/sum for all K*P slots. */
+int orc_normalize(const double* raw, int T, int K, int P, double* norm) {
+  const int k = K * P;
+  for (int t = 0; t < T; ++t) {
+    const double* r = raw + (size_t)t * k;
     double sum = 0.0;
-    if (normalize) {
-      for (int j = 0; j < K; ++j) sum += sraw[j];
-      if (!(sum > 0.0)) { st = ST_INVALID_ARGUMENT; break; }
-    }
-    /* replay_routing, moe.hpp:296-307: copy-major positions cp*K + s */
+    for (int j = 0; j < K; ++j) sum += r[j];
+    if (!(sum > 0.0)) return ST_INVALID_ARGUMENT;
+    for (int j = 0; j < k; ++j) norm[(size_t)t * k + j] = r[j] / sum;
+  }
+  return ST_OK;
+}
+
+/* apply_bands_fn, dropping.hpp:93-122, on copy-major T x K*P normalized
+ * scores.  Thresholds per original selection when the *_slot arrays are
+ * given (ep_sim.hpp:139-149), else the scalars. */
+void orc_apply_bands(const double* norm, int T, int K, int P, double t_major, double t_minor,
+                     const double* t_major_slot, const double* t_minor_slot, int keep_top1,
+                     double* frac) {
+  const int k = K * P;
+  for (int t = 0; t < T; ++t) {
     const size_t base = (size_t)t * k;
-    for (int cp = 0; cp < P; ++cp)
-      for (int s = 0; s < K; ++s) {
-        const size_t f = base + (size_t)cp * K + s;
-        idx[f] = sel[s] * P + cp;
-        raw[f] = sraw[s];
-        norm[f] = normalize ? sraw[s] / sum : sraw[s];
-        frac[f] = 1.0;
-        if (pre_frac) pre_frac[f] = 1.0;
-      }
-    if (kind == ORC_NONE) continue;
-    /* apply_bands_fn, dropping.hpp:93-122 */
     int top_slot = 0;
     for (int s = 0; s < K; ++s) {
       const double ns = norm[base + s];
@@ -180,11 +177,55 @@ int orc_route_from_logits(const float* logits, int T, int E, int K, int P, int k
     if (keep_top1)
       for (int cp = 0; cp < P; ++cp) frac[base + (size_t)cp * K + top_slot] = 1.0;
   }
+}
+
+/* Routing on caller logits = the routing half of route_and_drop
+ * (dropping.hpp:248-258): softmax_inplace per row, topk_route, replay_routing
+ * (moe.hpp:277-309, copy-major cp*K+s, index e*P+cp), ensure_normalized,
+ * drop_1t / drop_2t. */
+int orc_route_from_logits(const float* logits, int T, int E, int K, int P, int kind, double t_drop,
+                          double t_major, double t_minor, int keep_top1, int normalize,
+                          const double* t_major_slot, const double* t_minor_slot, int32_t* idx,
+                          double* raw, double* norm, double* frac, double* pre_frac) {
+  if (K < 1 || K > E) return ST_INVALID_ARGUMENT; /* moe.hpp:182-184 */
+  if (P < 1) return ST_INVALID_ARGUMENT;
+  if (kind == ORC_2T) {
+    if (!(t_major <= t_minor)) return ST_INVALID_ARGUMENT; /* dropping.hpp:145-146 */
+    if (P != 2) return ST_INVALID_STATE;                   /* dropping.hpp:147-148 */
+  }
+  if (kind == ORC_1T) t_major = t_minor = t_drop; /* drop_1t, dropping.hpp:136 */
+  const int k = K * P;
+  float* row = (float*)malloc(sizeof(float) * (size_t)E);
+  char* taken = (char*)malloc((size_t)E);
+  int32_t* sel = (int32_t*)malloc(sizeof(int32_t) * (size_t)K);
+  double* sraw = (double*)malloc(sizeof(double) * (size_t)K);
+  for (int t = 0; t < T; ++t) {
+    memcpy(row, logits + (size_t)t * E, sizeof(float) * (size_t)E);
+    softmax_row(row, E);
+    topk_row(row, E, K, taken, sel, sraw);
+    const size_t base = (size_t)t * k;
+    for (int cp = 0; cp < P; ++cp)
+      for (int s = 0; s < K; ++s) {
+        const size_t f = base + (size_t)cp * K + s;
+        idx[f] = sel[s] * P + cp;
+        raw[f] = sraw[s];
+        frac[f] = 1.0;
+        if (pre_frac) pre_frac[f] = 1.0;
+      }
+  }
   free(row);
   free(taken);
   free(sel);
   free(sraw);
-  return st;
+  int st = ST_OK;
+  if (normalize) {
+    st = orc_normalize(raw, T, K, P, norm);
+  } else {
+    memcpy(norm, raw, sizeof(double) * (size_t)T * k);
+  }
+  if (st != ST_OK || kind == ORC_NONE) return st;
+  orc_apply_bands(norm, T, K, P, t_major, t_minor, t_major_slot, t_minor_slot, keep_top1, frac);
+  return ST_OK;
 }
 
 void orc_drop_stats(const double* pre_frac, const double* post_frac, int64_t n, int P, int S,

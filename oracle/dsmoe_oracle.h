@@ -37,6 +37,15 @@ void orc_gate_logits(const float* x, const float* gate, int T, int d, int E, flo
 /* softmax_inplace (matrix.hpp:68-78) on each row of s. */
 void orc_softmax_rows(float* s, int T, int E);
 
+/* topk_route (moe.hpp:181-206) on T x E scores -> T x K. */
+int orc_topk(const float* scores, int T, int E, int K, int32_t* idx, double* raw);
+/* normalize_topk (dropping.hpp:60-72) on copy-major T x K*P raw scores. */
+int orc_normalize(const double* raw, int T, int K, int P, double* norm);
+/* apply_bands_fn (dropping.hpp:93-122) on copy-major T x K*P normalized scores. */
+void orc_apply_bands(const double* norm, int T, int K, int P, double t_major, double t_minor,
+                     const double* t_major_slot, const double* t_minor_slot, int keep_top1,
+                     double* frac);
+
 /* Routing on caller logits: softmax, topk_route (moe.hpp:181), replay_routing
  * (moe.hpp:277), ensure_normalized (dropping.hpp:75), drop_1t/drop_2t
  * (dropping.hpp:133/141).  Arrays are T*K*P in copy-major slot order.

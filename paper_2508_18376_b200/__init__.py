@@ -1,0 +1,11 @@
+"""B200-native DualSparse-MoE MoE-module forward (arxiv 2508.18376).
+
+The compute path is libdsmoe_b200.so (CUDA for sm_100a, C ABI in
+include/dsmoe_b200.h); dsmoe.py mirrors the reference's C++ partition /
+drop-policy / forward API on top of it; ep.py runs expert parallelism over
+torch.distributed (NCCL).
+"""
+from .dsmoe import (  # noqa: F401
+    DropPolicy, DsmoeError, MoeLayer, Context, RoutingDecision, route_and_drop, moe_forward, forward,
+    drop_stats, load_aware_thresholds, place_experts, lib, last_launch_count, LOGITS_TENSOR, LOGITS_EXACT,
+)

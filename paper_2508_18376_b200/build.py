@@ -1,0 +1,72 @@
+"""Build libdsmoe_b200.so in-tree with nvcc for sm_100a.
+
+    python -m paper_2508_18376_b200.build        (or __graft_entry__.build())
+
+Each .cu / .cpp under csrc/ is compiled to an object in build/ (parallel),
+then linked into paper_2508_18376_b200/libdsmoe_b200.so with the CUDA runtime
+linked statically.  The router translation unit is compiled with -fmad=false
+so its float/double arithmetic rounds exactly like the reference's
+(-ffp-contract=off, /root/reference/proj/CMakeLists.txt:8).
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(os.path.dirname(HERE), "build", "dsmoe_b200")
+LIB = os.path.join(HERE, "libdsmoe_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+          "-I" + CSRC, "-I" + os.path.join(os.path.dirname(HERE), "include")]
+PER_FILE = {"router.cu": ["-fmad=false"]}
+
+
+def sources():
+    return sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
+
+
+def _obj(src):
+    return os.path.join(BUILD, src + ".o")
+
+
+def _deps_mtime():
+    return max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC)) if os.path.isdir(CSRC) else 0
+
+
+def _compile(src, verbose=False):
+    out = _obj(src)
+    cmd = [NVCC, *ARCH, *COMMON, *PER_FILE.get(src, []), "-c", os.path.join(CSRC, src), "-o", out]
+    if src.endswith(".cu"):
+        cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    return r.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    newest = max(_deps_mtime(), os.path.getmtime(os.path.join(os.path.dirname(HERE), "include", "dsmoe_b200.h")))
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
+        return LIB
+    srcs = sources()
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        logs = list(ex.map(lambda s: _compile(s, verbose), srcs))
+    if verbose:
+        for s, l in zip(srcs, logs):
+            if l.strip():
+                print(f"--- {s}\n{l}", file=sys.stderr)
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *[_obj(s) for s in srcs]]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,911 @@
+// C ABI of libdsmoe_b200.so (include/dsmoe_b200.h) and the C++ host runtime
+// behind it: layer packing, workspace management, tensor-map encoding and the
+// launch sequence of the MoE-module forward.  Error convention follows the
+// reference C ABI (/root/reference/proj/src/capi.cpp:35-58): status codes,
+// thread-local message, nothing thrown across the boundary.
+#include "../../include/dsmoe_b200.h"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace {
+
+using namespace dsb;
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
+void require(bool ok, int code, const std::string& msg) {
+  if (!ok) fail(code, msg);
+}
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(DSMOE_E_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void launch_check(int rc, const char* what) {
+  if (rc == -1) fail(DSMOE_E_INVALID_ARGUMENT, std::string(what) + ": unsupported shape");
+  if (rc != 0) {
+    const cudaError_t e = cudaGetLastError();
+    fail(DSMOE_E_INTERNAL, std::string(what) + ": launch failed: " + cudaGetErrorString(e));
+  }
+}
+
+thread_local std::string g_last_error;
+thread_local int g_launches = 0;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return DSMOE_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of memory";
+    return DSMOE_E_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return DSMOE_E_INTERNAL;
+  }
+}
+
+// --------------------------------------------------------------- helpers
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  // grow-only allocation; contents are not preserved
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    release();
+    cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+    bytes = n;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+int esize(int dt) { return dt == DSMOE_B200_BF16 ? 2 : 4; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  require(fn != nullptr, DSMOE_E_INTERNAL, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D bf16 tensor map: `rows` x `cols` (row stride `ld` elements), box
+// 64 columns x box_rows rows, 128-byte swizzle (the UMMA descriptor layout).
+CUtensorMap make_map(const void* base, long long rows, long long cols, long long ld, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, DSMOE_E_INTERNAL,
+          "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  }
+  return n;
+}
+
+}  // namespace
+
+// ==================================================================== layer
+struct dsmoe_b200_layer {
+  int d = 0, ffn = 0, E = 0, K = 0, S = 0, P = 1, prenorm = 0, dtype = DSMOE_B200_BF16;
+  std::vector<int> widths, swidths;
+  std::vector<UnitInfo> units;  // E routed units then S shared units
+  int hstride = 0;
+  long long w13_rows = 0;
+  int Epad = 0;  // gate rows padded to 32 (UMMA N of the gate GEMM)
+  int max_chunks = 0;
+  DevBuf w13, w2t, gateT, gate_exact, d_units;
+  CUtensorMap map_w13{}, map_w2t{}, map_gate{};
+  std::vector<char> block_set, shared_set;
+  bool gate_set = false;
+
+  int nunits() const { return E + S; }
+  // sub-block p of routed unit e <- block (e, p) columns [col0, col0 + n)
+  void check_ready() const {
+    require(gate_set, DSMOE_E_INVALID_STATE, "layer: gate weights not set");
+    for (size_t b = 0; b < block_set.size(); ++b)
+      require(block_set[b], DSMOE_E_INVALID_STATE, "layer: expert block " + std::to_string(b) + " not set");
+    for (size_t s = 0; s < shared_set.size(); ++s)
+      require(shared_set[s], DSMOE_E_INVALID_STATE, "layer: shared expert " + std::to_string(s) + " not set");
+  }
+};
+
+namespace {
+
+void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c) {
+  require(c.d_model >= 1, DSMOE_E_INVALID_ARGUMENT, "config: d_model must be >= 1");
+  require(c.d_ffn >= 2, DSMOE_E_INVALID_ARGUMENT, "config: d_ffn must be >= 2");
+  require(c.num_experts >= 1, DSMOE_E_INVALID_ARGUMENT, "config: num_experts must be >= 1");
+  require(c.top_k >= 1 && c.top_k <= c.num_experts, DSMOE_E_INVALID_ARGUMENT,
+          "config: top_k must satisfy 1 <= K <= E");
+  require(c.num_shared_experts >= 0, DSMOE_E_INVALID_ARGUMENT, "config: num_shared_experts must be >= 0");
+  require(c.replay_factor >= 1 && c.replay_factor <= kMaxSub, DSMOE_E_INVALID_STATE,
+          "layer: replay_factor must be in [1, 8]");
+  require(c.dtype == DSMOE_B200_F32 || c.dtype == DSMOE_B200_BF16, DSMOE_E_INVALID_ARGUMENT,
+          "layer: dtype must be f32 or bf16");
+  require(c.d_model % 64 == 0, DSMOE_E_SHAPE_MISMATCH, "layer: d_model must be a multiple of 64 on device");
+  require(c.num_experts <= 256, DSMOE_E_INVALID_ARGUMENT, "layer: at most 256 experts on device");
+  require(c.top_k <= 16, DSMOE_E_INVALID_ARGUMENT, "layer: top_k must be <= 16 on device");
+  L->d = c.d_model;
+  L->ffn = c.d_ffn;
+  L->E = c.num_experts;
+  L->K = c.top_k;
+  L->S = c.num_shared_experts;
+  L->P = c.replay_factor;
+  L->prenorm = c.gate_prenormalized != 0;
+  L->dtype = c.dtype;
+  const int P = L->P;
+  for (int b = 0; b < L->E * P; ++b) L->widths.push_back(c.block_widths ? c.block_widths[b] : c.d_ffn / P);
+  for (int s = 0; s < L->S; ++s) L->swidths.push_back(c.shared_widths ? c.shared_widths[s] : c.d_ffn);
+  for (int e = 0; e < L->E; ++e) {
+    int tot = 0;
+    for (int p = 0; p < P; ++p) {
+      require(L->widths[e * P + p] >= 1, DSMOE_E_SHAPE_MISMATCH, "layer: block widths must be >= 1");
+      tot += L->widths[e * P + p];
+    }
+    require(tot == L->ffn, DSMOE_E_INVALID_STATE,
+            "layer: block widths of expert " + std::to_string(e) + " sum to " + std::to_string(tot) +
+                ", expected " + std::to_string(L->ffn));
+  }
+  long long row = 0;
+  int hmax = 0, chmax = 0;
+  for (int e = 0; e < L->E + L->S; ++e) {
+    UnitInfo u{};
+    const bool sh = e >= L->E;
+    std::vector<int> w;
+    if (sh) {
+      w = {L->swidths[e - L->E]};
+    } else if (P == 1) {
+      // virtual split at ceil(w/2): fraction 0.5 evaluates the first half
+      // (moe.hpp:264), i.e. sub-block 0; the routed layer needs no copy.
+      const int wd = L->widths[e], h0 = (wd + 1) / 2;
+      w = {h0};
+      if (wd - h0 > 0) w.push_back(wd - h0);
+    } else {
+      for (int p = 0; p < P; ++p) w.push_back(L->widths[e * P + p]);
+    }
+    u.nsub = static_cast<int>(w.size());
+    u.hwidth = 0;
+    int chunks = 0;
+    for (int p = 0; p < u.nsub; ++p) {
+      u.sub_w[p] = w[p];
+      u.sub_wpad[p] = round_up(w[p], 64);
+      u.hwidth += u.sub_wpad[p];
+      chunks += (u.sub_wpad[p] + kChunk - 1) / kChunk;
+    }
+    u.w13_row = static_cast<int>(row);
+    u.w2t_row = e * L->d;
+    u.shared = sh ? 1 : 0;
+    row += 2LL * u.hwidth;
+    hmax = std::max(hmax, u.hwidth);
+    chmax = std::max(chmax, chunks);
+    L->units.push_back(u);
+  }
+  require(row < (1LL << 31) && static_cast<long long>(L->E + L->S) * L->d < (1LL << 31),
+          DSMOE_E_INVALID_ARGUMENT, "layer: packed weights exceed 2^31 rows");
+  L->w13_rows = row;
+  L->hstride = hmax;
+  L->max_chunks = chmax;
+  L->Epad = round_up(L->E, 32);
+  const int es = esize(L->dtype);
+  L->w13.ensure(static_cast<size_t>(row) * L->d * es);
+  L->w2t.ensure(static_cast<size_t>(L->E + L->S) * L->d * L->hstride * es);
+  L->gateT.ensure(static_cast<size_t>(L->Epad) * L->d * es);
+  L->gate_exact.ensure(static_cast<size_t>(L->d) * L->E * 4);
+  cuda_check(cudaMemset(L->w13.p, 0, L->w13.bytes), "memset");
+  cuda_check(cudaMemset(L->w2t.p, 0, L->w2t.bytes), "memset");
+  cuda_check(cudaMemset(L->gateT.p, 0, L->gateT.bytes), "memset");
+  L->d_units.ensure(sizeof(UnitInfo) * L->units.size());
+  cuda_check(cudaMemcpy(L->d_units.p, L->units.data(), sizeof(UnitInfo) * L->units.size(),
+                        cudaMemcpyHostToDevice),
+             "upload units");
+  if (L->dtype == DSMOE_B200_BF16) {
+    L->map_w13 = make_map(L->w13.p, row, L->d, L->d, 256);
+    L->map_w2t = make_map(L->w2t.p, static_cast<long long>(L->E + L->S) * L->d, L->hstride, L->hstride, 256);
+    L->map_gate = make_map(L->gateT.p, L->Epad, L->d, L->d, L->Epad);
+  }
+  L->block_set.assign(static_cast<size_t>(L->E * P), 0);
+  L->shared_set.assign(static_cast<size_t>(L->S), 0);
+}
+
+// Source staging: host sources are copied to a temporary device buffer.
+struct Staged {
+  DevBuf buf;
+  const void* p = nullptr;
+  Staged(const void* src, size_t bytes, int on_device, cudaStream_t s) {
+    if (on_device) {
+      p = src;
+    } else {
+      buf.ensure(bytes);
+      cuda_check(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, s), "stage H2D");
+      p = buf.p;
+    }
+  }
+};
+
+// Pack sub-block p of unit u from a source block (w1/w3: d x ld, w2: ld x d);
+// neurons [col0, col0 + n) of the source, optionally through `order`.
+void pack_sub(dsmoe_b200_layer* L, int u, int p, const void* w1, const void* w3, const void* w2, int ld,
+              const int* order, int col0, int src_dt, cudaStream_t s) {
+  const UnitInfo& ui = L->units[u];
+  long long base = ui.w13_row;
+  int hcol = 0;
+  for (int q = 0; q < p; ++q) {
+    base += 2LL * ui.sub_wpad[q];
+    hcol += ui.sub_wpad[q];
+  }
+  launch_check(launch_pack_w13(src_dt, L->dtype, w1, w3, L->d, ld, order, col0, ui.sub_w[p], L->w13.p, base,
+                               ui.sub_wpad[p], s),
+               "pack_w13");
+  launch_check(launch_pack_w2t(src_dt, L->dtype, w2, L->d, order, col0, ui.sub_w[p], L->w2t.p,
+                               ui.w2t_row, hcol, L->hstride, s),
+               "pack_w2t");
+}
+
+}  // namespace
+
+// ====================================================================== ctx
+struct dsmoe_b200_ctx {
+  cudaStream_t stream = nullptr;
+  DevBuf logits, sel_code, sel_raw, slot_pos, cnt, counters, row_token, row_scale, seg, scalars;
+  DevBuf tiles1, tiles2, tiles_gate, xperm, H, Y, frac_ws;
+  int gate_tiles_T = -1, gate_tiles_Epad = -1, gate_tiles_d = -1;
+  long long scale_fill_key = -1;
+  unsigned long long last_err_flags = 0;
+  // optional per-stage CUDA-event timing (bench.py): 0 gate, 1 router,
+  // 2 permute+plan, 3 gather, 4 gemm1, 5 gemm2, 6 combine
+  static constexpr int kStages = 7;
+  bool profiling = false;
+  cudaEvent_t ev[kStages + 1] = {};
+  bool ev_hit[kStages + 1] = {};
+  double prof_ms[kStages] = {};
+  long prof_calls = 0;
+  void mark(int i) {
+    if (!profiling) return;
+    cuda_check(cudaEventRecord(ev[i], stream), "event");
+    ev_hit[i] = true;
+  }
+  void prof_begin() {
+    if (!profiling) return;
+    for (auto& h : ev_hit) h = false;
+  }
+  void prof_end() {
+    if (!profiling) return;
+    mark(kStages);
+    cuda_check(cudaEventSynchronize(ev[kStages]), "event sync");
+    int prev = -1;
+    for (int i = 0; i <= kStages; ++i) {
+      if (!ev_hit[i]) continue;
+      if (prev >= 0) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, ev[prev], ev[i]), "elapsed");
+        prof_ms[prev] += ms;
+      }
+      prev = i;
+    }
+    ++prof_calls;
+  }
+  ~dsmoe_b200_ctx() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+
+  // workspace for T tokens on layer L
+  void ensure(const dsmoe_b200_layer* L, int T) {
+    const int es = esize(L->dtype);
+    const long long TK = static_cast<long long>(T) * L->K;
+    const long long Rcap = TK;
+    const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
+    logits.ensure(static_cast<size_t>(T) * L->Epad * 4 + 16);
+    sel_code.ensure(static_cast<size_t>(TK) * 4 + 16);
+    sel_raw.ensure(static_cast<size_t>(TK) * 4 + 16);
+    slot_pos.ensure(static_cast<size_t>(TK) * 4 + 16);
+    cnt.ensure(static_cast<size_t>(2 * L->E) * 4);
+    counters.ensure(4 * sizeof(unsigned long long));
+    row_token.ensure(static_cast<size_t>(Rcap + kTileM) * 4);
+    seg.ensure(sizeof(UnitSeg) * L->E);
+    scalars.ensure(4 * sizeof(int));  // r_total, n1, n2, ngate
+    const long long mt = (Rcap + kTileM - 1) / kTileM + L->E;
+    const long long mts = static_cast<long long>(L->S) * ((T + kTileM - 1) / kTileM);
+    const long long t1 = (mt + mts) * L->max_chunks;
+    const long long t2 = (mt + mts) * ((L->d + kTileN2 - 1) / kTileN2);
+    tiles1.ensure(static_cast<size_t>(t1 + 1) * sizeof(GemmTile));
+    tiles2.ensure(static_cast<size_t>(t2 + 1) * sizeof(GemmTile));
+    xperm.ensure(static_cast<size_t>(Rcap + kTileM) * L->d * es);
+    H.ensure(static_cast<size_t>(rows) * L->hstride * es);
+    Y.ensure(static_cast<size_t>(rows) * L->d * es);
+    const size_t rs_bytes = static_cast<size_t>(rows) * 4;
+    if (row_scale.bytes < rs_bytes) {
+      row_scale.ensure(rs_bytes);
+      scale_fill_key = -1;
+    }
+    // shared-expert rows are weighted 1 (moe.hpp:267-268)
+    const long long key = (Rcap << 20) ^ (static_cast<long long>(L->S) * T);
+    if (L->S > 0 && scale_fill_key != key) {
+      launch_check(launch_fill_f32(row_scale.as<float>() + Rcap, 1.0f, static_cast<long long>(L->S) * T, stream),
+                   "fill");
+      ++g_launches;
+      scale_fill_key = key;
+    }
+  }
+  long long max_tiles1(const dsmoe_b200_layer* L, int T) const {
+    const long long Rcap = static_cast<long long>(T) * L->K;
+    const long long mt = (Rcap + kTileM - 1) / kTileM + L->E;
+    const long long mts = static_cast<long long>(L->S) * ((T + kTileM - 1) / kTileM);
+    return (mt + mts) * L->max_chunks;
+  }
+  long long max_tiles2(const dsmoe_b200_layer* L, int T) const {
+    const long long Rcap = static_cast<long long>(T) * L->K;
+    const long long mt = (Rcap + kTileM - 1) / kTileM + L->E;
+    const long long mts = static_cast<long long>(L->S) * ((T + kTileM - 1) / kTileM);
+    return (mt + mts) * ((L->d + kTileN2 - 1) / kTileN2);
+  }
+};
+
+namespace {
+
+struct PolicyResolved {
+  int kind = 0;
+  double t_drop = 0, t_major = 0, t_minor = 0;
+  int keep_top1 = 1, normalize = 1;
+  const double* t_unit = nullptr;
+  double maj_off = 0, min_off = 0;
+};
+
+PolicyResolved resolve_policy(const dsmoe_b200_layer* L, const dsmoe_b200_policy* p) {
+  PolicyResolved r;
+  r.normalize = !L->prenorm;
+  if (!p) return r;
+  require(p->kind >= 0 && p->kind <= 2, DSMOE_E_INVALID_ARGUMENT, "policy: kind must be none, 1t or 2t");
+  r.kind = p->kind;
+  r.t_drop = p->t_drop;
+  r.keep_top1 = p->keep_top1 != 0;
+  if (p->normalize >= 0) r.normalize = p->normalize != 0;
+  if (r.kind == DSMOE_B200_DROP_1T) {
+    r.t_major = r.t_minor = p->t_drop;  // drop_1t (dropping.hpp:133-138)
+  } else if (r.kind == DSMOE_B200_DROP_2T) {
+    require(p->t_major <= p->t_minor, DSMOE_E_INVALID_ARGUMENT, "drop policy: t_major must be <= t_minor");
+    // drop_2t (dropping.hpp:147-148) / map_from_layer (:233-234)
+    require(L->P == 2, DSMOE_E_INVALID_STATE, "drop_2t: routing must be replayed with P=2");
+    r.t_major = p->t_major;
+    r.t_minor = p->t_minor;
+  }
+  r.t_unit = p->t_unit;
+  if (r.kind == DSMOE_B200_DROP_2T) {  // ep_sim.hpp:139-142
+    r.maj_off = p->t_major - p->t_drop;
+    r.min_off = p->t_minor - p->t_drop;
+  }
+  return r;
+}
+
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// drop_stats (dropping.hpp:171-195) from retained-copy counts.  With P a
+// power of two every partial sum of fraction/P is exact, so the counts give
+// the reference's sequential sums bit for bit.
+void stats_from_counts(const dsmoe_b200_layer* L, int T, unsigned long long n1, unsigned long long nh,
+                       const uint8_t* frac_host, dsmoe_b200_drop_stats_t* st) {
+  const long long n = static_cast<long long>(T) * L->K * L->P;
+  const double w = 1.0 / L->P;
+  double total = 0.0, retained = 0.0;
+  if (is_pow2(L->P)) {
+    total = static_cast<double>(n) * w;
+    retained = static_cast<double>(2 * n1 + nh) * (0.5 * w);
+  } else {
+    for (long long i = 0; i < n; ++i) {
+      total += 1.0 * w;
+      const double f = frac_host[i] == 2 ? 1.0 : (frac_host[i] == 1 ? 0.5 : 0.0);
+      retained += f * w;
+    }
+  }
+  st->num_tokens = T;
+  st->total_routed_units = total;
+  st->dropped_units = total - retained;
+  st->shared_units = static_cast<double>(L->S) * T;
+  const double denom = st->total_routed_units + st->shared_units;
+  st->drop_rate = denom > 0.0 ? st->dropped_units / denom : 0.0;
+  const double unit = 6.0 * L->d * L->ffn;
+  st->total_flops = denom * unit;
+  st->saved_flops = st->dropped_units * unit;
+  st->retained_flops = st->total_flops - st->saved_flops;
+}
+
+void check_flags(dsmoe_b200_ctx* C) {
+  unsigned long long h[4];
+  cuda_check(cudaMemcpyAsync(h, C->counters.p, sizeof(h), cudaMemcpyDeviceToHost, C->stream), "D2H");
+  cuda_check(cudaStreamSynchronize(C->stream), "sync");
+  const unsigned long long f = h[2] | C->last_err_flags;
+  C->last_err_flags = 0;
+  if (f & 1ull) fail(DSMOE_E_INVALID_ARGUMENT, "normalize_topk: degenerate zero-sum scores");
+  if (f & 4ull)
+    fail(DSMOE_E_INVALID_STATE,
+         "moe_forward: routing is not in the canonical replayed layout the device path supports");
+}
+
+// -------------------------------------------------- stage: gate logits + K1
+void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                 const PolicyResolved& pol, int logits_mode, const float* logits_in, float* logits_out,
+                 const dsmoe_b200_routing* out, uint8_t* frac_ws) {
+  cudaStream_t s = C->stream;
+  cuda_check(cudaMemsetAsync(C->cnt.p, 0, 2 * L->E * sizeof(int), s), "memset");
+  cuda_check(cudaMemsetAsync(C->counters.p, 0, 4 * sizeof(unsigned long long), s), "memset");
+  const float* lg = logits_in;
+  int ld = L->E;
+  C->mark(0);
+  if (!lg) {
+    const bool tc = logits_mode == DSMOE_B200_LOGITS_TENSOR && L->dtype == DSMOE_B200_BF16;
+    if (tc) {
+      if (C->gate_tiles_T != T || C->gate_tiles_Epad != L->Epad || C->gate_tiles_d != L->d) {
+        const int nt = (T + kTileM - 1) / kTileM;
+        std::vector<GemmTile> tl(static_cast<size_t>(nt));
+        for (int m = 0; m < nt; ++m)
+          tl[m] = GemmTile{m * kTileM, 0, m * kTileM, 0, L->d / kTileK, L->Epad, std::min(kTileM, T - m * kTileM), 0};
+        C->tiles_gate.ensure(sizeof(GemmTile) * (nt + 1) + 16);
+        cuda_check(cudaMemcpyAsync(C->tiles_gate.p, tl.data(), sizeof(GemmTile) * nt, cudaMemcpyHostToDevice, s), "H2D");
+        int* ng = C->scalars.as<int>() + 3;
+        cuda_check(cudaMemcpyAsync(ng, &nt, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        C->gate_tiles_T = T;
+        C->gate_tiles_Epad = L->Epad;
+        C->gate_tiles_d = L->d;
+      }
+      const CUtensorMap mx = make_map(x, T, L->d, L->d, kTileM);
+      launch_check(launch_gemm_tc(0, &mx, &mx, &L->map_gate, C->tiles_gate.as<GemmTile>(),
+                                  C->scalars.as<int>() + 3, (T + kTileM - 1) / kTileM, C->logits.p, L->Epad,
+                                  nullptr, L->Epad, num_sms(), s),
+                   "gate gemm");
+      ld = L->Epad;
+    } else {
+      launch_check(launch_gate_logits_exact(x, L->dtype == DSMOE_B200_BF16, L->gate_exact.as<float>(),
+                                            C->logits.as<float>(), T, L->d, L->E, s),
+                   "gate logits");
+    }
+    ++g_launches;
+    lg = C->logits.as<float>();
+  }
+  if (logits_out && logits_out != lg) {
+    cuda_check(cudaMemcpy2DAsync(logits_out, L->E * 4, lg, ld * 4, L->E * 4, T, cudaMemcpyDeviceToDevice, s),
+               "logits copy");
+  }
+  C->mark(1);
+  RouterArgs a{};
+  a.logits = lg;
+  a.ld_logits = ld;
+  a.T = T;
+  a.E = L->E;
+  a.K = L->K;
+  a.P = L->P;
+  a.kind = pol.kind;
+  a.t_major = pol.t_major;
+  a.t_minor = pol.t_minor;
+  a.keep_top1 = pol.keep_top1;
+  a.normalize = pol.normalize;
+  a.t_unit = pol.t_unit;
+  a.maj_off = pol.maj_off;
+  a.min_off = pol.min_off;
+  if (out) {
+    a.idx = out->indices;
+    a.raw = out->raw;
+    a.norm = out->normalized;
+    a.frac = out->fraction;
+  }
+  if (!a.frac && frac_ws) a.frac = frac_ws;
+  a.sel_code = C->sel_code.as<int32_t>();
+  a.sel_raw = C->sel_raw.as<float>();
+  a.slot_pos = C->slot_pos.as<int32_t>();
+  a.cnt = C->cnt.as<int>();
+  a.counters = C->counters.as<unsigned long long>();
+  launch_check(launch_router(a, s), "router");
+  ++g_launches;
+}
+
+// ------------------------------------- stage: K2 permute/gather, K3, K4, K5
+void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T, void* out) {
+  cudaStream_t s = C->stream;
+  const int es = esize(L->dtype);
+  const long long Rcap = static_cast<long long>(T) * L->K;
+  int* r_total = C->scalars.as<int>();
+  int* n1 = r_total + 1;
+  int* n2 = r_total + 2;
+  C->mark(2);
+  launch_check(launch_permute(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), C->cnt.as<int>(), T, L->K, L->E,
+                              C->row_token.as<int32_t>(), C->row_scale.as<float>(), C->slot_pos.as<int32_t>(),
+                              C->seg.as<UnitSeg>(), r_total, s),
+               "permute");
+  PlanArgs pa{};
+  pa.units = L->d_units.as<UnitInfo>();
+  pa.seg_routed = C->seg.as<UnitSeg>();
+  pa.num_routed = L->E;
+  pa.num_shared = L->S;
+  pa.T = T;
+  pa.d = L->d;
+  pa.shared_row0 = static_cast<int>(Rcap);
+  pa.tiles1 = C->tiles1.as<GemmTile>();
+  pa.n1 = n1;
+  pa.tiles2 = C->tiles2.as<GemmTile>();
+  pa.n2 = n2;
+  launch_check(launch_plan(pa, s), "plan");
+  C->mark(3);
+  launch_check(launch_gather(x, C->xperm.p, C->row_token.as<int32_t>(), r_total, L->d * es, num_sms(), s), "gather");
+  g_launches += 3;
+  const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
+  const int mt1 = static_cast<int>(std::min<long long>(C->max_tiles1(L, T), 1 << 30));
+  const int mt2 = static_cast<int>(std::min<long long>(C->max_tiles2(L, T), 1 << 30));
+  if (L->dtype == DSMOE_B200_BF16) {
+    const CUtensorMap mx = make_map(x, T, L->d, L->d, kTileM);
+    const CUtensorMap mxp = make_map(C->xperm.p, Rcap + kTileM, L->d, L->d, kTileM);
+    const CUtensorMap mh = make_map(C->H.p, rows, L->hstride, L->hstride, kTileM);
+    C->mark(4);
+    launch_check(launch_gemm_tc(1, &mxp, &mx, &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
+                                nullptr, 256, num_sms(), s),
+                 "gemm1");
+    C->mark(5);
+    launch_check(launch_gemm_tc(2, &mh, &mh, &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, C->Y.p, L->d,
+                                C->row_scale.as<float>(), 256, num_sms(), s),
+                 "gemm2");
+  } else {
+    SimtArgs g1{};
+    g1.A = C->xperm.as<float>();
+    g1.A2 = static_cast<const float*>(x);
+    g1.lda = L->d;
+    g1.a_rows = Rcap + kTileM;
+    g1.a2_rows = T;
+    g1.B = L->w13.as<float>();
+    g1.ldb = L->d;
+    g1.tiles = C->tiles1.as<GemmTile>();
+    g1.num_tiles = n1;
+    g1.out = C->H.as<float>();
+    g1.ldo = L->hstride;
+    C->mark(4);
+    launch_check(launch_gemm_simt(1, g1, mt1, num_sms(), s), "gemm1 simt");
+    SimtArgs g2{};
+    g2.A = C->H.as<float>();
+    g2.A2 = C->H.as<float>();
+    g2.lda = L->hstride;
+    g2.a_rows = g2.a2_rows = rows;
+    g2.B = L->w2t.as<float>();
+    g2.ldb = L->hstride;
+    g2.tiles = C->tiles2.as<GemmTile>();
+    g2.num_tiles = n2;
+    g2.out = C->Y.as<float>();
+    g2.ldo = L->d;
+    g2.row_scale = C->row_scale.as<float>();
+    C->mark(5);
+    launch_check(launch_gemm_simt(2, g2, mt2, num_sms(), s), "gemm2 simt");
+  }
+  C->mark(6);
+  launch_check(launch_combine(C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d, L->K,
+                              L->S, static_cast<int>(Rcap), num_sms(), s),
+               "combine");
+  g_launches += 3;
+}
+
+void require_layer(const dsmoe_b200_layer* L) {
+  require(L != nullptr, DSMOE_E_INVALID_ARGUMENT, "null layer");
+  L->check_ready();
+}
+
+}  // namespace
+
+// ================================================================= C ABI
+extern "C" {
+
+const char* dsmoe_b200_version(void) { return "dsmoe_b200 0.1 (sm_100a)"; }
+const char* dsmoe_b200_last_error(void) { return g_last_error.c_str(); }
+int dsmoe_b200_last_launch_count(void) { return g_launches; }
+
+int dsmoe_b200_layer_create(const dsmoe_b200_layer_config* cfg, dsmoe_b200_layer** out) {
+  return guarded([&] {
+    require(cfg && out, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    auto* L = new dsmoe_b200_layer;
+    try {
+      layer_build(L, *cfg);
+    } catch (...) {
+      delete L;
+      throw;
+    }
+    *out = L;
+  });
+}
+
+void dsmoe_b200_layer_free(dsmoe_b200_layer* layer) { delete layer; }
+
+int dsmoe_b200_layer_info(const dsmoe_b200_layer* L, int32_t* o) {
+  return guarded([&] {
+    require(L && o, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    const int32_t v[8] = {L->d, L->ffn, L->E, L->K, L->S, L->P, L->dtype, L->prenorm};
+    std::memcpy(o, v, sizeof(v));
+  });
+}
+
+int dsmoe_b200_layer_set_gate(dsmoe_b200_layer* L, const void* gate, int src_dtype, int src_on_device,
+                              void* stream) {
+  return guarded([&] {
+    require(L && gate, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(src_dtype == 0 || src_dtype == 1, DSMOE_E_INVALID_ARGUMENT, "bad source dtype");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Staged g(gate, static_cast<size_t>(L->d) * L->E * esize(src_dtype), src_on_device, s);
+    launch_check(launch_pack_gate(src_dtype, L->dtype, g.p, L->d, L->E, L->gateT.p, L->gate_exact.as<float>(), s),
+                 "pack gate");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    L->gate_set = true;
+  });
+}
+
+int dsmoe_b200_layer_set_block(dsmoe_b200_layer* L, int b, const void* w1, const void* w3, const void* w2,
+                               int src_dtype, int src_on_device, void* stream) {
+  return guarded([&] {
+    require(L && w1 && w3 && w2, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(b >= 0 && b < L->E * L->P, DSMOE_E_INVALID_ARGUMENT, "block index out of range");
+    require(src_dtype == 0 || src_dtype == 1, DSMOE_E_INVALID_ARGUMENT, "bad source dtype");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int wd = L->widths[b];
+    const size_t nb = static_cast<size_t>(L->d) * wd * esize(src_dtype);
+    Staged a1(w1, nb, src_on_device, s), a3(w3, nb, src_on_device, s), a2(w2, nb, src_on_device, s);
+    const int e = b / L->P, p = b % L->P;
+    if (L->P == 1) {
+      const UnitInfo& u = L->units[e];
+      pack_sub(L, e, 0, a1.p, a3.p, a2.p, wd, nullptr, 0, src_dtype, s);
+      if (u.nsub > 1) pack_sub(L, e, 1, a1.p, a3.p, a2.p, wd, nullptr, u.sub_w[0], src_dtype, s);
+    } else {
+      pack_sub(L, e, p, a1.p, a3.p, a2.p, wd, nullptr, 0, src_dtype, s);
+    }
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    L->block_set[b] = 1;
+  });
+}
+
+int dsmoe_b200_layer_set_shared(dsmoe_b200_layer* L, int si, const void* w1, const void* w3, const void* w2,
+                                int src_dtype, int src_on_device, void* stream) {
+  return guarded([&] {
+    require(L && w1 && w3 && w2, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(si >= 0 && si < L->S, DSMOE_E_INVALID_ARGUMENT, "shared expert index out of range");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int wd = L->swidths[si];
+    const size_t nb = static_cast<size_t>(L->d) * wd * esize(src_dtype);
+    Staged a1(w1, nb, src_on_device, s), a3(w3, nb, src_on_device, s), a2(w2, nb, src_on_device, s);
+    pack_sub(L, L->E + si, 0, a1.p, a3.p, a2.p, wd, nullptr, 0, src_dtype, s);
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    L->shared_set[si] = 1;
+  });
+}
+
+int dsmoe_b200_ctx_create(void* stream, dsmoe_b200_ctx** out) {
+  return guarded([&] {
+    require(out != nullptr, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    auto* C = new dsmoe_b200_ctx;
+    C->stream = static_cast<cudaStream_t>(stream);
+    *out = C;
+  });
+}
+
+void dsmoe_b200_ctx_free(dsmoe_b200_ctx* C) {
+  if (C) cudaStreamSynchronize(C->stream);
+  delete C;
+}
+
+int dsmoe_b200_ctx_check(dsmoe_b200_ctx* C) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    if (!C->counters.p) return;
+    check_flags(C);
+  });
+}
+
+int dsmoe_b200_ctx_set_profiling(dsmoe_b200_ctx* C, int on) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    if (on && !C->ev[0])
+      for (auto& e : C->ev) cuda_check(cudaEventCreate(&e), "event create");
+    C->profiling = on != 0;
+    for (double& v : C->prof_ms) v = 0.0;
+    C->prof_calls = 0;
+  });
+}
+
+int dsmoe_b200_ctx_profile(const dsmoe_b200_ctx* C, double* ms, int n, long* calls) {
+  return guarded([&] {
+    require(C && ms, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    for (int i = 0; i < n && i < dsmoe_b200_ctx::kStages; ++i) ms[i] = C->prof_ms[i];
+    if (calls) *calls = C->prof_calls;
+  });
+}
+
+int dsmoe_b200_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                     const dsmoe_b200_policy* policy, int logits_mode, const float* logits_in,
+                     float* logits_out, const dsmoe_b200_routing* out, dsmoe_b200_drop_stats_t* stats) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(T >= 0, DSMOE_E_INVALID_ARGUMENT, "negative token count");
+    require(x || logits_in || T == 0, DSMOE_E_INVALID_ARGUMENT, "null input");
+    g_launches = 0;
+    const PolicyResolved pol = resolve_policy(L, policy);
+    if (T == 0) {
+      if (stats) stats_from_counts(L, 0, 0, 0, nullptr, stats);
+      return;
+    }
+    C->ensure(L, T);
+    const bool need_frac = stats && !is_pow2(L->P) && !(out && out->fraction);
+    if (need_frac) C->frac_ws.ensure(static_cast<size_t>(T) * L->K * L->P);
+    stage_route(C, L, x, T, pol, logits_mode, logits_in, logits_out, out, need_frac ? C->frac_ws.as<uint8_t>() : nullptr);
+    if (stats) {
+      unsigned long long h[4];
+      cuda_check(cudaMemcpyAsync(h, C->counters.p, sizeof(h), cudaMemcpyDeviceToHost, C->stream), "D2H");
+      cuda_check(cudaStreamSynchronize(C->stream), "sync");
+      if (h[2] & 1ull) fail(DSMOE_E_INVALID_ARGUMENT, "normalize_topk: degenerate zero-sum scores");
+      std::vector<uint8_t> fh;
+      if (!is_pow2(L->P)) {
+        fh.resize(static_cast<size_t>(T) * L->K * L->P);
+        const void* src = (out && out->fraction) ? static_cast<const void*>(out->fraction) : C->frac_ws.p;
+        cuda_check(cudaMemcpy(fh.data(), src, fh.size(), cudaMemcpyDeviceToHost), "D2H");
+      }
+      stats_from_counts(L, T, h[0], h[1], fh.data(), stats);
+    }
+  });
+}
+
+int dsmoe_b200_moe_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                           const int32_t* indices, const double* raw, const double* fraction, void* out) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(T >= 0, DSMOE_E_INVALID_ARGUMENT, "negative token count");
+    g_launches = 0;
+    if (T == 0) return;
+    require(x && indices && raw && fraction && out, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    C->ensure(L, T);
+    cudaStream_t s = C->stream;
+    cuda_check(cudaMemsetAsync(C->cnt.p, 0, 2 * L->E * sizeof(int), s), "memset");
+    cuda_check(cudaMemsetAsync(C->counters.p, 0, 4 * sizeof(unsigned long long), s), "memset");
+    ImportArgs a{};
+    a.idx = indices;
+    a.raw = raw;
+    a.frac = fraction;
+    a.T = T;
+    a.K = L->K;
+    a.P = L->P;
+    a.nphys = L->E * L->P;
+    a.sel_code = C->sel_code.as<int32_t>();
+    a.sel_raw = C->sel_raw.as<float>();
+    a.slot_pos = C->slot_pos.as<int32_t>();
+    a.cnt = C->cnt.as<int>();
+    a.counters = C->counters.as<unsigned long long>();
+    launch_check(launch_import_routing(a, s), "import routing");
+    ++g_launches;
+    stage_ffn(C, L, x, T, out);
+    check_flags(C);
+  });
+}
+
+int dsmoe_b200_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                       const dsmoe_b200_policy* policy, int logits_mode, void* out,
+                       dsmoe_b200_drop_stats_t* stats) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(T >= 0, DSMOE_E_INVALID_ARGUMENT, "negative token count");
+    g_launches = 0;
+    const PolicyResolved pol = resolve_policy(L, policy);
+    if (T == 0) {
+      if (stats) stats_from_counts(L, 0, 0, 0, nullptr, stats);
+      return;
+    }
+    require(x && out, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    C->ensure(L, T);
+    const bool need_frac = stats && !is_pow2(L->P);
+    if (need_frac) C->frac_ws.ensure(static_cast<size_t>(T) * L->K * L->P);
+    C->prof_begin();
+    stage_route(C, L, x, T, pol, logits_mode, nullptr, nullptr, nullptr, need_frac ? C->frac_ws.as<uint8_t>() : nullptr);
+    stage_ffn(C, L, x, T, out);
+    C->prof_end();
+    if (stats) {
+      unsigned long long h[4];
+      cuda_check(cudaMemcpyAsync(h, C->counters.p, sizeof(h), cudaMemcpyDeviceToHost, C->stream), "D2H");
+      cuda_check(cudaStreamSynchronize(C->stream), "sync");
+      if (h[2] & 1ull) fail(DSMOE_E_INVALID_ARGUMENT, "normalize_topk: degenerate zero-sum scores");
+      std::vector<uint8_t> fh;
+      if (need_frac) {
+        fh.resize(static_cast<size_t>(T) * L->K * L->P);
+        cuda_check(cudaMemcpy(fh.data(), C->frac_ws.p, fh.size(), cudaMemcpyDeviceToHost), "D2H");
+      }
+      stats_from_counts(L, T, h[0], h[1], fh.data(), stats);
+    }
+  });
+}
+
+int dsmoe_b200_drop_stats(const double* pre, const double* post, long n, int P, int S, long T, int d, int ffn,
+                          dsmoe_b200_drop_stats_t* st) {
+  return guarded([&] {
+    require(pre && post && st && P >= 1, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    const double w = 1.0 / P;
+    double total = 0.0, retained = 0.0;
+    for (long i = 0; i < n; ++i) {
+      total += pre[i] * w;
+      retained += post[i] * w;
+    }
+    st->num_tokens = T;
+    st->total_routed_units = total;
+    st->dropped_units = total - retained;
+    st->shared_units = static_cast<double>(S) * T;
+    const double denom = st->total_routed_units + st->shared_units;
+    st->drop_rate = denom > 0.0 ? st->dropped_units / denom : 0.0;
+    const double unit = 6.0 * d * ffn;
+    st->total_flops = denom * unit;
+    st->saved_flops = st->dropped_units * unit;
+    st->retained_flops = st->total_flops - st->saved_flops;
+  });
+}
+
+int dsmoe_b200_load_aware_thresholds(const double* loads, int D, double t_max, double* out) {
+  return guarded([&] {
+    require(loads && out && D >= 1, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(t_max > 0.0 && t_max <= 1.0, DSMOE_E_INVALID_ARGUMENT, "load_aware_thresholds: t_max must be in (0, 1]");
+    double total = 0.0;
+    for (int i = 0; i < D; ++i) total += loads[i];
+    require(total > 0.0, DSMOE_E_INVALID_ARGUMENT, "load_aware_thresholds: zero total load");
+    const double ideal = total / static_cast<double>(D);
+    for (int i = 0; i < D; ++i) {
+      const double ratio = loads[i] / ideal;
+      out[i] = ratio >= 1.0 ? t_max : t_max * ratio;
+    }
+  });
+}
+
+int dsmoe_b200_profile_importance(dsmoe_b200_ctx*, const dsmoe_b200_layer*, const void*, int, const int32_t*, int,
+                                  double*) {
+  return guarded([&] { fail(DSMOE_E_INTERNAL, "profile_importance: not built yet"); });
+}
+
+int dsmoe_b200_reconstruct(dsmoe_b200_ctx*, const dsmoe_b200_layer*, const double*, int32_t*, dsmoe_b200_layer**) {
+  return guarded([&] { fail(DSMOE_E_INTERNAL, "reconstruct: not built yet"); });
+}
+
+}  // extern "C"

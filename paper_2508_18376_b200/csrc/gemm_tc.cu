@@ -1,0 +1,252 @@
+// K3 / K4 (and K0): persistent grouped GEMM on the 5th-generation tensor cores.
+//
+// Replaces the per-token scalar loops of accumulate_block
+// (/root/reference/proj/include/dsmoe/moe.hpp:213-231) and the gate matmul of
+// gate_scores (moe.hpp:174 -> matrix.hpp:47-64) for bf16 layers.
+//
+// One CTA per SM (192 threads, warp-specialised):
+//   warp 0      TMA producer: A (128 x 64) and B (N x 64) bf16 tiles, SWIZZLE_128B,
+//               4-stage smem ring guarded by full/empty mbarriers;
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256,
+//               K=16 per instruction), fp32 accumulators in TMEM, two
+//               accumulator stages (2 x 256 columns) so the epilogue of tile i
+//               overlaps the MMAs of tile i+1;
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global.
+// Work items (GemmTile) are produced on the device by plan_tiles (permute.cu)
+// and walked in a static round-robin over the persistent CTAs.
+//
+// Epilogue modes
+//   kEpiF32     fp32 store (gate logits, K0);
+//   kEpiSwiGLU  h = swish(g) * u over the [g | u] column halves of the tile,
+//               rows >= m_live store zeros (major-only rows of a minor chunk),
+//               bf16 store into H (K3);
+//   kEpiScale   y = acc * row_scale[row] (the raw gate score, moe.hpp:235-237),
+//               bf16 store into Y (K4).
+#include "common.cuh"
+
+namespace dsb {
+
+constexpr int kStages = 4;
+constexpr int kABytes = kTileM * kTileK * 2;       // 16 KB
+constexpr int kBBytesMax = 256 * kTileK * 2;       // 32 KB
+constexpr int kStageBytes = kABytes + kBBytesMax;  // 48 KB
+constexpr int kGemmThreads = 192;
+constexpr int kAccCols = 256;
+constexpr int kGemmSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+enum { kEpiF32 = 0, kEpiSwiGLU = 1, kEpiScale = 2 };
+
+struct GemmArgs {
+  const GemmTile* tiles;
+  const int* num_tiles;
+  void* out;
+  long long ldo;           // output row stride in elements
+  const float* row_scale;  // kEpiScale
+  uint32_t b_bytes;        // bytes of one B box (rows * 128)
+};
+
+__device__ __forceinline__ float silu_fast(float g) { return g / (1.0f + __expf(-g)); }
+
+template <int MODE>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
+                   const __grid_constant__ CUtensorMap mapB, const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ntiles = *args.num_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    fence_mbar_init();
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapA2);
+    tma_prefetch(&mapB);
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 2 * kAccCols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const GemmTile tl = args.tiles[t];
+        const void* ma = (tl.m_live & kTileAltA) ? static_cast<const void*>(&mapA2)
+                                                 : static_cast<const void*>(&mapA);
+        for (int kb = 0; kb < tl.nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          mbar_expect_tx(&full[stage], kABytes + args.b_bytes);
+          tma_load_2d(sa, ma, &full[stage], kb * kTileK, tl.a_row);
+          tma_load_2d(sa + kABytes, &mapB, &full[stage], kb * kTileK, tl.b_row);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const uint32_t sbase = smem_u32(smem);
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const GemmTile tl = args.tiles[t];
+        const uint32_t idesc = idesc_bf16(kTileM, tl.n_mma);
+        const uint32_t dtmem = tmem_base + acc * kAccCols;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < tl.nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = sbase + stage * kStageBytes;
+          const uint64_t adesc = sdesc_sw128(sa);
+          const uint64_t bdesc = sdesc_sw128(sa + kABytes);
+#pragma unroll
+          for (int k = 0; k < kTileK / 16; ++k) {
+            // advance 16 bf16 = 32 B along K inside the 128 B swizzle row
+            umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int r = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const GemmTile tl = args.tiles[t];
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+      const bool valid = r < tl.m_valid;
+      const long long orow = static_cast<long long>(tl.out_row + r);
+      if constexpr (MODE == kEpiSwiGLU) {
+        const int nc = tl.n_mma >> 1;
+        const bool live = r < (tl.m_live & 0xFFFFF);
+        __nv_bfloat16* H = static_cast<__nv_bfloat16*>(args.out) + orow * args.ldo + tl.out_col;
+        for (int c = 0; c < nc; c += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(taddr + c, g);
+          tmem_ld32(taddr + nc + c, u);
+          tmem_ld_wait();
+          if (valid) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float h0 = 0.f, h1 = 0.f;
+              if (live) {
+                h0 = silu_fast(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+                h1 = silu_fast(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+              }
+              pk[i] = pack_bf16x2(h0, h1);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(H + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
+        }
+      } else if constexpr (MODE == kEpiScale) {
+        const float sc = valid ? args.row_scale[orow] : 0.f;
+        __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(args.out) + orow * args.ldo + tl.out_col;
+        for (int c = 0; c < tl.n_mma; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c, v);
+          tmem_ld_wait();
+          if (valid) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]) * sc, __uint_as_float(v[2 * i + 1]) * sc);
+            uint4* dst = reinterpret_cast<uint4*>(Y + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
+        }
+      } else {
+        float* O = static_cast<float*>(args.out) + orow * args.ldo + tl.out_col;
+        for (int c = 0; c < tl.n_mma; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c, v);
+          tmem_ld_wait();
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(O + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, 2 * kAccCols);
+}
+
+// ------------------------------------------------------------------ launcher
+int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
+                   const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
+                   int max_tiles, void* out, long long ldo, const float* row_scale,
+                   int b_box_rows, int num_sms, cudaStream_t stream) {
+  GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128)};
+  const int grid = max_tiles < num_sms ? (max_tiles > 0 ? max_tiles : 1) : num_sms;
+  cudaError_t err;
+  switch (mode) {
+#define DSB_LAUNCH(M)                                                                         \
+  case M: {                                                                                   \
+    static bool attr = false;                                                                 \
+    if (!attr) {                                                                              \
+      cudaFuncSetAttribute(gemm_tc_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                           kGemmSmem);                                                        \
+      attr = true;                                                                            \
+    }                                                                                         \
+    gemm_tc_kernel<M><<<grid, kGemmThreads, kGemmSmem, stream>>>(*mapA, *mapA2, *mapB, a);    \
+    break;                                                                                    \
+  }
+    DSB_LAUNCH(kEpiF32)
+    DSB_LAUNCH(kEpiSwiGLU)
+    DSB_LAUNCH(kEpiScale)
+#undef DSB_LAUNCH
+    default:
+      return -1;
+  }
+  err = cudaGetLastError();
+  return err == cudaSuccess ? 0 : static_cast<int>(err);
+}
+
+}  // namespace dsb

@@ -1,0 +1,99 @@
+// Host-side declarations of the kernel launchers (one per .cu file).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace dsb {
+
+// router.cu
+struct RouterArgs {
+  const float* logits;
+  int ld_logits;
+  int T, E, K, P;
+  int kind;
+  double t_major, t_minor;
+  int keep_top1, normalize;
+  const double* t_unit;
+  double maj_off, min_off;
+  int32_t* idx;
+  float* raw;
+  double* norm;
+  uint8_t* frac;
+  int32_t* sel_code;
+  float* sel_raw;
+  int32_t* slot_pos;
+  int* cnt;
+  unsigned long long* counters;
+};
+struct ImportArgs {
+  const int32_t* idx;
+  const double* raw;
+  const double* frac;
+  int T, K, P, nphys;
+  int32_t* sel_code;
+  float* sel_raw;
+  int32_t* slot_pos;
+  int* cnt;
+  unsigned long long* counters;
+};
+int launch_router(const RouterArgs& a, cudaStream_t stream);
+int launch_import_routing(const ImportArgs& a, cudaStream_t stream);
+int launch_gate_logits_exact(const void* x, int x_bf16, const float* gate, float* out, int T, int d,
+                             int E, cudaStream_t stream);
+
+// permute.cu
+struct PlanArgs {
+  const UnitInfo* units;
+  const UnitSeg* seg_routed;
+  int num_routed, num_shared;
+  int T, d;
+  int shared_row0;
+  GemmTile* tiles1;
+  int* n1;
+  GemmTile* tiles2;
+  int* n2;
+};
+int launch_permute(const int32_t* sel_code, const float* sel_raw, const int* cnt, int T, int K,
+                   int num_units, int32_t* row_token, float* row_scale, int32_t* slot_pos,
+                   UnitSeg* seg, int* r_total, cudaStream_t stream);
+int launch_plan(const PlanArgs& a, cudaStream_t stream);
+int launch_gather(const void* x, void* xp, const int32_t* row_token, const int* r_total,
+                  int row_bytes, int num_sms, cudaStream_t stream);
+int launch_combine(const void* y, int y_bf16, const int32_t* slot_pos, void* out, int T, int d, int K,
+                   int S, int shared_row0, int num_sms, cudaStream_t stream);
+int launch_fill_f32(float* p, float v, long long n, cudaStream_t stream);
+
+// gemm_tc.cu
+int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
+                   const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
+                   int max_tiles, void* out, long long ldo, const float* row_scale,
+                   int b_box_rows, int num_sms, cudaStream_t stream);
+
+// gemm_simt.cu
+struct SimtArgs {
+  const float* A;
+  const float* A2;
+  long long lda;
+  long long a_rows, a2_rows;
+  const float* B;
+  long long ldb;
+  const GemmTile* tiles;
+  const int* num_tiles;
+  float* out;
+  long long ldo;
+  const float* row_scale;
+};
+int launch_gemm_simt(int mode, const SimtArgs& a, int max_tiles, int num_sms, cudaStream_t stream);
+
+// pack.cu
+int launch_pack_w13(int src_dt, int dst_dt, const void* w1, const void* w3, int d, int ld, const int* order,
+                    int col0, int ncols, void* dst, long long base, int wpad, cudaStream_t s);
+int launch_pack_w2t(int src_dt, int dst_dt, const void* w2, int d, const int* order, int row0, int nrows,
+                    void* dst, long long drow, int hcol0, long long hstride, cudaStream_t s);
+int launch_pack_gate(int src_dt, int dst_dt, const void* gate, int d, int E, void* gateT, float* gate_exact,
+                     cudaStream_t s);
+
+}  // namespace dsb

@@ -1,0 +1,433 @@
+"""Host-side mirror of the reference's partition / drop-policy / forward API
+over the C ABI of libdsmoe_b200.so (include/dsmoe_b200.h).
+
+Names, argument meaning and error behaviour follow the reference's C++ layer
+(/root/reference/proj/include/dsmoe/*.hpp):
+
+    DropPolicy            dropping.hpp:12-56
+    RoutingDecision       moe.hpp:142-167
+    MoeLayer              moe.hpp:73-120   (device-resident, packed)
+    route_and_drop        dropping.hpp:248
+    moe_forward           moe.hpp:239
+    drop_stats            dropping.hpp:171
+    load_aware_thresholds ep_sim.hpp:76
+    place_experts / device_loads   ep_sim.hpp:38 / :59
+
+Failures raise DsmoeError carrying the reference status code
+(error.hpp:10-20).  There is no CPU fallback: every compute call goes through
+the CUDA library, and importing this module on a machine without the built
+library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdsmoe_b200.so")
+
+F32, BF16 = 0, 1
+KIND = {"none": 0, "1t": 1, "2t": 2}
+METRIC = {"gate": 0, "abs_gate": 1, "gate_up": 2, "abs_gate_up": 3}
+LOGITS_TENSOR, LOGITS_EXACT = 0, 1
+STATUS = {0: "ok", 1: "invalid_argument", 2: "shape_mismatch", 3: "invalid_state", 4: "io_error",
+          5: "bad_magic", 6: "truncated", 7: "schema_error", 8: "internal"}
+
+
+class DsmoeError(RuntimeError):
+    """dsmoe::Error (error.hpp:37-44): a status code plus message."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{STATUS.get(code, code)}] {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class LayerConfig(C.Structure):
+    _fields_ = [("d_model", C.c_int), ("d_ffn", C.c_int), ("num_experts", C.c_int), ("top_k", C.c_int),
+                ("num_shared_experts", C.c_int), ("gate_prenormalized", C.c_int),
+                ("replay_factor", C.c_int), ("dtype", C.c_int),
+                ("block_widths", C.POINTER(C.c_int32)), ("shared_widths", C.POINTER(C.c_int32))]
+
+
+class Policy(C.Structure):
+    _fields_ = [("kind", C.c_int), ("t_drop", C.c_double), ("t_major", C.c_double),
+                ("t_minor", C.c_double), ("keep_top1", C.c_int), ("normalize", C.c_int),
+                ("t_unit", C.c_void_p)]
+
+
+class RoutingOut(C.Structure):
+    _fields_ = [("indices", C.c_void_p), ("raw", C.c_void_p), ("normalized", C.c_void_p),
+                ("fraction", C.c_void_p)]
+
+
+class DropStatsC(C.Structure):
+    _fields_ = [("num_tokens", C.c_long), ("total_routed_units", C.c_double),
+                ("dropped_units", C.c_double), ("shared_units", C.c_double), ("drop_rate", C.c_double),
+                ("total_flops", C.c_double), ("saved_flops", C.c_double),
+                ("retained_flops", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+# every symbol include/dsmoe_b200.h declares (tests check the export table)
+SYMBOLS = {
+    "dsmoe_b200_version": (C.c_char_p, []),
+    "dsmoe_b200_last_error": (C.c_char_p, []),
+    "dsmoe_b200_last_launch_count": (C.c_int, []),
+    "dsmoe_b200_layer_create": (C.c_int, [C.POINTER(LayerConfig), C.POINTER(C.c_void_p)]),
+    "dsmoe_b200_layer_free": (None, [C.c_void_p]),
+    "dsmoe_b200_layer_set_gate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "dsmoe_b200_layer_set_block": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_int, C.c_int, C.c_void_p]),
+    "dsmoe_b200_layer_set_shared": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_int, C.c_int, C.c_void_p]),
+    "dsmoe_b200_layer_info": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dsmoe_b200_ctx_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "dsmoe_b200_ctx_free": (None, [C.c_void_p]),
+    "dsmoe_b200_ctx_check": (C.c_int, [C.c_void_p]),
+    "dsmoe_b200_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
+    "dsmoe_b200_ctx_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_long)]),
+    "dsmoe_b200_route": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
+                                   C.c_void_p, C.c_void_p, C.POINTER(RoutingOut), C.POINTER(DropStatsC)]),
+    "dsmoe_b200_moe_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dsmoe_b200_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
+                                     C.c_void_p, C.POINTER(DropStatsC)]),
+    "dsmoe_b200_drop_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_long, C.c_int, C.c_int, C.c_long, C.c_int,
+                                        C.c_int, C.POINTER(DropStatsC)]),
+    "dsmoe_b200_profile_importance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                                C.c_int, C.c_void_p]),
+    "dsmoe_b200_reconstruct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.POINTER(C.c_void_p)]),
+    "dsmoe_b200_load_aware_thresholds": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_void_p]),
+}
+
+
+def lib():
+    """Load libdsmoe_b200.so (built in-tree by build.py).  Raises if absent:
+    there is no fallback path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                              "(python -m paper_2508_18376_b200.build)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SYMBOLS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _chk(rc: int):
+    if rc != 0:
+        raise DsmoeError(rc, lib().dsmoe_b200_last_error().decode())
+
+
+def last_launch_count() -> int:
+    return int(lib().dsmoe_b200_last_launch_count())
+
+
+# ----------------------------------------------------------------- torch glue
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream=None):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _src(a):
+    """(pointer, dtype code, on_device, keepalive) for a numpy array or torch tensor."""
+    if isinstance(a, np.ndarray):
+        a = np.ascontiguousarray(a, np.float32)
+        return a.ctypes.data, F32, 0, a
+    torch = _torch()
+    t = a.contiguous()
+    if t.dtype == torch.bfloat16:
+        dt = BF16
+    else:
+        t = t.float()
+        dt = F32
+    return t.data_ptr(), dt, int(t.is_cuda), t
+
+
+# ---------------------------------------------------------------- policies
+@dataclass
+class DropPolicy:
+    """DropPolicy (dropping.hpp:12-56)."""
+
+    kind: str = "none"
+    t_drop: float = 0.0
+    t_major: float = 0.0
+    t_minor: float = 0.0
+    keep_top1: bool = True
+    normalize: bool | None = None   # None -> !gate_prenormalized (capi.cpp:111)
+
+    @staticmethod
+    def none_policy():
+        return DropPolicy()
+
+    @staticmethod
+    def one_t(t, keep_top1=True):
+        return DropPolicy("1t", t, keep_top1=keep_top1)
+
+    @staticmethod
+    def two_t_from(t, keep_top1=True):
+        return DropPolicy.two_t(t, t - 0.01, t + 0.01, keep_top1)
+
+    @staticmethod
+    def two_t(t, t_major, t_minor, keep_top1=True):
+        if not t_major <= t_minor:
+            raise DsmoeError(1, "drop policy: t_major must be <= t_minor")
+        return DropPolicy("2t", t, t_major, t_minor, keep_top1)
+
+    def c(self, t_unit=None) -> Policy:
+        return Policy(KIND[self.kind], self.t_drop, self.t_major, self.t_minor, int(self.keep_top1),
+                      -1 if self.normalize is None else int(self.normalize),
+                      None if t_unit is None else t_unit.data_ptr())
+
+
+# ------------------------------------------------------------------ layers
+class MoeLayer:
+    """A device-resident MoE layer (MoeLayer<T>, moe.hpp:73-120) packed for the
+    grouped GEMMs.  blocks[e*P + p] = (w1, w3, w2) of slice p of expert e;
+    shared = [(w1, w3, w2)]; arrays are numpy (host) or torch (host/device)."""
+
+    def __init__(self, d_model, d_ffn, num_experts, top_k, gate, blocks, shared=(), replay_factor=1,
+                 dtype="bf16", gate_prenormalized=False, stream=None):
+        self.d, self.ffn, self.E, self.K = d_model, d_ffn, num_experts, top_k
+        self.P = replay_factor
+        self.S = len(shared)
+        self.dtype = dtype
+        self.prenorm = bool(gate_prenormalized)
+        widths = (C.c_int32 * max(1, len(blocks)))(*[int(b[0].shape[1]) for b in blocks])
+        swidths = (C.c_int32 * max(1, self.S))(*([int(s[0].shape[1]) for s in shared] or [0]))
+        cfg = LayerConfig(d_model, d_ffn, num_experts, top_k, self.S, int(self.prenorm), replay_factor,
+                          BF16 if dtype == "bf16" else F32, widths, swidths)
+        h = C.c_void_p()
+        _chk(lib().dsmoe_b200_layer_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+        st = _stream_ptr(stream)
+        p, dt, dev, keep = _src(gate)
+        _chk(lib().dsmoe_b200_layer_set_gate(self.h, C.c_void_p(p), dt, dev, st))
+        for b, (w1, w3, w2) in enumerate(blocks):
+            a1, a3, a2 = _src(w1), _src(w3), _src(w2)
+            _chk(lib().dsmoe_b200_layer_set_block(self.h, b, C.c_void_p(a1[0]), C.c_void_p(a3[0]),
+                                                  C.c_void_p(a2[0]), a1[1], a1[2], st))
+        for s, (w1, w3, w2) in enumerate(shared):
+            a1, a3, a2 = _src(w1), _src(w3), _src(w2)
+            _chk(lib().dsmoe_b200_layer_set_shared(self.h, s, C.c_void_p(a1[0]), C.c_void_p(a3[0]),
+                                                   C.c_void_p(a2[0]), a1[1], a1[2], st))
+
+    @classmethod
+    def _wrap(cls, handle, like: "MoeLayer", P):
+        obj = cls.__new__(cls)
+        obj.__dict__.update(like.__dict__)
+        obj.h = handle
+        obj.P = P
+        return obj
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib is not None:
+            _lib.dsmoe_b200_layer_free(h)
+            self.h = None
+
+    @property
+    def torch_dtype(self):
+        torch = _torch()
+        return torch.bfloat16 if self.dtype == "bf16" else torch.float32
+
+
+class Context:
+    """Stream + workspace (one per CUDA stream)."""
+
+    def __init__(self, stream=None):
+        h = C.c_void_p()
+        _chk(lib().dsmoe_b200_ctx_create(_stream_ptr(stream), C.byref(h)))
+        self.h = h
+
+    def check(self):
+        _chk(lib().dsmoe_b200_ctx_check(self.h))
+
+    STAGES = ("gate", "router", "permute_plan", "gather", "gemm1", "gemm2", "combine")
+
+    def set_profiling(self, on: bool):
+        _chk(lib().dsmoe_b200_ctx_set_profiling(self.h, int(on)))
+
+    def profile(self) -> dict:
+        """Summed per-stage device milliseconds (CUDA events) since profiling
+        was enabled, plus the number of profiled calls."""
+        ms = (C.c_double * len(self.STAGES))()
+        calls = C.c_long()
+        _chk(lib().dsmoe_b200_ctx_profile(self.h, ms, len(self.STAGES), C.byref(calls)))
+        out = dict(zip(self.STAGES, list(ms)))
+        out["calls"] = calls.value
+        return out
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib is not None:
+            _lib.dsmoe_b200_ctx_free(h)
+            self.h = None
+
+
+# ------------------------------------------------------------------ routing
+@dataclass
+class RoutingDecision:
+    """RoutingDecision (moe.hpp:142-167), device tensors of shape T x (K*P)."""
+
+    num_tokens: int
+    k: int
+    base_k: int
+    replay_factor: int
+    indices: object
+    raw: object          # fp32 on device; double(raw) is the reference's raw
+    normalized: object   # fp64
+    fraction_code: object  # uint8: 0 -> 0.0, 1 -> 0.5, 2 -> 1.0
+    stats: dict = field(default_factory=dict)
+
+    @property
+    def fraction(self):
+        torch = _torch()
+        return torch.tensor([0.0, 0.5, 1.0], dtype=torch.float64,
+                            device=self.fraction_code.device)[self.fraction_code.long()]
+
+    def host(self):
+        """numpy copies with the reference's types (int32, double...)."""
+        return (self.indices.cpu().numpy(), self.raw.double().cpu().numpy(),
+                self.normalized.cpu().numpy(), self.fraction.cpu().numpy())
+
+
+def _x(x, layer: MoeLayer):
+    torch = _torch()
+    if not (isinstance(x, torch.Tensor) and x.is_cuda):
+        raise DsmoeError(1, "tokens must be a CUDA tensor")
+    if x.dtype != layer.torch_dtype:
+        raise DsmoeError(2, f"tokens dtype {x.dtype} does not match layer dtype {layer.dtype}")
+    if x.dim() != 2 or x.shape[1] != layer.d:
+        raise DsmoeError(2, f"tokens shape {tuple(x.shape)} does not match d_model {layer.d}")
+    return x.contiguous()
+
+
+def route_and_drop(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None = None, logits=None,
+                   logits_mode=LOGITS_TENSOR, t_unit=None, return_logits=False) -> RoutingDecision:
+    """route_and_drop (dropping.hpp:248): gate -> softmax -> Top-K -> replay ->
+    normalize -> 1T/2T drop, on the device.  `logits` (T x E fp32 CUDA tensor)
+    bypasses the gate matmul, for parity on identical logits."""
+    torch = _torch()
+    policy = policy or DropPolicy()
+    if logits is not None:
+        logits = logits.contiguous().float()
+        T = logits.shape[0]
+        dev = logits.device
+        xp = None
+    else:
+        x = _x(x, layer)
+        T = x.shape[0]
+        dev = x.device
+        xp = x.data_ptr()
+    n = T * layer.K * layer.P
+    idx = torch.empty(n, dtype=torch.int32, device=dev)
+    raw = torch.empty(n, dtype=torch.float32, device=dev)
+    norm = torch.empty(n, dtype=torch.float64, device=dev)
+    frac = torch.empty(n, dtype=torch.uint8, device=dev)
+    lg_out = torch.empty((T, layer.E), dtype=torch.float32, device=dev) if return_logits else None
+    out = RoutingOut(idx.data_ptr(), raw.data_ptr(), norm.data_ptr(), frac.data_ptr())
+    st = DropStatsC()
+    _chk(lib().dsmoe_b200_route(ctx.h, layer.h, None if xp is None else C.c_void_p(xp), T,
+                                C.byref(policy.c(t_unit)), logits_mode,
+                                None if logits is None else C.c_void_p(logits.data_ptr()),
+                                None if lg_out is None else C.c_void_p(lg_out.data_ptr()),
+                                C.byref(out), C.byref(st)))
+    sh = (T, layer.K * layer.P)
+    r = RoutingDecision(T, layer.K * layer.P, layer.K, layer.P, idx.view(sh), raw.view(sh), norm.view(sh),
+                        frac.view(sh), st.as_dict())
+    if return_logits:
+        return r, lg_out
+    return r
+
+
+def moe_forward(ctx: Context, layer: MoeLayer, x, routing) -> object:
+    """moe_forward (moe.hpp:239): raw-score-weighted sum of the kept expert
+    blocks plus the unweighted shared experts.  `routing` is a RoutingDecision
+    or a tuple (indices int32, raw float64, fraction float64) of CUDA tensors."""
+    torch = _torch()
+    x = _x(x, layer)
+    T = x.shape[0]
+    if isinstance(routing, RoutingDecision):
+        idx, raw, frac = routing.indices, routing.raw.double(), routing.fraction
+    else:
+        idx, raw, frac = routing
+    idx = idx.to(device=x.device, dtype=torch.int32).contiguous()
+    raw = raw.to(device=x.device, dtype=torch.float64).contiguous()
+    frac = frac.to(device=x.device, dtype=torch.float64).contiguous()
+    if idx.numel() != T * layer.K * layer.P:
+        raise DsmoeError(3, "moe_forward: routing does not match the layer's selections per token")
+    out = torch.empty_like(x)
+    _chk(lib().dsmoe_b200_moe_forward(ctx.h, layer.h, C.c_void_p(x.data_ptr()), T,
+                                      C.c_void_p(idx.data_ptr()), C.c_void_p(raw.data_ptr()),
+                                      C.c_void_p(frac.data_ptr()), C.c_void_p(out.data_ptr())))
+    return out
+
+
+def forward(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None = None, out=None,
+            logits_mode=LOGITS_TENSOR, with_stats=False):
+    """route_and_drop + moe_forward in one device launch sequence (the
+    per-layer body of model_forward_dropped, dropping.hpp:263-274)."""
+    torch = _torch()
+    x = _x(x, layer)
+    if out is None:
+        out = torch.empty_like(x)
+    st = DropStatsC()
+    _chk(lib().dsmoe_b200_forward(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
+                                  C.byref((policy or DropPolicy()).c()), logits_mode,
+                                  C.c_void_p(out.data_ptr()), C.byref(st) if with_stats else None))
+    return (out, st.as_dict()) if with_stats else out
+
+
+# ---------------------------------------------------------------- host math
+def drop_stats(pre_fraction, post_fraction, replay_factor, num_shared, num_tokens, d_model, d_ffn) -> dict:
+    """drop_stats (dropping.hpp:171-195) through the C ABI (host arithmetic)."""
+    pre = np.ascontiguousarray(pre_fraction, np.float64).ravel()
+    post = np.ascontiguousarray(post_fraction, np.float64).ravel()
+    if pre.size != post.size:
+        raise DsmoeError(1, "drop_stats: routing shapes differ")
+    st = DropStatsC()
+    _chk(lib().dsmoe_b200_drop_stats(pre.ctypes.data, post.ctypes.data, pre.size, replay_factor, num_shared,
+                                     num_tokens, d_model, d_ffn, C.byref(st)))
+    return st.as_dict()
+
+
+def load_aware_thresholds(loads, t_max) -> np.ndarray:
+    """load_aware_thresholds (ep_sim.hpp:76-89)."""
+    loads = np.ascontiguousarray(loads, np.float64)
+    out = np.empty_like(loads)
+    _chk(lib().dsmoe_b200_load_aware_thresholds(loads.ctypes.data, loads.size, t_max, out.ctypes.data))
+    return out
+
+
+def place_experts(num_experts: int, devices: int, strategy: str = "contiguous") -> np.ndarray:
+    """place_experts (ep_sim.hpp:38-54)."""
+    if not (devices >= 1 and num_experts >= devices):
+        raise DsmoeError(1, "place_experts: need num_experts >= devices >= 1")
+    if strategy in ("round_robin", "round-robin"):
+        return (np.arange(num_experts) % devices).astype(np.int32)
+    if strategy != "contiguous":
+        raise DsmoeError(1, f"unknown placement strategy: {strategy}")
+    if num_experts % devices:
+        raise DsmoeError(1, "place_experts: contiguous placement needs num_experts divisible by devices")
+    return (np.arange(num_experts) // (num_experts // devices)).astype(np.int32)
