@@ -1,0 +1,384 @@
+"""MoE-module forward throughput on B200 (BASELINE.json metric: "MoE-module
+tokens/s vs drop rate (0/25/50%) at 1/2/4/8 B200; EP speedup").
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c2|c3|c4] [--drop 0.25]
+    python bench.py --impl reference ...      (the reference's CPU path, host cores)
+
+A step is one MoE-module forward (gate -> route/drop -> permute -> grouped
+SwiGLU GEMMs -> combine) over T synthetic tokens already resident in HBM.
+Default workload: BASELINE config C2 (OLMoE-1B-7B layer: 64 experts, top-8,
+d=2048, ffn=1024, reconstructed into major/minor halves, bf16, T=16384).
+`value` is at the --drop target (2T policy, threshold calibrated on the
+device); the 0/25/50% sweep and the drop speed-ups ride along in `sweep`.
+Weights are random-init of the named shapes (no checkpoints offline).
+N > 1 (torchrun): every rank runs the same module on its own tokens (weak
+scaling, no collective on this path); the expert-parallel path is ep.py.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (d, ffn, E, K, S, workload label)
+    "c2": (2048, 1024, 64, 8, 0, "OLMoE-1B-7B MoE layer (64 experts, top-8, d=2048, ffn=1024), reconstructed P=2"),
+    "c3": (4096, 14336, 8, 2, 0, "Mixtral-8x7B MoE layer (8 experts, top-2, d=4096, ffn=14336), complete P=4 "
+                                 "(32 experts, top-8, ffn 3584) then reconstructed P=2"),
+    "c4": (2048, 1408, 64, 6, 2, "DeepSeek-V2-Lite MoE layer (64 routed + 2 shared, top-6, d=2048, ffn=1408), "
+                                 "reconstructed P=2"),
+}
+METRIC = "MoE-module tokens/s vs drop rate (0/25/50%) at 1/2/4/8 B200; EP speedup"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), d.get("hbm_gbs", 6650.0), "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[3:7]) if v.strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ layers
+def make_weights(cfg, seed=0, device="cuda"):
+    """Random-init weights of the named shapes, bf16, on the device, in the
+    reference layout (gate d x E, w1/w3 d x ffn, w2 ffn x d)."""
+    import torch
+    d, ffn, E, K, S, _ = CONFIGS[cfg]
+    g = torch.Generator(device=device).manual_seed(seed)
+    sd = d ** -0.5
+
+    def rnd(*s):
+        return (torch.randn(*s, device=device, generator=g) * sd).to(torch.bfloat16)
+
+    gate = rnd(d, E)
+    experts = [(rnd(d, ffn), rnd(d, ffn), rnd(ffn, d)) for _ in range(E)]
+    shared = [(rnd(d, ffn), rnd(d, ffn), rnd(ffn, d)) for _ in range(S)]
+    return gate, experts, shared
+
+
+def complete_transform_weights(gate, experts, p):
+    """complete_transform (transform.hpp:66-95) on torch tensors: E*p experts of
+    width ffn/p, gate columns repeated, W2 scaled by p (exact in bf16 for p=4)."""
+    import torch
+    ffn = experts[0][0].shape[1]
+    c = ffn // p
+    gate2 = torch.repeat_interleave(gate, p, dim=1)
+    ex2 = []
+    for w1, w3, w2 in experts:
+        for q in range(p):
+            sl = slice(q * c, (q + 1) * c)
+            ex2.append((w1[:, sl].contiguous(), w3[:, sl].contiguous(), (w2[sl] * p).contiguous()))
+    return gate2, ex2
+
+
+def build_layer(cfg, ctx, calib_tokens=512, seed=0):
+    """Base layer -> (C3: complete P=4) -> device importance profile on
+    calibration tokens -> device reconstruction into major/minor (P=2)."""
+    import torch
+    import paper_2508_18376_b200 as D
+    d, ffn, E, K, S, _ = CONFIGS[cfg]
+    gate, experts, shared = make_weights(cfg, seed)
+    if cfg == "c3":
+        gate, experts = complete_transform_weights(gate, experts, 4)
+        E, K, ffn = E * 4, K * 4, ffn // 4
+    base = D.MoeLayer(d, ffn, E, K, gate, experts, shared, dtype="bf16")
+    calib = torch.randn(calib_tokens, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(98))
+    calib = calib.to(torch.bfloat16)
+    r = D.route_and_drop(ctx, base, calib)
+    vals = D.profile_importance(ctx, base, calib, r.indices, "abs_gate")
+    rec, _ = D.reconstruct_experts(ctx, base, vals)
+    host = (gate, experts, shared, E, K, ffn)
+    return rec, host
+
+
+def calibrate(ctx, layer, x, target, tol=0.005):
+    """Threshold bisection to a target drop rate (acceptance.cpp:342-352 method)."""
+    import paper_2508_18376_b200 as D
+    if target <= 0:
+        return D.DropPolicy(), 0.0
+    lo, hi = 0.0, 1.0
+    best = None
+    for _ in range(40):
+        t = 0.5 * (lo + hi)
+        st = D.route_and_drop(ctx, layer, x, D.DropPolicy.two_t_from(t)).stats
+        if best is None or abs(st["drop_rate"] - target) < abs(best[1] - target):
+            best = (t, st["drop_rate"])
+        if abs(st["drop_rate"] - target) <= tol:
+            break
+        if st["drop_rate"] < target:
+            lo = t
+        else:
+            hi = t
+    return D.DropPolicy.two_t_from(best[0]), best[1]
+
+
+# ---------------------------------------------------------------- timing
+def time_steps(fn, steps, warmup, dist=None):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    return ms
+
+
+def cpu_reference_rate(host, T_sample, threads, seed=5):
+    """The reference's own CPU path (oracle/_ref: route_and_drop + moe_forward
+    compiled from /root/reference/proj), on the same (bf16-valued) weights,
+    `threads` host threads over token shards, on T_sample tokens."""
+    import numpy as np
+    import oracle as O
+    gate, experts, shared, E, K, ffn = host
+    d = gate.shape[0]
+    f = lambda t: t.float().cpu().numpy()
+    L = O.Layer(d, ffn, E, K, f(gate), [tuple(f(w) for w in ex) for ex in experts],
+                [tuple(f(w) for w in s) for s in shared])
+    # reconstructed layout is a permutation of the same work: time the
+    # reference on the partial P=2 split (same FLOPs, same band logic)
+    L = O.partial_transform(L, 2)
+    if not O.ref_available():
+        raise RuntimeError("oracle/_ref not built")
+    R = O.RefLayer.from_layer(L)
+    x = O.bf16_round(np.random.default_rng(seed).standard_normal((T_sample, d), dtype=np.float32))
+    t0 = time.perf_counter()
+    r = R.route_and_drop(x, K, 2, "2t", 0.08)
+    R.moe_forward(x, r.idx, r.raw, r.frac, threads=threads)
+    dt = time.perf_counter() - t0
+    del R
+    return T_sample / dt, dt
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=list(CONFIGS))
+    ap.add_argument("--drop", type=float, default=0.25)
+    ap.add_argument("--tokens", type=int, default=16384)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="tokens for the CPU baseline sample (0 = auto)")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    d, ffn, E, K, S, label = CONFIGS[args.config]
+    ncores = os.cpu_count() or 1
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import torch  # noqa: F401  (weights are generated with torch on the host CPU)
+        host = None
+        # host-side random weights of the same shapes
+        gate, experts, shared = make_weights(args.config, device="cpu")
+        Eh, Kh, fh = E, K, ffn
+        if args.config == "c3":
+            gate, experts = complete_transform_weights(gate, experts, 4)
+            Eh, Kh, fh = E * 4, K * 4, ffn // 4
+        host = (gate, experts, shared, Eh, Kh, fh)
+        sample = args.cpu_sample or {"c2": 96, "c3": 8, "c4": 96}[args.config]
+        rates = []
+        cpu_reference_rate(host, max(4, sample // 4), ncores)  # warm-up
+        for _ in range(args.steps):
+            rate, _ = cpu_reference_rate(host, sample, ncores)
+            rates.append(rate)
+        v = statistics.median(rates)
+        print(json.dumps({"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": sample / v * 1e3, "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                          "impl": "reference",
+                          "config": {"workload": label, "tokens_per_step": sample, "drop_policy": "2T t=0.08"},
+                          "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": ncores, "kind": "reference",
+                                           "sample": f"{sample} tokens/step, route_and_drop + moe_forward over "
+                                                     f"{ncores} threads"},
+                          "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    else:
+        dist = None
+    import paper_2508_18376_b200 as D
+
+    ctx = D.Context()
+    layer, host = build_layer(args.config, ctx, seed=0)
+    T = args.tokens
+    gx = torch.Generator(device="cuda").manual_seed(99 + rank)
+    x = torch.randn(T, d, device="cuda", generator=gx).to(torch.bfloat16)
+    out = torch.empty_like(x)
+
+    # ---- drop sweep (0 / 25 / 50 %) + the headline target
+    targets = sorted({0.0, 0.25, 0.5, args.drop})
+    sweep = {}
+    pol_main = None
+    for tg in targets:
+        pol, rate = calibrate(ctx, layer, x, tg)
+        ms = time_steps(lambda: D.forward(ctx, layer, x, pol, out=out), max(5, args.steps // 2), 3, dist)
+        n = max(5, args.steps // 2)
+        sweep[f"{tg:.2f}"] = {"drop_rate": rate, "ms_per_step": ms / n, "tokens_per_s": T * world / (ms / n * 1e-3)}
+        if tg == args.drop:
+            pol_main, rate_main = pol, rate
+    base_ms = sweep["0.00"]["ms_per_step"]
+    for k, v in sweep.items():
+        v["speedup_vs_0"] = base_ms / v["ms_per_step"]
+
+    # ---- headline timed region
+    launches_per_step = None
+    with ClockSampler(local) as clk:
+        ms = time_steps(lambda: D.forward(ctx, layer, x, pol_main, out=out), args.steps, args.warmup, dist)
+    launches_per_step = D.last_launch_count()
+    ms_step = ms / args.steps
+    value = T * world / (ms_step * 1e-3)
+
+    # ---- per-kernel device times (CUDA events on the context stream)
+    ctx.set_profiling(True)
+    nprof = 10
+    _, st = D.forward(ctx, layer, x, pol_main, out=out, with_stats=True)
+    ctx.set_profiling(True)
+    for _ in range(nprof):
+        D.forward(ctx, layer, x, pol_main, out=out)
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    per = {k: prof[k] / prof["calls"] for k in ctx.STAGES}
+    peak_burst, peak_sust, hbm, peak_src = load_peaks()
+    g1_flops = st["retained_flops"] * 2.0 / 3.0   # [W1|W3]: 4*d*width per kept row
+    g2_flops = st["retained_flops"] / 3.0         # W2: 2*d*width per kept row
+    g1_tf = g1_flops / (per["gemm1"] * 1e-3) / 1e12
+    g2_tf = g2_flops / (per["gemm2"] * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"ncu_gemm1_{args.config}.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"kernel": "gemm1 (grouped [W1|W3] GEMM + SwiGLU, tcgen05)", "bound": "tensor",
+                "achieved": g1_tf, "peak": peak_sust, "unit": "TFLOP/s", "frac": g1_tf / peak_sust,
+                "peak_kind": f"bf16 sustained ({peak_src}); burst {peak_burst}", "traffic": traffic,
+                "flops_per_launch": g1_flops, "ms_per_launch": per["gemm1"],
+                "gemm2": {"achieved": g2_tf, "frac": g2_tf / peak_sust, "ms_per_launch": per["gemm2"]},
+                "stages_ms": per}
+
+    # ---- e2e through the public API with host buffers
+    xh = x.cpu().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+    xd = torch.empty_like(x)
+
+    def e2e_step():
+        xd.copy_(xh, non_blocking=True)
+        D.forward(ctx, layer, xd, pol_main, out=out)
+        oh.copy_(out, non_blocking=True)
+
+    e2e_ms = time_steps(e2e_step, max(5, args.steps // 2), 2, dist) / max(5, args.steps // 2)
+    e2e = {"value": T * world / (e2e_ms * 1e-3), "unit": "tokens/s",
+           "h2d_bytes_per_step": xh.numel() * xh.element_size(), "d2h_bytes_per_step": oh.numel() * oh.element_size()}
+
+    # ---- CPU baseline (rank 0 at N=1 only; bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            sample = args.cpu_sample or {"c2": 64, "c3": 4, "c4": 64}[args.config]
+            rate, dt = cpu_reference_rate(host, sample, ncores)
+            cpu = {"value": rate, "unit": "tokens/s", "cores": ncores, "kind": "reference",
+                   "sample": f"{sample} tokens of the same layer shape (route_and_drop + moe_forward of "
+                             f"/root/reference/proj compiled into oracle/_ref), {dt:.1f} s"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "tokens/s", "cores": ncores, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic tokens N(0,1), random-init weights of the named shapes",
+                "config": {"workload": label, "config_id": args.config, "tokens_per_gpu": T, "experts": E,
+                           "top_k": K, "d_model": d, "d_ffn": ffn, "shared": S,
+                           "drop_target": args.drop, "drop_rate": rate_main, "policy": "2T (t-0.01, t+0.01)",
+                           "l2": "working set > L2 (weights %.2f GB read per step)" % (
+                               (E * 3 * d * ffn + S * 3 * d * ffn) * 2 / 1e9),
+                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                "sweep": sweep, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps,
+                "gpu_launches_per_step": launches_per_step, "clocks": clk.summary()}
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

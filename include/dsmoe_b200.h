@@ -157,6 +157,14 @@ int dsmoe_b200_ctx_check(dsmoe_b200_ctx* ctx);
 int dsmoe_b200_ctx_set_profiling(dsmoe_b200_ctx* ctx, int on);
 int dsmoe_b200_ctx_profile(const dsmoe_b200_ctx* ctx, double* ms, int n, long* calls);
 
+/* The token permutation of the last forward on this context (host copies,
+ * any pointer may be NULL): row_token[r] = token of permuted row r (r <
+ * *r_total), slot_pos[t*K+s] = row of selection (t, s) or -1 when dropped,
+ * seg[3e..3e+2] = start, full rows, total rows of expert unit e.  Canonical
+ * order: units ascending, full rows then major-only rows, (t, s) ascending. */
+int dsmoe_b200_ctx_permutation(dsmoe_b200_ctx* ctx, int T, int K, int E, int32_t* row_token,
+                               int32_t* slot_pos, int32_t* seg, int* r_total);
+
 /* ---- the forward path --------------------------------------------------- */
 /* route_and_drop on device x (T x d_model, layer dtype).  `logits_in`
  * (device, T x E fp32, optional) bypasses the gate matmul.  `logits_out`

@@ -267,6 +267,36 @@ def apply_bands(norm, K, P, t_major, t_minor, keep_top1=True):
     return frac
 
 
+def permutation(idx, frac, K, P, E):
+    """Canonical token permutation (the reference has
+    none): a CPU counting sort over a canonical RoutingDecision.  Selection
+    (t, s) of original expert e = idx[t, s] // P has level 2 (every copy kept /
+    fraction 1 on P=1), 1 (copy 0 only / fraction 0.5) or 0 (dropped).  Rows:
+    experts ascending; inside, level-2 rows then level-1 rows, (t, s)
+    ascending.  Returns (row_token, slot_pos T x K, seg E x 3)."""
+    idx = np.asarray(idx).reshape(-1, K * P)
+    frac = np.asarray(frac, np.float64).reshape(-1, K * P)
+    T = idx.shape[0]
+    unit = idx[:, :K] // P
+    if P == 1:
+        lvl = np.where(frac == 1.0, 2, np.where(frac == 0.5, 1, 0))
+    else:
+        lvl = np.where(frac[:, :K] == 0, 0, np.where(frac[:, K:2 * K] == 1.0, 2, 1))
+    rows, seg = [], np.zeros((E, 3), np.int32)
+    slot_pos = np.full((T, K), -1, np.int32)
+    for e in range(E):
+        seg[e, 0] = len(rows)
+        for want in (2, 1):
+            ts, ss = np.nonzero((unit == e) & (lvl == want))  # row-major = (t, s) ascending
+            for t, s in zip(ts, ss):
+                slot_pos[t, s] = len(rows)
+                rows.append(t)
+            if want == 2:
+                seg[e, 1] = len(rows) - seg[e, 0]
+        seg[e, 2] = len(rows) - seg[e, 0]
+    return np.array(rows, np.int32), slot_pos, seg
+
+
 def drop_stats(pre_frac, post_frac, P, S, T, d, ffn) -> dict:
     pre = np.ascontiguousarray(pre_frac, np.float64).ravel()
     post = np.ascontiguousarray(post_frac, np.float64).ravel()

@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
           "-I" + CSRC, "-I" + os.path.join(os.path.dirname(HERE), "include")]
-PER_FILE = {"router.cu": ["-fmad=false"]}
+PER_FILE = {"router.cu": ["-fmad=false"], "reconstruct.cu": ["-fmad=false"]}
 
 
 def sources():

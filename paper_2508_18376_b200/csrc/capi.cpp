@@ -294,7 +294,8 @@ void pack_sub(dsmoe_b200_layer* L, int u, int p, const void* w1, const void* w3,
 // ====================================================================== ctx
 struct dsmoe_b200_ctx {
   cudaStream_t stream = nullptr;
-  DevBuf logits, sel_code, sel_raw, slot_pos, cnt, counters, row_token, row_scale, seg, scalars;
+  DevBuf logits, sel_code, sel_raw, slot_pos, cnt_chunk, chunk_off, code_base, counters, row_token, row_scale, seg,
+      scalars;
   DevBuf tiles1, tiles2, tiles_gate, xperm, H, Y, frac_ws;
   int gate_tiles_T = -1, gate_tiles_Epad = -1, gate_tiles_d = -1;
   long long scale_fill_key = -1;
@@ -347,7 +348,10 @@ struct dsmoe_b200_ctx {
     sel_code.ensure(static_cast<size_t>(TK) * 4 + 16);
     sel_raw.ensure(static_cast<size_t>(TK) * 4 + 16);
     slot_pos.ensure(static_cast<size_t>(TK) * 4 + 16);
-    cnt.ensure(static_cast<size_t>(2 * L->E) * 4);
+    const size_t nchunks = static_cast<size_t>((T + kRouterChunk - 1) / kRouterChunk);
+    cnt_chunk.ensure(nchunks * 2 * L->E * 4 + 16);
+    chunk_off.ensure(nchunks * 2 * L->E * 4 + 16);
+    code_base.ensure(static_cast<size_t>(2 * L->E) * 4);
     counters.ensure(4 * sizeof(unsigned long long));
     row_token.ensure(static_cast<size_t>(Rcap + kTileM) * 4);
     seg.ensure(sizeof(UnitSeg) * L->E);
@@ -474,7 +478,6 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
                  const PolicyResolved& pol, int logits_mode, const float* logits_in, float* logits_out,
                  const dsmoe_b200_routing* out, uint8_t* frac_ws) {
   cudaStream_t s = C->stream;
-  cuda_check(cudaMemsetAsync(C->cnt.p, 0, 2 * L->E * sizeof(int), s), "memset");
   cuda_check(cudaMemsetAsync(C->counters.p, 0, 4 * sizeof(unsigned long long), s), "memset");
   const float* lg = logits_in;
   int ld = L->E;
@@ -539,11 +542,38 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   if (!a.frac && frac_ws) a.frac = frac_ws;
   a.sel_code = C->sel_code.as<int32_t>();
   a.sel_raw = C->sel_raw.as<float>();
-  a.slot_pos = C->slot_pos.as<int32_t>();
-  a.cnt = C->cnt.as<int>();
+  a.cnt_chunk = C->cnt_chunk.as<int>();
   a.counters = C->counters.as<unsigned long long>();
   launch_check(launch_router(a, s), "router");
   ++g_launches;
+}
+
+// K2a: chunk scan + unit segments (+ GEMM work lists) + ordered scatter
+void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool plan) {
+  cudaStream_t s = C->stream;
+  const long long Rcap = static_cast<long long>(T) * L->K;
+  int* r_total = C->scalars.as<int>();
+  PlanArgs pa{};
+  pa.units = L->d_units.as<UnitInfo>();
+  pa.seg_routed = C->seg.as<UnitSeg>();
+  pa.num_routed = L->E;
+  pa.num_shared = L->S;
+  pa.T = T;
+  pa.d = L->d;
+  pa.shared_row0 = static_cast<int>(Rcap);
+  pa.tiles1 = C->tiles1.as<GemmTile>();
+  pa.n1 = r_total + 1;
+  pa.tiles2 = C->tiles2.as<GemmTile>();
+  pa.n2 = r_total + 2;
+  const int nchunks = (T + kRouterChunk - 1) / kRouterChunk;
+  launch_check(launch_scan_plan(C->cnt_chunk.as<int>(), nchunks, L->E, C->chunk_off.as<int>(), C->code_base.as<int>(),
+                                C->seg.as<UnitSeg>(), r_total, plan ? &pa : nullptr, s),
+               "scan/plan");
+  launch_check(launch_scatter(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), T, L->K, L->E, C->chunk_off.as<int>(),
+                              C->code_base.as<int>(), C->row_token.as<int32_t>(), C->row_scale.as<float>(),
+                              C->slot_pos.as<int32_t>(), s),
+               "scatter");
+  g_launches += 2;
 }
 
 // ------------------------------------- stage: K2 permute/gather, K3, K4, K5
@@ -555,26 +585,10 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   int* n1 = r_total + 1;
   int* n2 = r_total + 2;
   C->mark(2);
-  launch_check(launch_permute(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), C->cnt.as<int>(), T, L->K, L->E,
-                              C->row_token.as<int32_t>(), C->row_scale.as<float>(), C->slot_pos.as<int32_t>(),
-                              C->seg.as<UnitSeg>(), r_total, s),
-               "permute");
-  PlanArgs pa{};
-  pa.units = L->d_units.as<UnitInfo>();
-  pa.seg_routed = C->seg.as<UnitSeg>();
-  pa.num_routed = L->E;
-  pa.num_shared = L->S;
-  pa.T = T;
-  pa.d = L->d;
-  pa.shared_row0 = static_cast<int>(Rcap);
-  pa.tiles1 = C->tiles1.as<GemmTile>();
-  pa.n1 = n1;
-  pa.tiles2 = C->tiles2.as<GemmTile>();
-  pa.n2 = n2;
-  launch_check(launch_plan(pa, s), "plan");
+  stage_permute(C, L, T, true);
   C->mark(3);
   launch_check(launch_gather(x, C->xperm.p, C->row_token.as<int32_t>(), r_total, L->d * es, num_sms(), s), "gather");
-  g_launches += 3;
+  g_launches += 1;
   const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
   const int mt1 = static_cast<int>(std::min<long long>(C->max_tiles1(L, T), 1 << 30));
   const int mt2 = static_cast<int>(std::min<long long>(C->max_tiles2(L, T), 1 << 30));
@@ -758,6 +772,32 @@ int dsmoe_b200_ctx_profile(const dsmoe_b200_ctx* C, double* ms, int n, long* cal
   });
 }
 
+int dsmoe_b200_ctx_permutation(dsmoe_b200_ctx* C, int T, int K, int E, int32_t* row_token, int32_t* slot_pos,
+                               int32_t* seg, int* r_total) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require(C->row_token.p && C->slot_pos.bytes >= static_cast<size_t>(T) * K * 4 &&
+                C->seg.bytes >= sizeof(UnitSeg) * E,
+            DSMOE_E_INVALID_STATE, "no permutation recorded for this shape");
+    int R = 0;
+    cuda_check(cudaStreamSynchronize(C->stream), "sync");
+    cuda_check(cudaMemcpy(&R, C->scalars.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+    if (r_total) *r_total = R;
+    if (row_token) cuda_check(cudaMemcpy(row_token, C->row_token.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost), "D2H");
+    if (slot_pos)
+      cuda_check(cudaMemcpy(slot_pos, C->slot_pos.p, sizeof(int32_t) * T * K, cudaMemcpyDeviceToHost), "D2H");
+    if (seg) {
+      std::vector<UnitSeg> h(static_cast<size_t>(E));
+      cuda_check(cudaMemcpy(h.data(), C->seg.p, sizeof(UnitSeg) * E, cudaMemcpyDeviceToHost), "D2H");
+      for (int e = 0; e < E; ++e) {
+        seg[3 * e] = h[e].start;
+        seg[3 * e + 1] = h[e].n_full;
+        seg[3 * e + 2] = h[e].n_tot;
+      }
+    }
+  });
+}
+
 int dsmoe_b200_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
                      const dsmoe_b200_policy* policy, int logits_mode, const float* logits_in,
                      float* logits_out, const dsmoe_b200_routing* out, dsmoe_b200_drop_stats_t* stats) {
@@ -803,7 +843,6 @@ int dsmoe_b200_moe_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
     require(x && indices && raw && fraction && out, DSMOE_E_INVALID_ARGUMENT, "null argument");
     C->ensure(L, T);
     cudaStream_t s = C->stream;
-    cuda_check(cudaMemsetAsync(C->cnt.p, 0, 2 * L->E * sizeof(int), s), "memset");
     cuda_check(cudaMemsetAsync(C->counters.p, 0, 4 * sizeof(unsigned long long), s), "memset");
     ImportArgs a{};
     a.idx = indices;
@@ -813,10 +852,10 @@ int dsmoe_b200_moe_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
     a.K = L->K;
     a.P = L->P;
     a.nphys = L->E * L->P;
+    a.nunits = L->E;
     a.sel_code = C->sel_code.as<int32_t>();
     a.sel_raw = C->sel_raw.as<float>();
-    a.slot_pos = C->slot_pos.as<int32_t>();
-    a.cnt = C->cnt.as<int>();
+    a.cnt_chunk = C->cnt_chunk.as<int>();
     a.counters = C->counters.as<unsigned long long>();
     launch_check(launch_import_routing(a, s), "import routing");
     ++g_launches;
@@ -899,13 +938,126 @@ int dsmoe_b200_load_aware_thresholds(const double* loads, int D, double t_max, d
   });
 }
 
-int dsmoe_b200_profile_importance(dsmoe_b200_ctx*, const dsmoe_b200_layer*, const void*, int, const int32_t*, int,
-                                  double*) {
-  return guarded([&] { fail(DSMOE_E_INTERNAL, "profile_importance: not built yet"); });
+static ImpUnitC imp_unit(const dsmoe_b200_layer* L, int e) {
+  const UnitInfo& u = L->units[e];
+  ImpUnitC c{};
+  c.base0 = u.w13_row;
+  c.base1 = u.w13_row + 2LL * u.sub_wpad[0];
+  c.h0 = u.sub_w[0];
+  c.wpad0 = u.sub_wpad[0];
+  c.wpad1 = u.nsub > 1 ? u.sub_wpad[1] : 0;
+  return c;
 }
 
-int dsmoe_b200_reconstruct(dsmoe_b200_ctx*, const dsmoe_b200_layer*, const double*, int32_t*, dsmoe_b200_layer**) {
-  return guarded([&] { fail(DSMOE_E_INTERNAL, "reconstruct: not built yet"); });
+int dsmoe_b200_profile_importance(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                                  const int32_t* indices, int metric, double* values) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(L->P == 1, DSMOE_E_INVALID_STATE,
+            "profile_importance: profile the original layer, not a partitioned one");
+    require(T >= 1, DSMOE_E_INVALID_ARGUMENT, "profile_importance: empty calibration set");
+    require(metric >= 0 && metric <= 3, DSMOE_E_INVALID_ARGUMENT, "unknown importance metric");
+    require(x && indices && values, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    g_launches = 0;
+    C->ensure(L, T);
+    cudaStream_t s = C->stream;
+    const long long n = static_cast<long long>(T) * L->K;
+    // every selection counts, regardless of fraction (reconstruct.hpp:121-125)
+    std::vector<double> ones(static_cast<size_t>(n), 1.0);
+    DevBuf dfrac;
+    dfrac.ensure(sizeof(double) * n);
+    cuda_check(cudaMemcpyAsync(dfrac.p, ones.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemsetAsync(C->counters.p, 0, 4 * sizeof(unsigned long long), s), "memset");
+    ImportArgs a{};
+    a.idx = indices;
+    a.raw = dfrac.as<double>();
+    a.frac = dfrac.as<double>();
+    a.T = T;
+    a.K = L->K;
+    a.P = 1;
+    a.nphys = L->E;
+    a.nunits = L->E;
+    a.sel_code = C->sel_code.as<int32_t>();
+    a.sel_raw = C->sel_raw.as<float>();
+    a.cnt_chunk = C->cnt_chunk.as<int>();
+    a.counters = C->counters.as<unsigned long long>();
+    launch_check(launch_import_routing(a, s), "import routing");
+    stage_permute(C, L, T, false);
+    unsigned long long flags[4];
+    cuda_check(cudaMemcpyAsync(flags, C->counters.p, sizeof(flags), cudaMemcpyDeviceToHost, s), "D2H");
+    std::vector<UnitSeg> seg(static_cast<size_t>(L->E));
+    cuda_check(cudaMemcpyAsync(seg.data(), C->seg.p, sizeof(UnitSeg) * L->E, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    require(!(flags[2] & 4ull), DSMOE_E_INVALID_STATE, "profile_importance: expert index out of range");
+    DevBuf v;
+    v.ensure(sizeof(double) * static_cast<size_t>(n) * L->ffn + 8);
+    for (int e = 0; e < L->E; ++e)
+      launch_check(launch_importance_tiles(L->dtype == DSMOE_B200_BF16, x, C->row_token.as<int32_t>(), seg[e].start,
+                                           seg[e].n_tot, L->w13.p, imp_unit(L, e), L->d, L->ffn, metric, v.as<double>(),
+                                           s),
+                   "importance");
+    launch_check(launch_importance_reduce(v.as<double>(), C->seg.as<UnitSeg>(), L->E, L->ffn, values, s), "reduce");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int dsmoe_b200_reconstruct(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const double* values, int32_t* order_out,
+                           dsmoe_b200_layer** out) {
+  return guarded([&] {
+    require(C != nullptr && out != nullptr && values != nullptr, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require_layer(L);
+    require(L->P == 1, DSMOE_E_INVALID_STATE, "reconstruct_experts: layer already partitioned");
+    cudaStream_t s = C->stream;
+    DevBuf ord;
+    int32_t* order = order_out;
+    if (!order) {
+      ord.ensure(sizeof(int32_t) * static_cast<size_t>(L->E) * L->ffn);
+      order = ord.as<int32_t>();
+    }
+    launch_check(launch_order_sort(values, L->E, L->ffn, order, s), "order sort");
+    const int major = (L->ffn + 1) / 2;  // ReconstructionMap::major_size (reconstruct.hpp:157)
+    std::vector<int32_t> widths;
+    for (int e = 0; e < L->E; ++e) {
+      widths.push_back(major);
+      widths.push_back(L->ffn - major);
+    }
+    dsmoe_b200_layer_config cfg{L->d, L->ffn, L->E, L->K, L->S, L->prenorm, 2, L->dtype, widths.data(),
+                                L->swidths.data()};
+    auto* R = new dsmoe_b200_layer;
+    try {
+      layer_build(R, cfg);
+      require(R->w13_rows == L->w13_rows && R->hstride == L->hstride, DSMOE_E_INTERNAL,
+              "reconstruct: packed geometry mismatch");
+      for (int e = 0; e < L->E; ++e)
+        launch_check(launch_gather_unit(L->dtype == DSMOE_B200_BF16, L->w13.p, R->w13.p, L->w2t.p, R->w2t.p,
+                                        order + static_cast<size_t>(e) * L->ffn, imp_unit(L, e), L->ffn, L->d,
+                                        static_cast<long long>(e) * L->d, L->hstride, s),
+                     "gather unit");
+      const int es = esize(L->dtype);
+      if (L->S > 0) {
+        const size_t r0 = static_cast<size_t>(L->units[L->E].w13_row);
+        cuda_check(cudaMemcpyAsync(R->w13.as<char>() + r0 * L->d * es, L->w13.as<char>() + r0 * L->d * es,
+                                   L->w13.bytes - r0 * L->d * es, cudaMemcpyDeviceToDevice, s),
+                   "copy shared");
+        const size_t q0 = static_cast<size_t>(L->E) * L->d * L->hstride * es;
+        cuda_check(cudaMemcpyAsync(R->w2t.as<char>() + q0, L->w2t.as<char>() + q0, L->w2t.bytes - q0,
+                                   cudaMemcpyDeviceToDevice, s),
+                   "copy shared");
+      }
+      cuda_check(cudaMemcpyAsync(R->gateT.p, L->gateT.p, L->gateT.bytes, cudaMemcpyDeviceToDevice, s), "copy gate");
+      cuda_check(cudaMemcpyAsync(R->gate_exact.p, L->gate_exact.p, L->gate_exact.bytes, cudaMemcpyDeviceToDevice, s),
+                 "copy gate");
+      cuda_check(cudaStreamSynchronize(s), "sync");
+      R->gate_set = true;
+      std::fill(R->block_set.begin(), R->block_set.end(), 1);
+      std::fill(R->shared_set.begin(), R->shared_set.end(), 1);
+    } catch (...) {
+      delete R;
+      throw;
+    }
+    *out = R;
+  });
 }
 
 }  // extern "C"

@@ -22,23 +22,22 @@ struct RouterArgs {
   float* raw;
   double* norm;
   uint8_t* frac;
-  int32_t* sel_code;
-  float* sel_raw;
-  int32_t* slot_pos;
-  int* cnt;
-  unsigned long long* counters;
+  int32_t* sel_code;   // T x K : unit * 4 + level, -1 when dropped
+  float* sel_raw;      // T x K
+  int* cnt_chunk;      // ceil(T/128) x 2E histograms of (unit, level)
+  unsigned long long* counters;  // [0] copies with fraction 1, [1] fraction 0.5, [2] error flags
 };
 struct ImportArgs {
   const int32_t* idx;
   const double* raw;
   const double* frac;
-  int T, K, P, nphys;
+  int T, K, P, nphys, nunits;
   int32_t* sel_code;
   float* sel_raw;
-  int32_t* slot_pos;
-  int* cnt;
+  int* cnt_chunk;
   unsigned long long* counters;
 };
+constexpr int kRouterChunk = 128;  // tokens per router block / scatter chunk
 int launch_router(const RouterArgs& a, cudaStream_t stream);
 int launch_import_routing(const ImportArgs& a, cudaStream_t stream);
 int launch_gate_logits_exact(const void* x, int x_bf16, const float* gate, float* out, int T, int d,
@@ -56,10 +55,10 @@ struct PlanArgs {
   GemmTile* tiles2;
   int* n2;
 };
-int launch_permute(const int32_t* sel_code, const float* sel_raw, const int* cnt, int T, int K,
-                   int num_units, int32_t* row_token, float* row_scale, int32_t* slot_pos,
-                   UnitSeg* seg, int* r_total, cudaStream_t stream);
-int launch_plan(const PlanArgs& a, cudaStream_t stream);
+int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
+                     int* r_total, const PlanArgs* plan, cudaStream_t stream);
+int launch_scatter(const int32_t* sel_code, const float* sel_raw, int T, int K, int E, const int* chunk_off,
+                   const int* code_base, int32_t* row_token, float* row_scale, int32_t* slot_pos, cudaStream_t stream);
 int launch_gather(const void* x, void* xp, const int32_t* row_token, const int* r_total,
                   int row_bytes, int num_sms, cudaStream_t stream);
 int launch_combine(const void* y, int y_bf16, const int32_t* slot_pos, void* out, int T, int d, int K,
@@ -87,6 +86,20 @@ struct SimtArgs {
   const float* row_scale;
 };
 int launch_gemm_simt(int mode, const SimtArgs& a, int max_tiles, int num_sms, cudaStream_t stream);
+
+// reconstruct.cu
+struct ImpUnitC {
+  long long base0, base1;
+  int h0, wpad0, wpad1;
+};
+int launch_importance_tiles(int bf16, const void* x, const int32_t* row_token, int seg_start, int nrows,
+                            const void* w13, const ImpUnitC& u, int d, int ffn, int metric, double* v,
+                            cudaStream_t s);
+int launch_importance_reduce(const double* v, const UnitSeg* seg, int E, int ffn, double* values, cudaStream_t s);
+int launch_order_sort(const double* values, int E, int ffn, int32_t* order, cudaStream_t s);
+int launch_gather_unit(int bf16, const void* w13_src, void* w13_dst, const void* w2t_src, void* w2t_dst,
+                       const int32_t* order, const ImpUnitC& u, int ffn, int d, long long w2t_row0,
+                       long long hstride, cudaStream_t s);
 
 // pack.cu
 int launch_pack_w13(int src_dt, int dst_dt, const void* w1, const void* w3, int d, int ld, const int* order,

@@ -1,4 +1,4 @@
-// K2 (permute + gather), the device-side tile planner, and K5 (combine).
+// K2 (scan + scatter + gather), the device-side tile planner, and K5 (combine).
 //
 // The reference has no token permutation: moe_forward walks tokens and their
 // kept selections one at a time (/root/reference/proj/include/dsmoe/moe.hpp:253-269).
@@ -6,98 +6,33 @@
 // expert FFN runs as a grouped GEMM.  Canonical row order:
 // units ascending; inside a unit the rows evaluated on every sub-block ("full")
 // first, then the major-only rows; each list in ascending (token, slot) order.
-// The order is a pure function of the routing, so it is deterministic and is
-// checked bit-for-bit against a CPU counting sort in tests/.
+// The order is a pure function of the routing (deterministic), checked
+// bit-for-bit against a CPU counting sort in tests/.
+//
+//   router / import  -> per 128-token chunk histograms of (unit, level)
+//   scan_plan        -> one block: exclusive scan of every code over chunks,
+//                       unit segments, and the GEMM1 / GEMM2 work lists
+//   scatter          -> one block per chunk: rank of each kept slot inside its
+//                       chunk (warp __match_any + per-warp prefix), final row
+//   gather           -> X_perm[row] = X[token(row)], 16-byte vectors
 #include "kernels.h"
 
 namespace dsb {
 
-// --------------------------------------------------------------------------
-// permute: grid (num_units, 2).  Block (u, 0) places the full rows of unit u,
-// block (u, 1) its major-only rows.  Ordered compaction with warp ballots.
-// --------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) permute_kernel(const int32_t* __restrict__ sel_code,
-                                                       const float* __restrict__ sel_raw,
-                                                       const int* __restrict__ cnt, int TK, int K,
-                                                       int num_units, int32_t* __restrict__ row_token,
-                                                       float* __restrict__ row_scale,
-                                                       int32_t* __restrict__ slot_pos,
-                                                       UnitSeg* __restrict__ seg, int* __restrict__ r_total) {
-  const int u = blockIdx.x;
-  const int lvl = blockIdx.y == 0 ? 2 : 1;
-  __shared__ int s_warp[32];
-  __shared__ int s_start;
-  // start of unit u = sum of the counts of units < u
-  int part = 0;
-  for (int i = threadIdx.x; i < u; i += blockDim.x) part += cnt[2 * i] + cnt[2 * i + 1];
-  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  if (lane == 0) s_warp[warp] = part;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int s = 0;
-    for (int w = 0; w < nwarps; ++w) s += s_warp[w];
-    s_start = s;
-  }
-  __syncthreads();
-  const int start = s_start;
-  const int n_full = cnt[2 * u], n_maj = cnt[2 * u + 1];
-  if (blockIdx.y == 0 && threadIdx.x == 0) {
-    seg[u] = UnitSeg{start, n_full, n_full + n_maj, 0};
-    if (u == num_units - 1) *r_total = start + n_full + n_maj;
-  }
-  const int base = start + (lvl == 2 ? 0 : n_full);
-  const int target = u * 4 + lvl;
-  int running = 0;
-  for (int i0 = 0; i0 < TK; i0 += blockDim.x) {
-    const int i = i0 + threadIdx.x;
-    const bool m = i < TK && sel_code[i] == target;
-    const unsigned bal = __ballot_sync(0xffffffffu, m);
-    __syncthreads();  // s_warp reuse
-    if (lane == 0) s_warp[warp] = __popc(bal);
-    __syncthreads();
-    int woff = 0, tot = 0;
-    for (int w = 0; w < nwarps; ++w) {
-      const int c = s_warp[w];
-      woff += w < warp ? c : 0;
-      tot += c;
-    }
-    if (m) {
-      const int pos = base + running + woff + __popc(bal & ((1u << lane) - 1u));
-      row_token[pos] = i / K;
-      row_scale[pos] = sel_raw[i];
-      slot_pos[i] = pos;
-    }
-    running += tot;
-  }
-}
-
-int launch_permute(const int32_t* sel_code, const float* sel_raw, const int* cnt, int T, int K,
-                   int num_units, int32_t* row_token, float* row_scale, int32_t* slot_pos,
-                   UnitSeg* seg, int* r_total, cudaStream_t stream) {
-  dim3 grid(num_units, 2);
-  permute_kernel<<<grid, 1024, 0, stream>>>(sel_code, sel_raw, cnt, T * K, K, num_units, row_token,
-                                            row_scale, slot_pos, seg, r_total);
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
-}
+__device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 // --------------------------------------------------------------------------
-// plan_tiles: one block turns the unit segments into the GEMM1 ([W1|W3] +
-// SwiGLU) and GEMM2 (W2 + raw-score scale) work lists.  Minor sub-blocks get
-// tiles only for the full rows, so FLOPs fall with the drop rate (no masks).
+// scan + plan (one block of 1024 threads)
 // --------------------------------------------------------------------------
-__device__ __forceinline__ UnitSeg plan_seg(const PlanArgs& a, int u) {
-  if (u < a.num_routed) return a.seg_routed[u];
+__device__ __forceinline__ UnitSeg plan_seg(const PlanArgs& a, const UnitSeg* seg, int u) {
+  if (u < a.num_routed) return seg[u];
   const int s = u - a.num_routed;
   return UnitSeg{a.shared_row0 + s * a.T, a.T, a.T, 0};
 }
 
-__device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
-
-__global__ void __launch_bounds__(1024) plan_tiles_kernel(const PlanArgs a) {
-  __shared__ int s1[1024], s2[1024];
-  __shared__ int carry1, carry2;
+__device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* s1, int* s2, int& carry1, int& carry2) {
   if (threadIdx.x == 0) { carry1 = 0; carry2 = 0; }
+  __syncthreads();
   const int nu = a.num_routed + a.num_shared;
   const int ntd = cdiv(a.d, kTileN2);
   for (int u0 = 0; u0 < nu; u0 += blockDim.x) {
@@ -107,17 +42,15 @@ __global__ void __launch_bounds__(1024) plan_tiles_kernel(const PlanArgs a) {
     UnitInfo ui{};
     if (u < nu) {
       ui = a.units[u];
-      sg = plan_seg(a, u);
+      sg = plan_seg(a, seg, u);
       const int mt_all = cdiv(sg.n_tot, kTileM), mt_full = cdiv(sg.n_full, kTileM);
       for (int p = 0; p < ui.nsub; ++p) c1 += cdiv(ui.sub_wpad[p], kChunk) * (p == 0 ? mt_all : mt_full);
       c2 = mt_all * ntd;
     }
-    __syncthreads();
     s1[threadIdx.x] = c1;
     s2[threadIdx.x] = c2;
     __syncthreads();
-    // inclusive Hillis-Steele scan
-    for (int o = 1; o < blockDim.x; o <<= 1) {
+    for (int o = 1; o < blockDim.x; o <<= 1) {  // inclusive Hillis-Steele scan
       const int v1 = threadIdx.x >= o ? s1[threadIdx.x - o] : 0;
       const int v2 = threadIdx.x >= o ? s2[threadIdx.x - o] : 0;
       __syncthreads();
@@ -182,13 +115,122 @@ __global__ void __launch_bounds__(1024) plan_tiles_kernel(const PlanArgs a) {
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    *a.n1 = carry1;
-    *a.n2 = carry2;
+    if (a.n1) *a.n1 = carry1;
+    if (a.n2) *a.n2 = carry2;
   }
 }
 
-int launch_plan(const PlanArgs& a, cudaStream_t stream) {
-  plan_tiles_kernel<<<1, 1024, 0, stream>>>(a);
+// codes: c = unit * 2 + (level == 2 ? 0 : 1).  chunk_off[chunk][c] = rows of
+// code c in earlier chunks; code_base[c] = first row of code c.
+__global__ void __launch_bounds__(1024) scan_plan_kernel(const int* __restrict__ cnt_chunk, int nchunks, int E,
+                                                         int* __restrict__ chunk_off, int* __restrict__ code_base,
+                                                         UnitSeg* __restrict__ seg, int* __restrict__ r_total,
+                                                         const PlanArgs a, int do_plan) {
+  __shared__ int s1[1024], s2[1024];
+  __shared__ int carry1, carry2;
+  __shared__ int s_tot[512];
+  const int ncode = 2 * E;
+  for (int c = threadIdx.x; c < ncode; c += blockDim.x) {
+    int run = 0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      chunk_off[static_cast<long long>(ch) * ncode + c] = run;
+      run += cnt_chunk[static_cast<long long>(ch) * ncode + c];
+    }
+    s_tot[c] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int start = 0;
+    for (int u = 0; u < E; ++u) {
+      const int nf = s_tot[2 * u], nm = s_tot[2 * u + 1];
+      seg[u] = UnitSeg{start, nf, nf + nm, 0};
+      code_base[2 * u] = start;
+      code_base[2 * u + 1] = start + nf;
+      start += nf + nm;
+    }
+    *r_total = start;
+  }
+  __syncthreads();
+  if (do_plan) plan_body(a, seg, s1, s2, carry1, carry2);
+}
+
+int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
+                     int* r_total, const PlanArgs* plan, cudaStream_t stream) {
+  if (E > 256) return -1;
+  PlanArgs a{};
+  if (plan) a = *plan;
+  scan_plan_kernel<<<1, 1024, 0, stream>>>(cnt_chunk, nchunks, E, chunk_off, code_base, seg, r_total, a,
+                                           plan != nullptr);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// --------------------------------------------------------------------------
+// scatter: one block per 128-token chunk, slots processed in passes of
+// blockDim in slot order; rank = chunk offset + earlier passes + earlier warps
+// + earlier lanes with the same code.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) scatter_kernel(const int32_t* __restrict__ sel_code,
+                                                       const float* __restrict__ sel_raw, int T, int K, int E,
+                                                       const int* __restrict__ chunk_off,
+                                                       const int* __restrict__ code_base,
+                                                       int32_t* __restrict__ row_token, float* __restrict__ row_scale,
+                                                       int32_t* __restrict__ slot_pos) {
+  extern __shared__ int sm[];
+  const int ncode = 2 * E;
+  const int nwarps = blockDim.x >> 5;
+  int* carry = sm;                 // ncode: rows placed by earlier passes
+  int* wcnt = sm + ncode;          // nwarps x ncode
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int chunk = blockIdx.x;
+  for (int c = threadIdx.x; c < ncode; c += blockDim.x)
+    carry[c] = chunk_off[static_cast<long long>(chunk) * ncode + c] + code_base[c];
+  const long long s0 = static_cast<long long>(chunk) * kRouterChunk * K;
+  const long long s1 = min(static_cast<long long>(T) * K, s0 + static_cast<long long>(kRouterChunk) * K);
+  for (long long p0 = s0; p0 < s1; p0 += blockDim.x) {
+    for (int i = threadIdx.x; i < nwarps * ncode; i += blockDim.x) wcnt[i] = 0;
+    __syncthreads();
+    const long long i = p0 + threadIdx.x;
+    const int code = i < s1 ? sel_code[i] : -1;
+    const int c = code < 0 ? -1 : (code >> 2) * 2 + ((code & 3) == 2 ? 0 : 1);
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    const int rank_w = __popc(grp & ((1u << lane) - 1u));
+    if (c >= 0 && rank_w == 0) wcnt[warp * ncode + c] = __popc(grp);
+    __syncthreads();
+    // exclusive prefix over warps, per code (in place), then advance carry
+    for (int cc = threadIdx.x; cc < ncode; cc += blockDim.x) {
+      int run = carry[cc];
+      for (int w = 0; w < nwarps; ++w) {
+        const int v = wcnt[w * ncode + cc];
+        wcnt[w * ncode + cc] = run;
+        run += v;
+      }
+      carry[cc] = run;
+    }
+    __syncthreads();
+    if (i < s1) {
+      if (c >= 0) {
+        const int pos = wcnt[warp * ncode + c] + rank_w;
+        row_token[pos] = static_cast<int32_t>(i / K);
+        row_scale[pos] = sel_raw[i];
+        slot_pos[i] = pos;
+      } else {
+        slot_pos[i] = -1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+int launch_scatter(const int32_t* sel_code, const float* sel_raw, int T, int K, int E, const int* chunk_off,
+                   const int* code_base, int32_t* row_token, float* row_scale, int32_t* slot_pos, cudaStream_t stream) {
+  const int nchunks = (T + kRouterChunk - 1) / kRouterChunk;
+  const int threads = 1024;
+  const size_t smem = static_cast<size_t>(2 * E) * (1 + threads / 32) * sizeof(int);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (nchunks > 0)
+    scatter_kernel<<<nchunks, threads, smem, stream>>>(sel_code, sel_raw, T, K, E, chunk_off, code_base, row_token,
+                                                       row_scale, slot_pos);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
@@ -248,8 +290,15 @@ __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y,
       }
       for (int s = 0; s < S; ++s) add_row(static_cast<long long>(shared_row0) + static_cast<long long>(s) * T + t);
       TO* o = out + static_cast<long long>(t) * d + static_cast<long long>(v) * V;
+      if constexpr (sizeof(TO) == 2) {
+        uint32_t pk[V / 2];
 #pragma unroll
-      for (int i = 0; i < V; ++i) o[i] = static_cast<TO>(acc[i]);
+        for (int i = 0; i < V / 2; ++i) pk[i] = pack_bf16x2(acc[2 * i], acc[2 * i + 1]);
+        *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(pk);
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) o[i] = static_cast<TO>(acc[i]);
+      }
     }
   }
 }

@@ -2,17 +2,23 @@
 //
 // K1 restates, per token and bit for bit, the routing half of route_and_drop
 // (/root/reference/proj/include/dsmoe/dropping.hpp:248-258):
-//   softmax_inplace      matrix.hpp:68-78   (sequential max, glibc expf, sequential
-//                                            float sum in ascending e, IEEE divide)
+//   softmax_inplace      matrix.hpp:68-78   (max, glibc expf, float sum in
+//                                            ascending e, IEEE divide)
 //   topk_route           moe.hpp:181-206    (K argmax rounds, strict >, lower index wins)
 //   replay_routing       moe.hpp:277-309    (copy-major slots p*K+s, index e*P+p)
 //   normalize_topk       dropping.hpp:60-72 (double sum over base_k in slot order)
 //   apply_bands_fn       dropping.hpp:93-122 (1T/2T bands, keep-top-1 guard)
 //   + per-owner-device thresholds of simulate_step (ep_sim.hpp:139-149) for EP.
-// It also emits the forward metadata the permute kernel consumes: per original
+// One warp per token: lanes hold experts e = lane + 32 j.  The max and the
+// arg-max rounds are order-independent, so they run as warp shuffles; the
+// softmax denominator is order-dependent, so lane 0 adds the exponentials in
+// ascending e exactly like the reference loop.
+//
+// It also emits the forward metadata the scatter kernel consumes: per original
 // selection (t, s) the expert unit and its level (2 = every sub-block, 1 =
-// major sub-block only, 0 = dropped), per-unit row counts, and the retained
-// copy counters drop_stats (dropping.hpp:171-195) is computed from.
+// major sub-block only, 0 = dropped), per-chunk (128 tokens) histograms of
+// (unit, level), and the retained-copy counters drop_stats
+// (dropping.hpp:171-195) is computed from.
 //
 // This translation unit is compiled with -fmad=false: every float / double
 // operation rounds exactly where the reference's (-ffp-contract=off) does.
@@ -20,65 +26,124 @@
 
 namespace dsb {
 
-constexpr int kMaxK = 16;  // Top-K selections per token supported on device
+constexpr int kMaxK = 16;     // Top-K selections per token supported on device
+constexpr int kMaxEPL = 8;    // experts per lane (E <= 256)
+constexpr int kRouterWarps = 16;
 
-__global__ void __launch_bounds__(128) router_kernel(const RouterArgs a) {
-  extern __shared__ float sm[];
-  const int E = a.E, K = a.K, P = a.P;
-  const int ld = E + 1;
-  const int t0 = blockIdx.x * blockDim.x;
-  const int nt = min(static_cast<int>(blockDim.x), a.T - t0);
-  // coalesced stage of this block's logits rows
-  for (int i = threadIdx.x; i < nt * E; i += blockDim.x) {
-    const int r = i / E, c = i - r * E;
-    sm[r * ld + c] = a.logits[static_cast<long long>(t0 + r) * a.ld_logits + c];
+// glibc expf (expf_glibc.h) with the 2^(i/32) table staged in shared memory:
+// lanes index it divergently, which serialises in the constant cache.
+__device__ __forceinline__ float expf_tab(float x, const uint64_t* tab) {
+  const uint32_t abstop = (__float_as_uint(x) >> 20) & 0x7ff;
+  if (abstop >= 0x42b) {
+    if (__float_as_uint(x) == 0xff800000u) return 0.0f;
+    if (abstop >= 0x7f8) return x + x;
+    if (x > 0x1.62e42ep6f) return __uint_as_float(0x7f800000u);
+    if (x < -0x1.9fe368p6f) return 0.0f;
   }
+  const double InvLn2N = 0x1.71547652b82fep+5, SHIFT = 0x1.8p+52;
+  const double C0 = 0x1.c6af84b912394p-20, C1 = 0x1.ebfce50fac4f3p-13, C2 = 0x1.62e42ff0c52d6p-6;
+  const double xd = static_cast<double>(x);
+  double kd = __fma_rn(InvLn2N, xd, SHIFT);
+  const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(kd));
+  kd = __dsub_rn(kd, SHIFT);
+  const double r = __fma_rn(InvLn2N, xd, -kd);
+  const double s = __longlong_as_double(static_cast<long long>(tab[ki % 32] + (ki << 47)));
+  const double y = __fma_rn(__fma_rn(C0, r, C1), __dmul_rn(r, r), __fma_rn(C2, r, 1.0));
+  return static_cast<float>(__dmul_rn(y, s));
+}
+
+__global__ void __launch_bounds__(kRouterWarps * 32) router_kernel(const RouterArgs a) {
+  extern __shared__ int s_hist[];  // 2E codes: [unit*2 + (level==2 ? 0 : 1)]
+  __shared__ uint64_t tab[32];
   __shared__ unsigned long long s_n1, s_nh;
+  const int E = a.E, K = a.K, P = a.P;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) s_hist[i] = 0;
+  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
   if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }
   __syncthreads();
+  const int epl = (E + 31) >> 5;
   unsigned long long n1 = 0, nh = 0;
-  const int tl = threadIdx.x;
-  if (tl < nt) {
-    const int t = t0 + tl;
-    float* v = sm + tl * ld;
-    // softmax_inplace: mx = std::max(mx, x) over the row
-    float mx = v[0];
-    for (int e = 0; e < E; ++e) mx = (mx < v[e]) ? v[e] : mx;
-    float sum = 0.0f;
-    for (int e = 0; e < E; ++e) {
-      const float ex = glibc_expf(__fsub_rn(v[e], mx));
-      v[e] = ex;
-      sum = __fadd_rn(sum, ex);
+  const int t_begin = blockIdx.x * kRouterChunk;
+  const int t_end = min(a.T, t_begin + kRouterChunk);
+  for (int t = t_begin + warp; t < t_end; t += kRouterWarps) {
+    const float* row = a.logits + static_cast<long long>(t) * a.ld_logits;
+    float v[kMaxEPL];
+#pragma unroll
+    for (int j = 0; j < kMaxEPL; ++j) {
+      const int e = lane + 32 * j;
+      v[j] = (j < epl && e < E) ? row[e] : -INFINITY;
     }
-    for (int e = 0; e < E; ++e) v[e] = __fdiv_rn(v[e], sum);
-    // topk_route
+    // softmax_inplace
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kMaxEPL; ++j) mx = (mx < v[j]) ? v[j] : mx;
+    for (int o = 16; o > 0; o >>= 1) {
+      const float other = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = (mx < other) ? other : mx;
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxEPL; ++j) {
+      const int e = lane + 32 * j;
+      v[j] = (j < epl && e < E) ? expf_tab(__fsub_rn(v[j], mx), tab) : 0.0f;
+    }
+    float sum = 0.0f;  // sequential in ascending e (on every lane, same order)
+#pragma unroll
+    for (int j = 0; j < kMaxEPL; ++j) {
+      if (j >= epl) break;
+      for (int l = 0; l < 32; ++l) {
+        const float ex = __shfl_sync(0xffffffffu, v[j], l);
+        if (32 * j + l < E) sum = __fadd_rn(sum, ex);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxEPL; ++j) v[j] = __fdiv_rn(v[j], sum);
+    // topk_route: K arg-max rounds over the untaken experts
+    unsigned taken = 0;  // bit j: expert lane + 32 j already selected
     int sel[kMaxK];
     float sraw[kMaxK];
-    unsigned long long taken[4] = {0, 0, 0, 0};
-    for (int j = 0; j < K; ++j) {
-      int best = -1;
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s) {
+      sel[s] = 0;
+      sraw[s] = 0.f;
+      if (s >= K) continue;
       float bv = 0.f;
-      for (int e = 0; e < E; ++e) {
-        if ((taken[e >> 6] >> (e & 63)) & 1ull) continue;
-        if (best < 0 || v[e] > bv) { best = e; bv = v[e]; }
+      int be = -1;
+#pragma unroll
+      for (int j = 0; j < kMaxEPL; ++j) {
+        const int e = lane + 32 * j;
+        if (j >= epl || e >= E || ((taken >> j) & 1u)) continue;
+        if (be < 0 || v[j] > bv) { bv = v[j]; be = e; }
       }
-      taken[best >> 6] |= 1ull << (best & 63);
-      sel[j] = best;
-      sraw[j] = bv;
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+        const bool take = oe >= 0 && (be < 0 || ov > bv || (ov == bv && oe < be));
+        if (take) { bv = ov; be = oe; }
+      }
+      sel[s] = be;
+      sraw[s] = bv;
+      if ((be & 31) == lane) taken |= 1u << (be >> 5);
     }
-    // ensure_normalized / normalize_topk
+    // normalize_topk / ensure_normalized
     double dsum = 0.0;
     if (a.normalize) {
-      for (int j = 0; j < K; ++j) dsum = __dadd_rn(dsum, static_cast<double>(sraw[j]));
-      if (!(dsum > 0.0)) atomicOr(&a.counters[2], 1ull);
+#pragma unroll
+      for (int s = 0; s < kMaxK; ++s)
+        if (s < K) dsum = __dadd_rn(dsum, static_cast<double>(sraw[s]));
+      if (!(dsum > 0.0) && lane == 0) atomicOr(&a.counters[2], 1ull);
     }
     double ns[kMaxK];
-    for (int j = 0; j < K; ++j)
-      ns[j] = a.normalize ? __ddiv_rn(static_cast<double>(sraw[j]), dsum) : static_cast<double>(sraw[j]);
-    // apply_bands_fn: level 2 = keep all copies, 1 = major part, 0 = drop
     int level[kMaxK];
     int top_slot = 0;
-    for (int s = 0; s < K; ++s) {
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s)
+      ns[s] = a.normalize ? __ddiv_rn(static_cast<double>(sraw[s]), dsum) : static_cast<double>(sraw[s]);
+    // apply_bands_fn
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s) {
+      level[s] = 0;
+      if (s >= K) continue;
       if (ns[s] > ns[top_slot]) top_slot = s;
       if (a.kind == 0) { level[s] = 2; continue; }
       double tmaj = a.t_major, tmin = a.t_minor;
@@ -89,42 +154,48 @@ __global__ void __launch_bounds__(128) router_kernel(const RouterArgs a) {
       }
       level[s] = ns[s] >= tmin ? 2 : (ns[s] >= tmaj ? 1 : 0);
     }
-    if (a.kind != 0 && a.keep_top1) level[top_slot] = 2;
-    // outputs
-    const long long kp = static_cast<long long>(K) * P;
-    for (int s = 0; s < K; ++s) {
-      const int lv = level[s];
-      for (int cp = 0; cp < P; ++cp) {
-        // fraction code of copy cp: P == 1 -> {0, 0.5, 1}; P > 1 -> copy 0 kept
-        // unless dropped, copies >= 1 kept only in the full band.
-        uint8_t fc;
-        if (P == 1) fc = static_cast<uint8_t>(lv);  // 2 -> 1.0, 1 -> 0.5
-        else fc = (cp == 0) ? (lv > 0 ? 2 : 0) : (lv == 2 ? 2 : 0);
-        n1 += fc == 2;
-        nh += fc == 1;
-        const long long f = t * kp + static_cast<long long>(cp) * K + s;
-        if (a.idx) a.idx[f] = sel[s] * P + cp;
-        if (a.raw) a.raw[f] = sraw[s];
-        if (a.norm) a.norm[f] = ns[s];
-        if (a.frac) a.frac[f] = fc;
+    if (a.kind != 0 && a.keep_top1) {
+#pragma unroll
+      for (int s = 0; s < kMaxK; ++s)
+        if (s == top_slot) level[s] = 2;
+    }
+    // outputs: lane-parallel over slots
+    const int kp = K * P;
+    for (int f = lane; f < kp; f += 32) {
+      const int s = f % K, cp = f / K;
+      int lv = 0, e = 0;
+      float rw = 0.f;
+      double nv = 0.0;
+#pragma unroll
+      for (int q = 0; q < kMaxK; ++q)
+        if (q == s) { lv = level[q]; e = sel[q]; rw = sraw[q]; nv = ns[q]; }
+      const uint8_t fc = P == 1 ? static_cast<uint8_t>(lv) : (cp == 0 ? (lv > 0 ? 2 : 0) : (lv == 2 ? 2 : 0));
+      n1 += fc == 2;
+      nh += fc == 1;
+      const long long g = static_cast<long long>(t) * kp + f;
+      if (a.idx) a.idx[g] = e * P + cp;
+      if (a.raw) a.raw[g] = rw;
+      if (a.norm) a.norm[g] = nv;
+      if (a.frac) a.frac[g] = fc;
+      if (cp == 0) {
+        const long long q = static_cast<long long>(t) * K + s;
+        a.sel_code[q] = lv > 0 ? e * 4 + lv : -1;
+        a.sel_raw[q] = rw;
+        if (lv > 0) atomicAdd(&s_hist[2 * e + (lv == 2 ? 0 : 1)], 1);
       }
-      const long long g = static_cast<long long>(t) * K + s;
-      a.sel_code[g] = lv > 0 ? sel[s] * 4 + lv : -1;
-      a.sel_raw[g] = sraw[s];
-      a.slot_pos[g] = -1;
-      if (lv > 0) atomicAdd(&a.cnt[2 * sel[s] + (lv == 2 ? 0 : 1)], 1);
     }
   }
-  // block-reduce the retained-copy counters
   for (int o = 16; o > 0; o >>= 1) {
     n1 += __shfl_xor_sync(0xffffffffu, n1, o);
     nh += __shfl_xor_sync(0xffffffffu, nh, o);
   }
-  if ((threadIdx.x & 31) == 0) {
+  if (lane == 0) {
     atomicAdd(&s_n1, n1);
     atomicAdd(&s_nh, nh);
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < 2 * E; i += blockDim.x)
+    a.cnt_chunk[static_cast<long long>(blockIdx.x) * 2 * E + i] = s_hist[i];
   if (threadIdx.x == 0) {
     atomicAdd(&a.counters[0], s_n1);
     atomicAdd(&a.counters[1], s_nh);
@@ -132,12 +203,10 @@ __global__ void __launch_bounds__(128) router_kernel(const RouterArgs a) {
 }
 
 int launch_router(const RouterArgs& a, cudaStream_t stream) {
-  if (a.K > kMaxK || a.E > 256 || a.K < 1 || a.K > a.E) return -1;
-  const int threads = 128;
-  const int blocks = (a.T + threads - 1) / threads;
-  const size_t smem = static_cast<size_t>(threads) * (a.E + 1) * sizeof(float);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(router_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (blocks > 0) router_kernel<<<blocks, threads, smem, stream>>>(a);
+  if (a.K > kMaxK || a.E > 32 * kMaxEPL || a.K < 1 || a.K > a.E) return -1;
+  const int blocks = (a.T + kRouterChunk - 1) / kRouterChunk;
+  const size_t smem = static_cast<size_t>(2 * a.E) * sizeof(int);
+  if (blocks > 0) router_kernel<<<blocks, kRouterWarps * 32, smem, stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
@@ -148,44 +217,54 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
 // with index (e/P)*P+cp, copies >= 1 sharing one fraction, copy 0 kept whenever
 // any copy is, equal raw scores across copies; P == 1 allows fraction 0.5.
 // Anything else sets error bit 2 (the host reports invalid_state).
+// One block per 128-token chunk, one thread per token.
 // ---------------------------------------------------------------------------
-__global__ void import_routing_kernel(const ImportArgs a) {
-  const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (g >= static_cast<long long>(a.T) * a.K) return;
-  const int t = static_cast<int>(g / a.K), s = static_cast<int>(g - static_cast<long long>(t) * a.K);
-  const long long kp = static_cast<long long>(a.K) * a.P;
-  const long long f0 = t * kp + s;
-  const int e0 = a.idx[f0];
-  const double fr0 = a.frac[f0];
-  const double r0 = a.raw[f0];
-  bool ok = e0 >= 0 && e0 < a.nphys && (e0 % a.P) == 0;
-  int lv = 0;
-  if (a.P == 1) {
-    ok = ok && (fr0 == 0.0 || fr0 == 0.5 || fr0 == 1.0);
-    lv = fr0 == 1.0 ? 2 : (fr0 == 0.5 ? 1 : 0);
-  } else {
-    const double fr1 = a.frac[f0 + a.K];
-    ok = ok && (fr0 == 0.0 || fr0 == 1.0) && (fr1 == 0.0 || fr1 == 1.0) && !(fr0 == 0.0 && fr1 != 0.0);
-    for (int cp = 1; cp < a.P; ++cp) {
-      const long long f = f0 + static_cast<long long>(cp) * a.K;
-      ok = ok && a.idx[f] == e0 + cp && a.frac[f] == fr1 && a.raw[f] == r0;
+__global__ void __launch_bounds__(kRouterChunk) import_routing_kernel(const ImportArgs a) {
+  extern __shared__ int s_hist[];
+  for (int i = threadIdx.x; i < 2 * a.nunits; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+  const int t = blockIdx.x * kRouterChunk + threadIdx.x;
+  if (t < a.T) {
+    const long long kp = static_cast<long long>(a.K) * a.P;
+    for (int s = 0; s < a.K; ++s) {
+      const long long f0 = t * kp + s;
+      const int e0 = a.idx[f0];
+      const double fr0 = a.frac[f0];
+      const double r0 = a.raw[f0];
+      bool ok = e0 >= 0 && e0 < a.nphys && (e0 % a.P) == 0;
+      int lv = 0;
+      if (a.P == 1) {
+        ok = ok && (fr0 == 0.0 || fr0 == 0.5 || fr0 == 1.0);
+        lv = fr0 == 1.0 ? 2 : (fr0 == 0.5 ? 1 : 0);
+      } else {
+        const double fr1 = a.frac[f0 + a.K];
+        ok = ok && (fr0 == 0.0 || fr0 == 1.0) && (fr1 == 0.0 || fr1 == 1.0) && !(fr0 == 0.0 && fr1 != 0.0);
+        for (int cp = 1; cp < a.P; ++cp) {
+          const long long f = f0 + static_cast<long long>(cp) * a.K;
+          ok = ok && a.idx[f] == e0 + cp && a.frac[f] == fr1 && a.raw[f] == r0;
+        }
+        lv = fr0 == 0.0 ? 0 : (fr1 == 1.0 ? 2 : 1);
+      }
+      if (!ok) {
+        atomicOr(&a.counters[2], 4ull);
+        lv = 0;
+      }
+      const int unit = ok ? e0 / a.P : 0;
+      const long long g = static_cast<long long>(t) * a.K + s;
+      a.sel_code[g] = lv > 0 ? unit * 4 + lv : -1;
+      a.sel_raw[g] = static_cast<float>(r0);
+      if (lv > 0) atomicAdd(&s_hist[2 * unit + (lv == 2 ? 0 : 1)], 1);
     }
-    lv = fr0 == 0.0 ? 0 : (fr1 == 1.0 ? 2 : 1);
   }
-  if (!ok) {
-    atomicOr(&a.counters[2], 4ull);
-    lv = 0;
-  }
-  const int unit = e0 / a.P;
-  a.sel_code[g] = lv > 0 ? unit * 4 + lv : -1;
-  a.sel_raw[g] = static_cast<float>(r0);
-  a.slot_pos[g] = -1;
-  if (lv > 0) atomicAdd(&a.cnt[2 * unit + (lv == 2 ? 0 : 1)], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * a.nunits; i += blockDim.x)
+    a.cnt_chunk[static_cast<long long>(blockIdx.x) * 2 * a.nunits + i] = s_hist[i];
 }
 
 int launch_import_routing(const ImportArgs& a, cudaStream_t stream) {
-  const long long n = static_cast<long long>(a.T) * a.K;
-  if (n > 0) import_routing_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, stream>>>(a);
+  const int blocks = (a.T + kRouterChunk - 1) / kRouterChunk;
+  if (blocks > 0)
+    import_routing_kernel<<<blocks, kRouterChunk, static_cast<size_t>(2 * a.nunits) * sizeof(int), stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

@@ -94,6 +94,8 @@ SYMBOLS = {
     "dsmoe_b200_ctx_check": (C.c_int, [C.c_void_p]),
     "dsmoe_b200_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "dsmoe_b200_ctx_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_long)]),
+    "dsmoe_b200_ctx_permutation": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                             C.c_void_p, C.POINTER(C.c_int)]),
     "dsmoe_b200_route": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
                                    C.c_void_p, C.c_void_p, C.POINTER(RoutingOut), C.POINTER(DropStatsC)]),
     "dsmoe_b200_moe_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
@@ -278,6 +280,17 @@ class Context:
         out["calls"] = calls.value
         return out
 
+    def permutation(self, T: int, K: int, E: int):
+        """(row_token, slot_pos T x K, seg E x 3) of the last forward (numpy)."""
+        R = C.c_int()
+        _chk(lib().dsmoe_b200_ctx_permutation(self.h, T, K, E, None, None, None, C.byref(R)))
+        rt = np.empty(max(R.value, 1), np.int32)
+        sp = np.empty(T * K, np.int32)
+        sg = np.empty(3 * E, np.int32)
+        _chk(lib().dsmoe_b200_ctx_permutation(self.h, T, K, E, rt.ctypes.data, sp.ctypes.data, sg.ctypes.data,
+                                              C.byref(R)))
+        return rt[:R.value], sp.reshape(T, K), sg.reshape(E, 3)
+
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and _lib is not None:
@@ -431,3 +444,32 @@ def place_experts(num_experts: int, devices: int, strategy: str = "contiguous") 
     if num_experts % devices:
         raise DsmoeError(1, "place_experts: contiguous placement needs num_experts divisible by devices")
     return (np.arange(num_experts) // (num_experts // devices)).astype(np.int32)
+
+
+# ------------------------------------------------- offline reconstruction (K7/K8)
+def profile_importance(ctx: Context, layer: MoeLayer, calib, indices, metric="abs_gate"):
+    """profile_importance (reconstruct.hpp:99-149) on the device: E x d_ffn
+    float64 importance, bit-equal to the reference on the same inputs.
+    `indices` are the layer's own routing (route_tokens, T x K)."""
+    torch = _torch()
+    x = _x(calib, layer)
+    idx = indices.to(device=x.device, dtype=torch.int32).contiguous()
+    if idx.numel() != x.shape[0] * layer.K:
+        raise DsmoeError(1, "profile_importance: routing does not match calibration batch")
+    vals = torch.empty((layer.E, layer.ffn), dtype=torch.float64, device=x.device)
+    _chk(lib().dsmoe_b200_profile_importance(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
+                                             C.c_void_p(idx.data_ptr()), METRIC[metric.replace("-", "_")],
+                                             C.c_void_p(vals.data_ptr())))
+    return vals
+
+
+def reconstruct_experts(ctx: Context, layer: MoeLayer, values):
+    """build_reconstruction_map + reconstruct_experts (reconstruct.hpp:151-230)
+    on the device: returns (reconstructed MoeLayer with P=2, order E x d_ffn)."""
+    torch = _torch()
+    values = values.to(device="cuda", dtype=torch.float64).contiguous()
+    order = torch.empty((layer.E, layer.ffn), dtype=torch.int32, device=values.device)
+    h = C.c_void_p()
+    _chk(lib().dsmoe_b200_reconstruct(ctx.h, layer.h, C.c_void_p(values.data_ptr()), C.c_void_p(order.data_ptr()),
+                                      C.byref(h)))
+    return MoeLayer._wrap(h, layer, 2), order
