@@ -556,6 +556,8 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
   PlanArgs pa{};
   pa.units = L->d_units.as<UnitInfo>();
   pa.seg_routed = C->seg.as<UnitSeg>();
+  pa.seg_unit = nullptr;
+  pa.shared_unit0 = L->E;
   pa.num_routed = L->E;
   pa.num_shared = L->S;
   pa.T = T;

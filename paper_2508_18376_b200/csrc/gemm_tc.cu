@@ -4,14 +4,15 @@
 // (/root/reference/proj/include/dsmoe/moe.hpp:213-231) and the gate matmul of
 // gate_scores (moe.hpp:174 -> matrix.hpp:47-64) for bf16 layers.
 //
-// One CTA per SM (192 threads, warp-specialised):
+// One CTA per SM (320 threads, warp-specialised):
 //   warp 0      TMA producer: A (128 x 64) and B (N x 64) bf16 tiles, SWIZZLE_128B,
 //               4-stage smem ring guarded by full/empty mbarriers;
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256,
 //               K=16 per instruction), fp32 accumulators in TMEM, two
 //               accumulator stages (2 x 256 columns) so the epilogue of tile i
 //               overlaps the MMAs of tile i+1;
-//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global.
+//   warps 2..9  epilogue (two warps per TMEM lane quarter, alternating 32-column
+//               chunks): tcgen05.ld 32x32b -> registers -> fused op -> global.
 // Work items (GemmTile) are produced on the device by plan_tiles (permute.cu)
 // and walked in a static round-robin over the persistent CTAs.
 //
@@ -30,7 +31,8 @@ constexpr int kStages = 4;
 constexpr int kABytes = kTileM * kTileK * 2;       // 16 KB
 constexpr int kBBytesMax = 256 * kTileK * 2;       // 32 KB
 constexpr int kStageBytes = kABytes + kBBytesMax;  // 48 KB
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 320;  // producer, MMA, 8 epilogue warps
+constexpr int kEpiThreads = 256;
 constexpr int kAccCols = 256;
 constexpr int kGemmSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 128);
+      mbar_init(&tempty[s], kEpiThreads);
     }
     fence_mbar_init();
     tma_prefetch(&mapA);
@@ -139,8 +141,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue warps 2..5
+    // ---------------- epilogue warps 2..9: two per TMEM lane quarter, 32-column
+    // chunks interleaved between them
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int nc = tl.n_mma >> 1;
         const bool live = r < (tl.m_live & 0xFFFFF);
         __nv_bfloat16* H = static_cast<__nv_bfloat16*>(args.out) + orow * args.ldo + tl.out_col;
-        for (int c = 0; c < nc; c += 32) {
+        for (int c = 32 * half; c < nc; c += 64) {
           uint32_t g[32], u[32];
           tmem_ld32(taddr + c, g);
           tmem_ld32(taddr + nc + c, u);
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       } else if constexpr (MODE == kEpiScale) {
         const float sc = valid ? args.row_scale[orow] : 0.f;
         __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(args.out) + orow * args.ldo + tl.out_col;
-        for (int c = 0; c < tl.n_mma; c += 32) {
+        for (int c = 32 * half; c < tl.n_mma; c += 64) {
           uint32_t v[32];
           tmem_ld32(taddr + c, v);
           tmem_ld_wait();
@@ -197,7 +201,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       } else {
         float* O = static_cast<float*>(args.out) + orow * args.ldo + tl.out_col;
-        for (int c = 0; c < tl.n_mma; c += 32) {
+        for (int c = 32 * half; c < tl.n_mma; c += 64) {
           uint32_t v[32];
           tmem_ld32(taddr + c, v);
           tmem_ld_wait();

@@ -37,7 +37,7 @@ struct ImportArgs {
   int* cnt_chunk;
   unsigned long long* counters;
 };
-constexpr int kRouterChunk = 128;  // tokens per router block / scatter chunk
+constexpr int kRouterChunk = 32;  // tokens per router block (one warp each) / scatter chunk
 int launch_router(const RouterArgs& a, cudaStream_t stream);
 int launch_import_routing(const ImportArgs& a, cudaStream_t stream);
 int launch_gate_logits_exact(const void* x, int x_bf16, const float* gate, float* out, int T, int d,
@@ -46,7 +46,9 @@ int launch_gate_logits_exact(const void* x, int x_bf16, const float* gate, float
 // permute.cu
 struct PlanArgs {
   const UnitInfo* units;
-  const UnitSeg* seg_routed;
+  const UnitSeg* seg_routed;   // num_routed segments
+  const int* seg_unit;         // optional: unit (index into units) of each segment; identity if null
+  int shared_unit0;            // index of the first shared unit in units
   int num_routed, num_shared;
   int T, d;
   int shared_row0;
@@ -57,6 +59,7 @@ struct PlanArgs {
 };
 int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
                      int* r_total, const PlanArgs* plan, cudaStream_t stream);
+int launch_plan(const PlanArgs& a, cudaStream_t stream);
 int launch_scatter(const int32_t* sel_code, const float* sel_raw, int T, int K, int E, const int* chunk_off,
                    const int* code_base, int32_t* row_token, float* row_scale, int32_t* slot_pos, cudaStream_t stream);
 int launch_gather(const void* x, void* xp, const int32_t* row_token, const int* r_total,

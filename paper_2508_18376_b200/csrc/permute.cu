@@ -24,119 +24,139 @@ __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
 // --------------------------------------------------------------------------
 // scan + plan (one block of 1024 threads)
 // --------------------------------------------------------------------------
-__device__ __forceinline__ UnitSeg plan_seg(const PlanArgs& a, const UnitSeg* seg, int u) {
-  if (u < a.num_routed) return seg[u];
-  const int s = u - a.num_routed;
-  return UnitSeg{a.shared_row0 + s * a.T, a.T, a.T, 0};
-}
+constexpr int kPlanMaxUnits = 2048;
 
-__device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* s1, int* s2, int& carry1, int& carry2) {
-  if (threadIdx.x == 0) { carry1 = 0; carry2 = 0; }
-  __syncthreads();
+// Work lists.  GEMM1 tiles of a unit: m-tile major; for m-tiles holding full
+// rows every sub-block's chunks, afterwards only sub-block 0's.  GEMM2 tiles:
+// m-tile major, then d_model tiles.  Minor sub-blocks get tiles only for the
+// full rows, so FLOPs fall with the drop rate (no masks).
+__device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int* off2) {
   const int nu = a.num_routed + a.num_shared;
   const int ntd = cdiv(a.d, kTileN2);
-  for (int u0 = 0; u0 < nu; u0 += blockDim.x) {
-    const int u = u0 + threadIdx.x;
-    int c1 = 0, c2 = 0;
-    UnitSeg sg{0, 0, 0, 0};
-    UnitInfo ui{};
-    if (u < nu) {
-      ui = a.units[u];
-      sg = plan_seg(a, seg, u);
-      const int mt_all = cdiv(sg.n_tot, kTileM), mt_full = cdiv(sg.n_full, kTileM);
-      for (int p = 0; p < ui.nsub; ++p) c1 += cdiv(ui.sub_wpad[p], kChunk) * (p == 0 ? mt_all : mt_full);
-      c2 = mt_all * ntd;
-    }
-    s1[threadIdx.x] = c1;
-    s2[threadIdx.x] = c2;
-    __syncthreads();
-    for (int o = 1; o < blockDim.x; o <<= 1) {  // inclusive Hillis-Steele scan
-      const int v1 = threadIdx.x >= o ? s1[threadIdx.x - o] : 0;
-      const int v2 = threadIdx.x >= o ? s2[threadIdx.x - o] : 0;
-      __syncthreads();
-      s1[threadIdx.x] += v1;
-      s2[threadIdx.x] += v2;
-      __syncthreads();
-    }
-    const int off1 = carry1 + s1[threadIdx.x] - c1;
-    const int off2 = carry2 + s2[threadIdx.x] - c2;
-    if (u < nu) {
-      const bool sh = ui.shared != 0;
-      const int mt_all = cdiv(sg.n_tot, kTileM), mt_full = cdiv(sg.n_full, kTileM);
-      int k1 = off1;
-      for (int mt = 0; mt < mt_all; ++mt) {
-        const int m_valid = min(kTileM, sg.n_tot - mt * kTileM);
-        int wrow = ui.w13_row, hcol = 0;
-        for (int p = 0; p < ui.nsub; ++p) {
-          const int wp = ui.sub_wpad[p];
-          if (p == 0 || mt < mt_full) {
-            const int live = p == 0 ? m_valid : max(0, min(kTileM, sg.n_full - mt * kTileM));
-            for (int c = 0; c < cdiv(wp, kChunk); ++c) {
-              const int nc = min(kChunk, wp - c * kChunk);
-              GemmTile tl;
-              tl.a_row = sh ? mt * kTileM : sg.start + mt * kTileM;
-              tl.b_row = wrow + 2 * kChunk * c;
-              tl.out_row = sg.start + mt * kTileM;
-              tl.out_col = hcol + kChunk * c;
-              tl.nkb = a.d / kTileK;
-              tl.n_mma = 2 * nc;
-              tl.m_valid = m_valid;
-              tl.m_live = live | (sh ? kTileAltA : 0);
-              a.tiles1[k1++] = tl;
-            }
-          }
-          wrow += 2 * wp;
-          hcol += wp;
-        }
-      }
-      int k2 = off2;
-      for (int mt = 0; mt < mt_all; ++mt) {
-        const int m_valid = min(kTileM, sg.n_tot - mt * kTileM);
-        const int kw = (mt * kTileM < sg.n_full) ? ui.hwidth : ui.sub_wpad[0];
-        for (int nt = 0; nt < ntd; ++nt) {
-          GemmTile tl;
-          tl.a_row = sg.start + mt * kTileM;
-          tl.b_row = ui.w2t_row + nt * kTileN2;
-          tl.out_row = sg.start + mt * kTileM;
-          tl.out_col = nt * kTileN2;
-          tl.nkb = kw / kTileK;
-          tl.n_mma = min(kTileN2, a.d - nt * kTileN2);
-          tl.m_valid = m_valid;
-          tl.m_live = m_valid;
-          a.tiles2[k2++] = tl;
-        }
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) {
-      carry1 += s1[threadIdx.x];
-      carry2 += s2[threadIdx.x];
-    }
-    __syncthreads();
+  auto unit_of = [&](int u) { return u < a.num_routed ? (a.seg_unit ? a.seg_unit[u] : u) : a.shared_unit0 + (u - a.num_routed); };
+  auto seg_of = [&](int u) {
+    if (u < a.num_routed) return seg[u];
+    const int s = u - a.num_routed;
+    return UnitSeg{a.shared_row0 + s * a.T, a.T, a.T, 0};
+  };
+  // tile counts, exclusive scan (single pass: nu <= 2048, two per thread)
+  for (int u = threadIdx.x; u < nu; u += blockDim.x) {
+    const UnitInfo& ui = a.units[unit_of(u)];
+    const UnitSeg sg = seg_of(u);
+    const int mt_all = cdiv(sg.n_tot, kTileM), mt_full = cdiv(sg.n_full, kTileM);
+    int c1 = 0;
+    for (int p = 0; p < ui.nsub; ++p) c1 += cdiv(ui.sub_wpad[p], kChunk) * (p == 0 ? mt_all : mt_full);
+    off1[u + 1] = c1;
+    off2[u + 1] = mt_all * ntd;
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    if (a.n1) *a.n1 = carry1;
-    if (a.n2) *a.n2 = carry2;
+    off1[0] = off2[0] = 0;
+    for (int u = 0; u < nu; ++u) {
+      off1[u + 1] += off1[u];
+      off2[u + 1] += off2[u];
+    }
+    if (a.n1) *a.n1 = off1[nu];
+    if (a.n2) *a.n2 = off2[nu];
+  }
+  __syncthreads();
+  auto find = [&](const int* off, int i) {  // largest u with off[u] <= i
+    int lo = 0, hi = nu - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  };
+  for (int i = threadIdx.x; i < off1[nu]; i += blockDim.x) {
+    const int u = find(off1, i);
+    const UnitInfo& ui = a.units[unit_of(u)];
+    const UnitSeg sg = seg_of(u);
+    const bool sh = ui.shared != 0;
+    const int mt_full = cdiv(sg.n_full, kTileM);
+    int ch_all = 0;
+    for (int p = 0; p < ui.nsub; ++p) ch_all += cdiv(ui.sub_wpad[p], kChunk);
+    const int ch0 = cdiv(ui.sub_wpad[0], kChunk);
+    int li = i - off1[u], mt, r;
+    if (li < mt_full * ch_all) {
+      mt = li / ch_all;
+      r = li - mt * ch_all;
+    } else {
+      li -= mt_full * ch_all;
+      mt = mt_full + li / ch0;
+      r = li - (mt - mt_full) * ch0;
+    }
+    int p = 0, wrow = ui.w13_row, hcol = 0;
+    while (r >= cdiv(ui.sub_wpad[p], kChunk)) {
+      r -= cdiv(ui.sub_wpad[p], kChunk);
+      wrow += 2 * ui.sub_wpad[p];
+      hcol += ui.sub_wpad[p];
+      ++p;
+    }
+    const int c = r;
+    const int nc = min(kChunk, ui.sub_wpad[p] - c * kChunk);
+    const int m_valid = min(kTileM, sg.n_tot - mt * kTileM);
+    const int live = p == 0 ? m_valid : max(0, min(kTileM, sg.n_full - mt * kTileM));
+    GemmTile tl;
+    tl.a_row = sh ? mt * kTileM : sg.start + mt * kTileM;
+    tl.b_row = wrow + 2 * kChunk * c;
+    tl.out_row = sg.start + mt * kTileM;
+    tl.out_col = hcol + kChunk * c;
+    tl.nkb = a.d / kTileK;
+    tl.n_mma = 2 * nc;
+    tl.m_valid = m_valid;
+    tl.m_live = live | (sh ? kTileAltA : 0);
+    a.tiles1[i] = tl;
+  }
+  for (int i = threadIdx.x; i < off2[nu]; i += blockDim.x) {
+    const int u = find(off2, i);
+    const UnitInfo& ui = a.units[unit_of(u)];
+    const UnitSeg sg = seg_of(u);
+    const int li = i - off2[u];
+    const int mt = li / ntd, nt = li - mt * ntd;
+    const int m_valid = min(kTileM, sg.n_tot - mt * kTileM);
+    GemmTile tl;
+    tl.a_row = sg.start + mt * kTileM;
+    tl.b_row = ui.w2t_row + nt * kTileN2;
+    tl.out_row = sg.start + mt * kTileM;
+    tl.out_col = nt * kTileN2;
+    tl.nkb = ((mt * kTileM < sg.n_full) ? ui.hwidth : ui.sub_wpad[0]) / kTileK;
+    tl.n_mma = min(kTileN2, a.d - nt * kTileN2);
+    tl.m_valid = m_valid;
+    tl.m_live = m_valid;
+    a.tiles2[i] = tl;
   }
 }
 
 // codes: c = unit * 2 + (level == 2 ? 0 : 1).  chunk_off[chunk][c] = rows of
-// code c in earlier chunks; code_base[c] = first row of code c.
+// code c in earlier chunks; code_base[c] = first row of code c.  One warp per
+// code: lanes own contiguous runs of chunks, warp-scan of the run sums.
 __global__ void __launch_bounds__(1024) scan_plan_kernel(const int* __restrict__ cnt_chunk, int nchunks, int E,
                                                          int* __restrict__ chunk_off, int* __restrict__ code_base,
                                                          UnitSeg* __restrict__ seg, int* __restrict__ r_total,
                                                          const PlanArgs a, int do_plan) {
-  __shared__ int s1[1024], s2[1024];
-  __shared__ int carry1, carry2;
+  __shared__ int off1[kPlanMaxUnits + 1], off2[kPlanMaxUnits + 1];
   __shared__ int s_tot[512];
   const int ncode = 2 * E;
-  for (int c = threadIdx.x; c < ncode; c += blockDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int q = cdiv(nchunks, 32);
+  for (int c = warp; c < ncode; c += nwarps) {
+    const int ch0 = min(nchunks, lane * q), ch1 = min(nchunks, ch0 + q);
     int run = 0;
-    for (int ch = 0; ch < nchunks; ++ch) {
-      chunk_off[static_cast<long long>(ch) * ncode + c] = run;
-      run += cnt_chunk[static_cast<long long>(ch) * ncode + c];
+    for (int ch = ch0; ch < ch1; ++ch) run += cnt_chunk[static_cast<long long>(ch) * ncode + c];
+    int incl = run;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    s_tot[c] = run;
+    int pos = incl - run;
+    for (int ch = ch0; ch < ch1; ++ch) {
+      const long long k = static_cast<long long>(ch) * ncode + c;
+      const int v = cnt_chunk[k];
+      chunk_off[k] = pos;
+      pos += v;
+    }
+    if (lane == 31) s_tot[c] = incl;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -151,7 +171,7 @@ __global__ void __launch_bounds__(1024) scan_plan_kernel(const int* __restrict__
     *r_total = start;
   }
   __syncthreads();
-  if (do_plan) plan_body(a, seg, s1, s2, carry1, carry2);
+  if (do_plan) plan_body(a, seg, off1, off2);
 }
 
 int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
@@ -161,6 +181,18 @@ int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, i
   if (plan) a = *plan;
   scan_plan_kernel<<<1, 1024, 0, stream>>>(cnt_chunk, nchunks, E, chunk_off, code_base, seg, r_total, a,
                                            plan != nullptr);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// plan only, over caller segments (expert-parallel receive side)
+__global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
+  __shared__ int off1[kPlanMaxUnits + 1], off2[kPlanMaxUnits + 1];
+  plan_body(a, a.seg_routed, off1, off2);
+}
+
+int launch_plan(const PlanArgs& a, cudaStream_t stream) {
+  if (a.num_routed + a.num_shared > kPlanMaxUnits) return -1;
+  plan_kernel<<<1, 1024, 0, stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

@@ -26,9 +26,8 @@
 
 namespace dsb {
 
-constexpr int kMaxK = 16;     // Top-K selections per token supported on device
+constexpr int kMaxK = 32;     // Top-K selections per token supported on device (one lane each)
 constexpr int kMaxEPL = 8;    // experts per lane (E <= 256)
-constexpr int kRouterWarps = 16;
 
 // glibc expf (expf_glibc.h) with the 2^(i/32) table staged in shared memory:
 // lanes index it divergently, which serialises in the constant cache.
@@ -52,7 +51,7 @@ __device__ __forceinline__ float expf_tab(float x, const uint64_t* tab) {
   return static_cast<float>(__dmul_rn(y, s));
 }
 
-__global__ void __launch_bounds__(kRouterWarps * 32) router_kernel(const RouterArgs a) {
+__global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterArgs a) {
   extern __shared__ int s_hist[];  // 2E codes: [unit*2 + (level==2 ? 0 : 1)]
   __shared__ uint64_t tab[32];
   __shared__ unsigned long long s_n1, s_nh;
@@ -64,9 +63,8 @@ __global__ void __launch_bounds__(kRouterWarps * 32) router_kernel(const RouterA
   __syncthreads();
   const int epl = (E + 31) >> 5;
   unsigned long long n1 = 0, nh = 0;
-  const int t_begin = blockIdx.x * kRouterChunk;
-  const int t_end = min(a.T, t_begin + kRouterChunk);
-  for (int t = t_begin + warp; t < t_end; t += kRouterWarps) {
+  const int t = blockIdx.x * kRouterChunk + warp;  // one token per warp
+  if (t < a.T) {
     const float* row = a.logits + static_cast<long long>(t) * a.ld_logits;
     float v[kMaxEPL];
 #pragma unroll
@@ -74,7 +72,7 @@ __global__ void __launch_bounds__(kRouterWarps * 32) router_kernel(const RouterA
       const int e = lane + 32 * j;
       v[j] = (j < epl && e < E) ? row[e] : -INFINITY;
     }
-    // softmax_inplace
+    // softmax_inplace: max (order-free), exp, ordered float sum, divide
     float mx = -INFINITY;
 #pragma unroll
     for (int j = 0; j < kMaxEPL; ++j) mx = (mx < v[j]) ? v[j] : mx;
@@ -83,30 +81,27 @@ __global__ void __launch_bounds__(kRouterWarps * 32) router_kernel(const RouterA
       mx = (mx < other) ? other : mx;
     }
 #pragma unroll
-    for (int j = 0; j < kMaxEPL; ++j) {
-      const int e = lane + 32 * j;
-      v[j] = (j < epl && e < E) ? expf_tab(__fsub_rn(v[j], mx), tab) : 0.0f;
-    }
-    float sum = 0.0f;  // sequential in ascending e (on every lane, same order)
+    for (int j = 0; j < kMaxEPL; ++j)
+      if (j < epl) v[j] = (lane + 32 * j < E) ? expf_tab(__fsub_rn(v[j], mx), tab) : 0.0f;
+    float sum = 0.0f;  // ascending e, identical on every lane
 #pragma unroll
     for (int j = 0; j < kMaxEPL; ++j) {
       if (j >= epl) break;
+      const int lim = min(32, E - 32 * j);
+#pragma unroll 8
       for (int l = 0; l < 32; ++l) {
         const float ex = __shfl_sync(0xffffffffu, v[j], l);
-        if (32 * j + l < E) sum = __fadd_rn(sum, ex);
+        if (l < lim) sum = __fadd_rn(sum, ex);
       }
     }
 #pragma unroll
-    for (int j = 0; j < kMaxEPL; ++j) v[j] = __fdiv_rn(v[j], sum);
-    // topk_route: K arg-max rounds over the untaken experts
+    for (int j = 0; j < kMaxEPL; ++j)
+      if (j < epl) v[j] = __fdiv_rn(v[j], sum);
+    // topk_route: K arg-max rounds; lane s keeps selection s
     unsigned taken = 0;  // bit j: expert lane + 32 j already selected
-    int sel[kMaxK];
-    float sraw[kMaxK];
-#pragma unroll
-    for (int s = 0; s < kMaxK; ++s) {
-      sel[s] = 0;
-      sraw[s] = 0.f;
-      if (s >= K) continue;
+    int my_e = 0;
+    float my_raw = 0.f;
+    for (int s = 0; s < K; ++s) {
       float bv = 0.f;
       int be = -1;
 #pragma unroll
@@ -118,78 +113,64 @@ __global__ void __launch_bounds__(kRouterWarps * 32) router_kernel(const RouterA
       for (int o = 16; o > 0; o >>= 1) {
         const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
         const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-        const bool take = oe >= 0 && (be < 0 || ov > bv || (ov == bv && oe < be));
-        if (take) { bv = ov; be = oe; }
+        if (oe >= 0 && (be < 0 || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
       }
-      sel[s] = be;
-      sraw[s] = bv;
+      if (lane == s) { my_e = be; my_raw = bv; }
       if ((be & 31) == lane) taken |= 1u << (be >> 5);
     }
-    // normalize_topk / ensure_normalized
+    // normalize_topk: ordered double sum over the K selections, then divide
+    const bool active = lane < K;
     double dsum = 0.0;
     if (a.normalize) {
-#pragma unroll
-      for (int s = 0; s < kMaxK; ++s)
-        if (s < K) dsum = __dadd_rn(dsum, static_cast<double>(sraw[s]));
+      for (int s = 0; s < K; ++s) dsum = __dadd_rn(dsum, static_cast<double>(__shfl_sync(0xffffffffu, my_raw, s)));
       if (!(dsum > 0.0) && lane == 0) atomicOr(&a.counters[2], 1ull);
     }
-    double ns[kMaxK];
-    int level[kMaxK];
-    int top_slot = 0;
-#pragma unroll
-    for (int s = 0; s < kMaxK; ++s)
-      ns[s] = a.normalize ? __ddiv_rn(static_cast<double>(sraw[s]), dsum) : static_cast<double>(sraw[s]);
-    // apply_bands_fn
-#pragma unroll
-    for (int s = 0; s < kMaxK; ++s) {
-      level[s] = 0;
-      if (s >= K) continue;
-      if (ns[s] > ns[top_slot]) top_slot = s;
-      if (a.kind == 0) { level[s] = 2; continue; }
-      double tmaj = a.t_major, tmin = a.t_minor;
-      if (a.t_unit) {
-        const double own = a.t_unit[sel[s]];
-        tmaj = __dadd_rn(own, a.maj_off);
-        tmin = __dadd_rn(own, a.min_off);
-      }
-      level[s] = ns[s] >= tmin ? 2 : (ns[s] >= tmaj ? 1 : 0);
+    const double ns = active ? (a.normalize ? __ddiv_rn(static_cast<double>(my_raw), dsum) : static_cast<double>(my_raw))
+                             : -1.0;
+    // top_slot = first maximum of ns (strict >, dropping.hpp:99)
+    double tv = ns;
+    int ts = active ? lane : 1 << 30;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, tv, o);
+      const int os = __shfl_xor_sync(0xffffffffu, ts, o);
+      if (ov > tv || (ov == tv && os < ts)) { tv = ov; ts = os; }
     }
-    if (a.kind != 0 && a.keep_top1) {
-#pragma unroll
-      for (int s = 0; s < kMaxK; ++s)
-        if (s == top_slot) level[s] = 2;
-    }
-    // outputs: lane-parallel over slots
-    const int kp = K * P;
-    for (int f = lane; f < kp; f += 32) {
-      const int s = f % K, cp = f / K;
-      int lv = 0, e = 0;
-      float rw = 0.f;
-      double nv = 0.0;
-#pragma unroll
-      for (int q = 0; q < kMaxK; ++q)
-        if (q == s) { lv = level[q]; e = sel[q]; rw = sraw[q]; nv = ns[q]; }
-      const uint8_t fc = P == 1 ? static_cast<uint8_t>(lv) : (cp == 0 ? (lv > 0 ? 2 : 0) : (lv == 2 ? 2 : 0));
-      n1 += fc == 2;
-      nh += fc == 1;
-      const long long g = static_cast<long long>(t) * kp + f;
-      if (a.idx) a.idx[g] = e * P + cp;
-      if (a.raw) a.raw[g] = rw;
-      if (a.norm) a.norm[g] = nv;
-      if (a.frac) a.frac[g] = fc;
-      if (cp == 0) {
-        const long long q = static_cast<long long>(t) * K + s;
-        a.sel_code[q] = lv > 0 ? e * 4 + lv : -1;
-        a.sel_raw[q] = rw;
-        if (lv > 0) atomicAdd(&s_hist[2 * e + (lv == 2 ? 0 : 1)], 1);
+    // apply_bands_fn on this lane's selection
+    int lv = 0;
+    if (active) {
+      if (a.kind == 0) {
+        lv = 2;
+      } else {
+        double tmaj = a.t_major, tmin = a.t_minor;
+        if (a.t_unit) {
+          const double own = a.t_unit[my_e];
+          tmaj = __dadd_rn(own, a.maj_off);
+          tmin = __dadd_rn(own, a.min_off);
+        }
+        lv = ns >= tmin ? 2 : (ns >= tmaj ? 1 : 0);
+        if (a.keep_top1 && lane == ts) lv = 2;
       }
+      for (int cp = 0; cp < P; ++cp) {
+        const uint8_t fc = P == 1 ? static_cast<uint8_t>(lv) : (cp == 0 ? (lv > 0 ? 2 : 0) : (lv == 2 ? 2 : 0));
+        n1 += fc == 2;
+        nh += fc == 1;
+        const long long g = static_cast<long long>(t) * K * P + static_cast<long long>(cp) * K + lane;
+        if (a.idx) a.idx[g] = my_e * P + cp;
+        if (a.raw) a.raw[g] = my_raw;
+        if (a.norm) a.norm[g] = ns;
+        if (a.frac) a.frac[g] = fc;
+      }
+      const long long q = static_cast<long long>(t) * K + lane;
+      a.sel_code[q] = lv > 0 ? my_e * 4 + lv : -1;
+      a.sel_raw[q] = my_raw;
+      if (lv > 0) atomicAdd(&s_hist[2 * my_e + (lv == 2 ? 0 : 1)], 1);
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
     n1 += __shfl_xor_sync(0xffffffffu, n1, o);
     nh += __shfl_xor_sync(0xffffffffu, nh, o);
   }
-  if (lane == 0) {
+  if (lane == 0 && (n1 | nh)) {
     atomicAdd(&s_n1, n1);
     atomicAdd(&s_nh, nh);
   }
@@ -206,7 +187,7 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
   if (a.K > kMaxK || a.E > 32 * kMaxEPL || a.K < 1 || a.K > a.E) return -1;
   const int blocks = (a.T + kRouterChunk - 1) / kRouterChunk;
   const size_t smem = static_cast<size_t>(2 * a.E) * sizeof(int);
-  if (blocks > 0) router_kernel<<<blocks, kRouterWarps * 32, smem, stream>>>(a);
+  if (blocks > 0) router_kernel<<<blocks, kRouterChunk * 32, smem, stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

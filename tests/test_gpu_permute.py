@@ -88,12 +88,11 @@ def test_threshold_boundaries_inclusive(ctx):
     xd = torch.from_numpy(x).cuda()
     r0 = O.route(L, x)
     for tv in (r0.norm[5, 2], r0.norm[17, 1], r0.norm[100, 3]):
-        for kind, pol, kw in (("1t", pkg.DropPolicy.one_t(tv, keep_top1=False), {}),
-                              ("2t", pkg.DropPolicy.two_t(tv, tv, r0.norm[5, 1], keep_top1=False),
-                               {"t_major": tv, "t_minor": r0.norm[5, 1]})):
-            if kind == "2t" and not tv <= r0.norm[5, 1]:
-                continue
-            r = pkg.route_and_drop(ctx, layer, xd, pol, logits_mode=pkg.LOGITS_EXACT)
+        hi = max(tv, r0.norm[5, 1])
+        for kind, mk, kw in (("1t", lambda: pkg.DropPolicy.one_t(tv, keep_top1=False), {}),
+                             ("2t", lambda: pkg.DropPolicy.two_t(tv, tv, hi, keep_top1=False),
+                              {"t_major": tv, "t_minor": hi})):
+            r = pkg.route_and_drop(ctx, layer, xd, mk(), logits_mode=pkg.LOGITS_EXACT)
             ro = O.route(L, x, kind, tv, keep_top1=False, **kw)
             assert np.array_equal(r.host()[3].reshape(ro.frac.shape), ro.frac)
 
