@@ -185,6 +185,33 @@ int dsmoe_b200_forward(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const
                        const dsmoe_b200_policy* policy, int logits_mode, void* out,
                        dsmoe_b200_drop_stats_t* stats);
 
+/* ---- expert parallelism data path (north-star item 6; ep.py drives NCCL) --
+ * Source side: route + drop (policy->t_unit carries the owner-device
+ * thresholds of simulate_step, ep_sim.hpp:133-149), permute, and gather the
+ * kept token rows in the canonical order — experts ascending, so under
+ * contiguous placement (ep_sim.hpp:48-52) the rows for each destination rank
+ * are one contiguous run.  rows_out (device, >= T*K x d_model, layer dtype)
+ * and scale_out (device, >= T*K fp32 raw scores) may be NULL (count only);
+ * seg_out (host, E x 3) = start, full rows, total rows per expert.  Shared
+ * experts are evaluated locally here.  Synchronises the stream. */
+int dsmoe_b200_dispatch(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
+                        const dsmoe_b200_policy* policy, int logits_mode, void* rows_out,
+                        float* scale_out, int32_t* seg_out, int* r_total,
+                        dsmoe_b200_drop_stats_t* stats);
+/* Expert side: grouped SwiGLU FFN (K3 + K4) over caller segments of `rows`
+ * (device, nrows x d_model): segment i = rows [seg_start[i], +seg_ntot[i]) of
+ * expert seg_unit[i], its first seg_nfull[i] rows evaluated on every
+ * sub-block, the rest on the major sub-block only; y_out (device, nrows x
+ * d_model) = row_scale[r] * expert(row r).  Segment arrays are host. */
+int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* rows,
+                          const float* row_scale, long nrows, int nseg, const int32_t* seg_unit,
+                          const int32_t* seg_start, const int32_t* seg_nfull,
+                          const int32_t* seg_ntot, void* y_out);
+/* out (device, T x d_model) = sum over the last dispatch's kept selections of
+ * y_rows (device, dispatch row order) + the local shared experts (K5). */
+int dsmoe_b200_combine(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* y_rows, int T,
+                       void* out);
+
 /* drop_stats from host fraction arrays (n = T*K*P doubles each). */
 int dsmoe_b200_drop_stats(const double* pre_fraction, const double* post_fraction, long n,
                           int replay_factor, int num_shared, long num_tokens, int d_model,

@@ -296,7 +296,7 @@ struct dsmoe_b200_ctx {
   cudaStream_t stream = nullptr;
   DevBuf logits, sel_code, sel_raw, slot_pos, cnt_chunk, chunk_off, code_base, counters, row_token, row_scale, seg,
       scalars;
-  DevBuf tiles1, tiles2, tiles_gate, xperm, H, Y, frac_ws;
+  DevBuf tiles1, tiles2, tiles_gate, xperm, H, Y, frac_ws, vseg, vseg_unit;
   int gate_tiles_T = -1, gate_tiles_Epad = -1, gate_tiles_d = -1;
   long long scale_fill_key = -1;
   unsigned long long last_err_flags = 0;
@@ -351,7 +351,7 @@ struct dsmoe_b200_ctx {
     const size_t nchunks = static_cast<size_t>((T + kRouterChunk - 1) / kRouterChunk);
     cnt_chunk.ensure(nchunks * 2 * L->E * 4 + 16);
     chunk_off.ensure(nchunks * 2 * L->E * 4 + 16);
-    code_base.ensure(static_cast<size_t>(2 * L->E) * 4);
+    code_base.ensure(static_cast<size_t>(4 * L->E) * 4);  // [2E bases | 2E totals]
     counters.ensure(4 * sizeof(unsigned long long));
     row_token.ensure(static_cast<size_t>(Rcap + kTileM) * 4);
     seg.ensure(sizeof(UnitSeg) * L->E);
@@ -569,12 +569,65 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
   pa.n2 = r_total + 2;
   const int nchunks = (T + kRouterChunk - 1) / kRouterChunk;
   launch_check(launch_scan_plan(C->cnt_chunk.as<int>(), nchunks, L->E, C->chunk_off.as<int>(), C->code_base.as<int>(),
-                                C->seg.as<UnitSeg>(), r_total, plan ? &pa : nullptr, s),
+                                C->seg.as<UnitSeg>(), r_total, C->code_base.as<int>() + 2 * L->E, plan ? &pa : nullptr, num_sms(), s),
                "scan/plan");
   launch_check(launch_scatter(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), T, L->K, L->E, C->chunk_off.as<int>(),
                               C->code_base.as<int>(), C->row_token.as<int32_t>(), C->row_scale.as<float>(),
                               C->slot_pos.as<int32_t>(), s),
                "scatter");
+  g_launches += 3;
+}
+
+// K3 + K4 over the work lists at n1/n2: A = `rows` (permuted tokens, a_rows
+// allocated), alt A = x (shared experts), H in the context, Y = y (ld d).
+void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long long a_rows, const void* x,
+               int T, const int* n1, const int* n2, long long max1, long long max2, long long h_rows, void* y,
+               const float* row_scale) {
+  cudaStream_t s = C->stream;
+  const int mt1 = static_cast<int>(std::min<long long>(max1, 1 << 30));
+  const int mt2 = static_cast<int>(std::min<long long>(max2, 1 << 30));
+  if (L->dtype == DSMOE_B200_BF16) {
+    const CUtensorMap mx = make_map(x ? x : rows, x ? T : a_rows, L->d, L->d, kTileM);
+    const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, kTileM);
+    const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, kTileM);
+    C->mark(4);
+    launch_check(launch_gemm_tc(1, &mxp, &mx, &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
+                                nullptr, 256, num_sms(), s),
+                 "gemm1");
+    C->mark(5);
+    launch_check(launch_gemm_tc(2, &mh, &mh, &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,
+                                256, num_sms(), s),
+                 "gemm2");
+  } else {
+    SimtArgs g1{};
+    g1.A = static_cast<const float*>(rows);
+    g1.A2 = static_cast<const float*>(x ? x : rows);
+    g1.lda = L->d;
+    g1.a_rows = a_rows;
+    g1.a2_rows = x ? T : a_rows;
+    g1.B = L->w13.as<float>();
+    g1.ldb = L->d;
+    g1.tiles = C->tiles1.as<GemmTile>();
+    g1.num_tiles = n1;
+    g1.out = C->H.as<float>();
+    g1.ldo = L->hstride;
+    C->mark(4);
+    launch_check(launch_gemm_simt(1, g1, mt1, num_sms(), s), "gemm1 simt");
+    SimtArgs g2{};
+    g2.A = C->H.as<float>();
+    g2.A2 = C->H.as<float>();
+    g2.lda = L->hstride;
+    g2.a_rows = g2.a2_rows = h_rows;
+    g2.B = L->w2t.as<float>();
+    g2.ldb = L->hstride;
+    g2.tiles = C->tiles2.as<GemmTile>();
+    g2.num_tiles = n2;
+    g2.out = static_cast<float*>(y);
+    g2.ldo = L->d;
+    g2.row_scale = row_scale;
+    C->mark(5);
+    launch_check(launch_gemm_simt(2, g2, mt2, num_sms(), s), "gemm2 simt");
+  }
   g_launches += 2;
 }
 
@@ -592,55 +645,13 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   launch_check(launch_gather(x, C->xperm.p, C->row_token.as<int32_t>(), r_total, L->d * es, num_sms(), s), "gather");
   g_launches += 1;
   const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
-  const int mt1 = static_cast<int>(std::min<long long>(C->max_tiles1(L, T), 1 << 30));
-  const int mt2 = static_cast<int>(std::min<long long>(C->max_tiles2(L, T), 1 << 30));
-  if (L->dtype == DSMOE_B200_BF16) {
-    const CUtensorMap mx = make_map(x, T, L->d, L->d, kTileM);
-    const CUtensorMap mxp = make_map(C->xperm.p, Rcap + kTileM, L->d, L->d, kTileM);
-    const CUtensorMap mh = make_map(C->H.p, rows, L->hstride, L->hstride, kTileM);
-    C->mark(4);
-    launch_check(launch_gemm_tc(1, &mxp, &mx, &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
-                                nullptr, 256, num_sms(), s),
-                 "gemm1");
-    C->mark(5);
-    launch_check(launch_gemm_tc(2, &mh, &mh, &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, C->Y.p, L->d,
-                                C->row_scale.as<float>(), 256, num_sms(), s),
-                 "gemm2");
-  } else {
-    SimtArgs g1{};
-    g1.A = C->xperm.as<float>();
-    g1.A2 = static_cast<const float*>(x);
-    g1.lda = L->d;
-    g1.a_rows = Rcap + kTileM;
-    g1.a2_rows = T;
-    g1.B = L->w13.as<float>();
-    g1.ldb = L->d;
-    g1.tiles = C->tiles1.as<GemmTile>();
-    g1.num_tiles = n1;
-    g1.out = C->H.as<float>();
-    g1.ldo = L->hstride;
-    C->mark(4);
-    launch_check(launch_gemm_simt(1, g1, mt1, num_sms(), s), "gemm1 simt");
-    SimtArgs g2{};
-    g2.A = C->H.as<float>();
-    g2.A2 = C->H.as<float>();
-    g2.lda = L->hstride;
-    g2.a_rows = g2.a2_rows = rows;
-    g2.B = L->w2t.as<float>();
-    g2.ldb = L->hstride;
-    g2.tiles = C->tiles2.as<GemmTile>();
-    g2.num_tiles = n2;
-    g2.out = C->Y.as<float>();
-    g2.ldo = L->d;
-    g2.row_scale = C->row_scale.as<float>();
-    C->mark(5);
-    launch_check(launch_gemm_simt(2, g2, mt2, num_sms(), s), "gemm2 simt");
-  }
+  run_gemms(C, L, C->xperm.p, Rcap + kTileM, x, T, n1, n2, C->max_tiles1(L, T), C->max_tiles2(L, T), rows, C->Y.p,
+            C->row_scale.as<float>());
   C->mark(6);
   launch_check(launch_combine(C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d, L->K,
                               L->S, static_cast<int>(Rcap), num_sms(), s),
                "combine");
-  g_launches += 3;
+  g_launches += 1;
 }
 
 void require_layer(const dsmoe_b200_layer* L) {
@@ -899,6 +910,153 @@ int dsmoe_b200_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void*
       }
       stats_from_counts(L, T, h[0], h[1], fh.data(), stats);
     }
+  });
+}
+
+int dsmoe_b200_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                        const dsmoe_b200_policy* policy, int logits_mode, void* rows_out, float* scale_out,
+                        int32_t* seg_out, int* r_total_out, dsmoe_b200_drop_stats_t* stats) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(T >= 1 && x, DSMOE_E_INVALID_ARGUMENT, "dispatch: empty batch");
+    g_launches = 0;
+    const PolicyResolved pol = resolve_policy(L, policy);
+    C->ensure(L, T);
+    cudaStream_t s = C->stream;
+    const bool need_frac = stats && !is_pow2(L->P);
+    if (need_frac) C->frac_ws.ensure(static_cast<size_t>(T) * L->K * L->P);
+    stage_route(C, L, x, T, pol, logits_mode, nullptr, nullptr, nullptr, need_frac ? C->frac_ws.as<uint8_t>() : nullptr);
+    stage_permute(C, L, T, false);
+    int* r_total = C->scalars.as<int>();
+    if (rows_out) {
+      launch_check(launch_gather(x, rows_out, C->row_token.as<int32_t>(), r_total, L->d * esize(L->dtype), num_sms(), s),
+                   "gather");
+      ++g_launches;
+    }
+    if (scale_out)
+      cuda_check(cudaMemcpyAsync(scale_out, C->row_scale.p, sizeof(float) * static_cast<size_t>(T) * L->K,
+                                 cudaMemcpyDeviceToDevice, s),
+                 "scale copy");
+    // shared experts run locally on this rank's tokens (moe.hpp:267-268)
+    if (L->S > 0) {
+      const long long Rcap = static_cast<long long>(T) * L->K;
+      PlanArgs pa{};
+      pa.units = L->d_units.as<UnitInfo>();
+      pa.seg_routed = C->seg.as<UnitSeg>();
+      pa.shared_unit0 = L->E;
+      pa.num_routed = 0;
+      pa.num_shared = L->S;
+      pa.T = T;
+      pa.d = L->d;
+      pa.shared_row0 = static_cast<int>(Rcap);
+      pa.tiles1 = C->tiles1.as<GemmTile>();
+      pa.n1 = r_total + 1;
+      pa.tiles2 = C->tiles2.as<GemmTile>();
+      pa.n2 = r_total + 2;
+      launch_check(launch_plan(pa, num_sms(), s), "plan shared");
+      ++g_launches;
+      const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
+      run_gemms(C, L, x, T, x, T, r_total + 1, r_total + 2, C->max_tiles1(L, T), C->max_tiles2(L, T), rows, C->Y.p,
+                C->row_scale.as<float>());
+    }
+    std::vector<UnitSeg> h(static_cast<size_t>(L->E));
+    unsigned long long cnt[4];
+    cuda_check(cudaMemcpyAsync(h.data(), C->seg.p, sizeof(UnitSeg) * L->E, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaMemcpyAsync(cnt, C->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    if (cnt[2] & 1ull) fail(DSMOE_E_INVALID_ARGUMENT, "normalize_topk: degenerate zero-sum scores");
+    int R = 0;
+    for (int e = 0; e < L->E; ++e) {
+      if (seg_out) {
+        seg_out[3 * e] = h[e].start;
+        seg_out[3 * e + 1] = h[e].n_full;
+        seg_out[3 * e + 2] = h[e].n_tot;
+      }
+      R += h[e].n_tot;
+    }
+    if (r_total_out) *r_total_out = R;
+    if (stats) {
+      std::vector<uint8_t> fh;
+      if (need_frac) {
+        fh.resize(static_cast<size_t>(T) * L->K * L->P);
+        cuda_check(cudaMemcpy(fh.data(), C->frac_ws.p, fh.size(), cudaMemcpyDeviceToHost), "D2H");
+      }
+      stats_from_counts(L, T, cnt[0], cnt[1], fh.data(), stats);
+    }
+  });
+}
+
+int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, const float* row_scale,
+                          long nrows, int nseg, const int32_t* seg_unit, const int32_t* seg_start,
+                          const int32_t* seg_nfull, const int32_t* seg_ntot, void* y_out) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(nseg >= 0 && nseg <= 2048, DSMOE_E_INVALID_ARGUMENT, "expert_ffn: at most 2048 segments");
+    require(nseg == 0 || (seg_unit && seg_start && seg_nfull && seg_ntot), DSMOE_E_INVALID_ARGUMENT, "null segments");
+    g_launches = 0;
+    if (nseg == 0 || nrows == 0) return;
+    require(rows && row_scale && y_out, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    cudaStream_t s = C->stream;
+    std::vector<UnitSeg> sg(static_cast<size_t>(nseg));
+    long long mt = 0;
+    for (int i = 0; i < nseg; ++i) {
+      require(seg_unit[i] >= 0 && seg_unit[i] < L->E, DSMOE_E_INVALID_ARGUMENT, "expert_ffn: unit out of range");
+      require(seg_start[i] >= 0 && seg_nfull[i] >= 0 && seg_nfull[i] <= seg_ntot[i] &&
+                  static_cast<long long>(seg_start[i]) + seg_ntot[i] <= nrows,
+              DSMOE_E_INVALID_ARGUMENT, "expert_ffn: segment outside the row buffer");
+      sg[i] = UnitSeg{seg_start[i], seg_nfull[i], seg_ntot[i], 0};
+      mt += (seg_ntot[i] + kTileM - 1) / kTileM;
+    }
+    C->vseg.ensure(sizeof(UnitSeg) * nseg);
+    C->vseg_unit.ensure(sizeof(int) * nseg);
+    C->scalars.ensure(4 * sizeof(int));
+    cuda_check(cudaMemcpyAsync(C->vseg.p, sg.data(), sizeof(UnitSeg) * nseg, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemcpyAsync(C->vseg_unit.p, seg_unit, sizeof(int) * nseg, cudaMemcpyHostToDevice, s), "H2D");
+    const long long max1 = mt * L->max_chunks, max2 = mt * ((L->d + kTileN2 - 1) / kTileN2);
+    C->tiles1.ensure(static_cast<size_t>(max1 + 1) * sizeof(GemmTile));
+    C->tiles2.ensure(static_cast<size_t>(max2 + 1) * sizeof(GemmTile));
+    const long long h_rows = nrows + kTileM;
+    C->H.ensure(static_cast<size_t>(h_rows) * L->hstride * esize(L->dtype));
+    int* nn = C->scalars.as<int>();
+    PlanArgs pa{};
+    pa.units = L->d_units.as<UnitInfo>();
+    pa.seg_routed = C->vseg.as<UnitSeg>();
+    pa.seg_unit = C->vseg_unit.as<int>();
+    pa.shared_unit0 = L->E;
+    pa.num_routed = nseg;
+    pa.num_shared = 0;
+    pa.T = 0;
+    pa.d = L->d;
+    pa.tiles1 = C->tiles1.as<GemmTile>();
+    pa.n1 = nn + 1;
+    pa.tiles2 = C->tiles2.as<GemmTile>();
+    pa.n2 = nn + 2;
+    launch_check(launch_plan(pa, num_sms(), s), "plan");
+    ++g_launches;
+    run_gemms(C, L, rows, nrows, nullptr, 0, nn + 1, nn + 2, max1, max2, h_rows, y_out, row_scale);
+    // keep the caller's buffers alive until the work is done
+    cuda_check(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int dsmoe_b200_combine(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* y_rows, int T, void* out) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(T >= 0 && (T == 0 || (y_rows && out)), DSMOE_E_INVALID_ARGUMENT, "null argument");
+    g_launches = 0;
+    if (T == 0) return;
+    require(C->slot_pos.bytes >= static_cast<size_t>(T) * L->K * 4, DSMOE_E_INVALID_STATE,
+            "combine: no dispatch recorded for this batch");
+    const long long Rcap = static_cast<long long>(T) * L->K;
+    // routed rows come from the caller (returned expert outputs); shared rows
+    // from the dispatch's local shared-expert GEMMs (context Y)
+    launch_check(launch_combine2(y_rows, C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d,
+                                 L->K, L->S, static_cast<int>(Rcap), num_sms(), C->stream),
+                 "combine");
+    ++g_launches;
   });
 }
 

@@ -94,8 +94,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const GemmTile tl = args.tiles[t];
+        const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
+        if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
         const void* ma = (tl.m_live & kTileAltA) ? static_cast<const void*>(&mapA2)
                                                  : static_cast<const void*>(&mapA);
         for (int kb = 0; kb < tl.nkb; ++kb) {
@@ -116,8 +118,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       const uint32_t sbase = smem_u32(smem);
+      GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const GemmTile tl = args.tiles[t];
+        const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
+        if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
         const uint32_t idesc = idesc_bf16(kTileM, tl.n_mma);
         const uint32_t dtmem = tmem_base + acc * kAccCols;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -148,8 +152,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int r = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
+    GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const GemmTile tl = args.tiles[t];
+      const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
+      if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * kAccCols + (static_cast<uint32_t>(q * 32) << 16);

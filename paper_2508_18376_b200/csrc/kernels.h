@@ -58,14 +58,16 @@ struct PlanArgs {
   int* n2;
 };
 int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
-                     int* r_total, const PlanArgs* plan, cudaStream_t stream);
-int launch_plan(const PlanArgs& a, cudaStream_t stream);
+                     int* r_total, int* code_tot, const PlanArgs* plan, int num_sms, cudaStream_t stream);
+int launch_plan(const PlanArgs& a, int num_sms, cudaStream_t stream);
 int launch_scatter(const int32_t* sel_code, const float* sel_raw, int T, int K, int E, const int* chunk_off,
                    const int* code_base, int32_t* row_token, float* row_scale, int32_t* slot_pos, cudaStream_t stream);
 int launch_gather(const void* x, void* xp, const int32_t* row_token, const int* r_total,
                   int row_bytes, int num_sms, cudaStream_t stream);
 int launch_combine(const void* y, int y_bf16, const int32_t* slot_pos, void* out, int T, int d, int K,
                    int S, int shared_row0, int num_sms, cudaStream_t stream);
+int launch_combine2(const void* y, const void* ysh, int y_bf16, const int32_t* slot_pos, void* out, int T, int d,
+                    int K, int S, int shared_row0, int num_sms, cudaStream_t stream);
 int launch_fill_f32(float* p, float v, long long n, cudaStream_t stream);
 
 // gemm_tc.cu

@@ -56,8 +56,8 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
       off1[u + 1] += off1[u];
       off2[u + 1] += off2[u];
     }
-    if (a.n1) *a.n1 = off1[nu];
-    if (a.n2) *a.n2 = off2[nu];
+    if (a.n1 && blockIdx.x == 0) *a.n1 = off1[nu];
+    if (a.n2 && blockIdx.x == 0) *a.n2 = off2[nu];
   }
   __syncthreads();
   auto find = [&](const int* off, int i) {  // largest u with off[u] <= i
@@ -68,7 +68,8 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     }
     return lo;
   };
-  for (int i = threadIdx.x; i < off1[nu]; i += blockDim.x) {
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  for (int i = gtid; i < off1[nu]; i += gstride) {
     const int u = find(off1, i);
     const UnitInfo& ui = a.units[unit_of(u)];
     const UnitSeg sg = seg_of(u);
@@ -108,7 +109,7 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     tl.m_live = live | (sh ? kTileAltA : 0);
     a.tiles1[i] = tl;
   }
-  for (int i = threadIdx.x; i < off2[nu]; i += blockDim.x) {
+  for (int i = gtid; i < off2[nu]; i += gstride) {
     const int u = find(off2, i);
     const UnitInfo& ui = a.units[unit_of(u)];
     const UnitSeg sg = seg_of(u);
@@ -129,58 +130,73 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
 }
 
 // codes: c = unit * 2 + (level == 2 ? 0 : 1).  chunk_off[chunk][c] = rows of
-// code c in earlier chunks; code_base[c] = first row of code c.  One warp per
-// code: lanes own contiguous runs of chunks, warp-scan of the run sums.
-__global__ void __launch_bounds__(1024) scan_plan_kernel(const int* __restrict__ cnt_chunk, int nchunks, int E,
-                                                         int* __restrict__ chunk_off, int* __restrict__ code_base,
-                                                         UnitSeg* __restrict__ seg, int* __restrict__ r_total,
-                                                         const PlanArgs a, int do_plan) {
-  __shared__ int off1[kPlanMaxUnits + 1], off2[kPlanMaxUnits + 1];
-  __shared__ int s_tot[512];
-  const int ncode = 2 * E;
+// code c in earlier chunks.  One block per code: every chunk count loaded in
+// parallel, block-wide exclusive scan, total per code.
+__global__ void __launch_bounds__(512) scan_codes_kernel(const int* __restrict__ cnt_chunk, int nchunks, int ncode,
+                                                         int* __restrict__ chunk_off, int* __restrict__ code_tot) {
+  __shared__ int warp_sum[16];
+  __shared__ int carry;
+  const int c = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int q = cdiv(nchunks, 32);
-  for (int c = warp; c < ncode; c += nwarps) {
-    const int ch0 = min(nchunks, lane * q), ch1 = min(nchunks, ch0 + q);
-    int run = 0;
-    for (int ch = ch0; ch < ch1; ++ch) run += cnt_chunk[static_cast<long long>(ch) * ncode + c];
-    int incl = run;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    int pos = incl - run;
-    for (int ch = ch0; ch < ch1; ++ch) {
-      const long long k = static_cast<long long>(ch) * ncode + c;
-      const int v = cnt_chunk[k];
-      chunk_off[k] = pos;
-      pos += v;
-    }
-    if (lane == 31) s_tot[c] = incl;
-  }
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
+  for (int ch0 = 0; ch0 < nchunks; ch0 += blockDim.x) {
+    const int ch = ch0 + threadIdx.x;
+    const int v = ch < nchunks ? cnt_chunk[static_cast<long long>(ch) * ncode + c] : 0;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_sum[warp] = incl;
+    __syncthreads();
+    int before = carry;
+    for (int w = 0; w < warp; ++w) before += warp_sum[w];
+    if (ch < nchunks) chunk_off[static_cast<long long>(ch) * ncode + c] = before + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < nwarps; ++w) t += warp_sum[w];
+      carry += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) code_tot[c] = carry;
+}
+
+// Unit segments from the per-code totals (every block, in shared memory;
+// block 0 publishes them), then optionally the GEMM work lists.
+__global__ void __launch_bounds__(1024) seg_plan_kernel(const int* __restrict__ code_tot, int E,
+                                                        UnitSeg* __restrict__ seg, int* __restrict__ code_base,
+                                                        int* __restrict__ r_total, const PlanArgs a, int do_plan) {
+  __shared__ int off1[kPlanMaxUnits + 1], off2[kPlanMaxUnits + 1];
+  __shared__ UnitSeg s_seg[256];
   if (threadIdx.x == 0) {
     int start = 0;
     for (int u = 0; u < E; ++u) {
-      const int nf = s_tot[2 * u], nm = s_tot[2 * u + 1];
-      seg[u] = UnitSeg{start, nf, nf + nm, 0};
-      code_base[2 * u] = start;
-      code_base[2 * u + 1] = start + nf;
+      const int nf = code_tot[2 * u], nm = code_tot[2 * u + 1];
+      s_seg[u] = UnitSeg{start, nf, nf + nm, 0};
       start += nf + nm;
     }
-    *r_total = start;
+    if (blockIdx.x == 0) *r_total = start;
   }
   __syncthreads();
-  if (do_plan) plan_body(a, seg, off1, off2);
+  if (blockIdx.x == 0)
+    for (int u = threadIdx.x; u < E; u += blockDim.x) {
+      seg[u] = s_seg[u];
+      code_base[2 * u] = s_seg[u].start;
+      code_base[2 * u + 1] = s_seg[u].start + s_seg[u].n_full;
+    }
+  if (do_plan) plan_body(a, s_seg, off1, off2);
 }
 
 int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
-                     int* r_total, const PlanArgs* plan, cudaStream_t stream) {
+                     int* r_total, int* code_tot, const PlanArgs* plan, int num_sms, cudaStream_t stream) {
   if (E > 256) return -1;
   PlanArgs a{};
   if (plan) a = *plan;
-  scan_plan_kernel<<<1, 1024, 0, stream>>>(cnt_chunk, nchunks, E, chunk_off, code_base, seg, r_total, a,
-                                           plan != nullptr);
+  scan_codes_kernel<<<2 * E, 512, 0, stream>>>(cnt_chunk, nchunks, 2 * E, chunk_off, code_tot);
+  seg_plan_kernel<<<plan ? num_sms : 1, 1024, 0, stream>>>(code_tot, E, seg, code_base, r_total, a, plan != nullptr);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
@@ -190,9 +206,9 @@ __global__ void __launch_bounds__(1024) plan_kernel(const PlanArgs a) {
   plan_body(a, a.seg_routed, off1, off2);
 }
 
-int launch_plan(const PlanArgs& a, cudaStream_t stream) {
+int launch_plan(const PlanArgs& a, int num_sms, cudaStream_t stream) {
   if (a.num_routed + a.num_shared > kPlanMaxUnits) return -1;
-  plan_kernel<<<1, 1024, 0, stream>>>(a);
+  plan_kernel<<<num_sms, 1024, 0, stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
@@ -299,7 +315,7 @@ int launch_gather(const void* x, void* xp, const int32_t* row_token, const int* 
 // atomics).  Y rows already carry the raw-score weight (K4 epilogue).
 // --------------------------------------------------------------------------
 template <typename TY, typename TO>
-__global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y,
+__global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y, const TY* __restrict__ ysh,
                                                       const int32_t* __restrict__ slot_pos,
                                                       TO* __restrict__ out, int T, int d, int K,
                                                       int S, int shared_row0) {
@@ -310,17 +326,18 @@ __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y,
       float acc[V];
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[i] = 0.f;
-      auto add_row = [&](long long row) {
-        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(y + row * d) + v);
+      auto add_row = [&](const TY* base, long long row) {
+        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(base + row * d) + v);
         const TY* e = reinterpret_cast<const TY*>(&q);
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] += static_cast<float>(e[i]);
       };
       for (int s = 0; s < K; ++s) {
         const int p = slot_pos[static_cast<long long>(t) * K + s];
-        if (p >= 0) add_row(p);
+        if (p >= 0) add_row(y, p);
       }
-      for (int s = 0; s < S; ++s) add_row(static_cast<long long>(shared_row0) + static_cast<long long>(s) * T + t);
+      for (int s = 0; s < S; ++s)
+        add_row(ysh, static_cast<long long>(shared_row0) + static_cast<long long>(s) * T + t);
       TO* o = out + static_cast<long long>(t) * d + static_cast<long long>(v) * V;
       if constexpr (sizeof(TO) == 2) {
         uint32_t pk[V / 2];
@@ -335,18 +352,24 @@ __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y,
   }
 }
 
-int launch_combine(const void* y, int y_bf16, const int32_t* slot_pos, void* out, int T, int d, int K,
-                   int S, int shared_row0, int num_sms, cudaStream_t stream) {
+// y: routed rows (slot_pos); ysh: buffer holding the shared-expert rows
+int launch_combine2(const void* y, const void* ysh, int y_bf16, const int32_t* slot_pos, void* out, int T, int d,
+                    int K, int S, int shared_row0, int num_sms, cudaStream_t stream) {
   const int grid = T < num_sms * 16 ? (T > 0 ? T : 1) : num_sms * 16;
   if (y_bf16)
     combine_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(y), slot_pos, static_cast<__nv_bfloat16*>(out), T, d, K, S,
-        shared_row0);
+        static_cast<const __nv_bfloat16*>(y), static_cast<const __nv_bfloat16*>(ysh), slot_pos,
+        static_cast<__nv_bfloat16*>(out), T, d, K, S, shared_row0);
   else
-    combine_kernel<float, float><<<grid, 256, 0, stream>>>(static_cast<const float*>(y), slot_pos,
-                                                           static_cast<float*>(out), T, d, K, S,
-                                                           shared_row0);
+    combine_kernel<float, float><<<grid, 256, 0, stream>>>(static_cast<const float*>(y),
+                                                           static_cast<const float*>(ysh), slot_pos,
+                                                           static_cast<float*>(out), T, d, K, S, shared_row0);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+int launch_combine(const void* y, int y_bf16, const int32_t* slot_pos, void* out, int T, int d, int K,
+                   int S, int shared_row0, int num_sms, cudaStream_t stream) {
+  return launch_combine2(y, y, y_bf16, slot_pos, out, T, d, K, S, shared_row0, num_sms, stream);
 }
 
 __global__ void fill_f32_kernel(float* p, float v, long long n) {

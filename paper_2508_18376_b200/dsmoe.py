@@ -102,6 +102,12 @@ SYMBOLS = {
                                          C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsmoe_b200_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
                                      C.c_void_p, C.POINTER(DropStatsC)]),
+    "dsmoe_b200_dispatch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
+                                      C.POINTER(DropStatsC)]),
+    "dsmoe_b200_expert_ffn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_long, C.c_int,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dsmoe_b200_combine": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "dsmoe_b200_drop_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_long, C.c_int, C.c_int, C.c_long, C.c_int,
                                         C.c_int, C.POINTER(DropStatsC)]),
     "dsmoe_b200_profile_importance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
@@ -473,3 +479,43 @@ def reconstruct_experts(ctx: Context, layer: MoeLayer, values):
     _chk(lib().dsmoe_b200_reconstruct(ctx.h, layer.h, C.c_void_p(values.data_ptr()), C.c_void_p(order.data_ptr()),
                                       C.byref(h)))
     return MoeLayer._wrap(h, layer, 2), order
+
+
+# ------------------------------------------------ expert-parallel data path
+def dispatch(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None = None, t_unit=None,
+             rows_out=None, scale_out=None, logits_mode=LOGITS_TENSOR, with_stats=False):
+    """Route + drop + permute (+ gather into rows_out / scale_out when given).
+    Returns (seg E x 3 numpy [start, full rows, total rows], R, stats)."""
+    x = _x(x, layer)
+    seg = np.empty((layer.E, 3), np.int32)
+    R = C.c_int()
+    st = DropStatsC()
+    _chk(lib().dsmoe_b200_dispatch(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
+                                   C.byref((policy or DropPolicy()).c(t_unit)), logits_mode,
+                                   None if rows_out is None else C.c_void_p(rows_out.data_ptr()),
+                                   None if scale_out is None else C.c_void_p(scale_out.data_ptr()),
+                                   seg.ctypes.data, C.byref(R), C.byref(st) if with_stats else None))
+    return seg, R.value, (st.as_dict() if with_stats else None)
+
+
+def expert_ffn(ctx: Context, layer: MoeLayer, rows, row_scale, segments, y_out=None):
+    """Grouped expert FFN over segments [(unit, start, n_full, n_tot), ...] of
+    `rows` (CUDA tensor nrows x d); returns y (nrows x d)."""
+    torch = _torch()
+    if y_out is None:
+        y_out = torch.empty_like(rows)
+    segs = np.asarray(segments, np.int32).reshape(-1, 4)
+    cols = [np.ascontiguousarray(segs[:, i]) for i in range(4)]
+    _chk(lib().dsmoe_b200_expert_ffn(ctx.h, layer.h, C.c_void_p(rows.data_ptr()), C.c_void_p(row_scale.data_ptr()),
+                                     rows.shape[0], segs.shape[0], *[c.ctypes.data for c in cols],
+                                     C.c_void_p(y_out.data_ptr())))
+    return y_out
+
+
+def combine(ctx: Context, layer: MoeLayer, y_rows, T, out=None):
+    """out = sum of the returned expert rows at the last dispatch's slots + shared experts."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty((T, layer.d), dtype=layer.torch_dtype, device=y_rows.device)
+    _chk(lib().dsmoe_b200_combine(ctx.h, layer.h, C.c_void_p(y_rows.data_ptr()), T, C.c_void_p(out.data_ptr())))
+    return out

@@ -1,0 +1,268 @@
+"""Expert parallelism across the GPUs of one box (north-star item 6).
+
+The reference only simulates EP (/root/reference/proj/include/dsmoe/ep_sim.hpp):
+it places physical expert blocks on devices (place_experts :38), measures
+per-device loads in compute units (device_loads :59), derives load-aware
+per-device thresholds (load_aware_thresholds :76) and applies each selection's
+owner-device threshold (simulate_step :110-160), reporting
+speedup = max(pre load) / max(post load).  Here the same policy drives a real
+data path, one process per GPU over torch.distributed (NCCL):
+
+  1. every rank routes its own tokens without drop and the per-expert
+     selection counts are all-reduced (integers, so every rank derives the
+     bit-identical loads the reference's device_loads would give on the
+     concatenation of all ranks' tokens);
+  2. loads -> thresholds (uniform or load-aware) -> per-expert owner
+     threshold table t_unit; the device router re-routes with it
+     (dsmoe_b200_dispatch) and gathers the kept rows, experts ascending, so
+     under contiguous placement each destination rank's rows are one run;
+  3. per-expert (full, major-only) row counts and then the rows + raw scores
+     travel with all_to_all_single (dispatch);
+  4. each rank runs the grouped SwiGLU FFN over the received segments
+     (dsmoe_b200_expert_ffn), major-only rows skipping the minor sub-block;
+  5. the expert outputs travel back with the reverse all_to_all_single and
+     are combined in slot order (dsmoe_b200_combine).
+
+The host-side policy arithmetic (owner table, loads, thresholds, splits,
+receive segments) is plain numpy below and is unit-tested with gloo on CPU.
+EpEmulator runs the same data path for D virtual ranks on one GPU (the
+all-to-alls become slices), which is how the path is checked against the
+oracle here, where only one GPU is available.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import dsmoe as D
+
+
+# --------------------------------------------------------------- host policy
+def owner_of_experts(num_experts: int, replay_factor: int, devices: int, strategy: str = "contiguous"):
+    """Device of each original expert = device of its copy-0 block, the owner
+    simulate_step thresholds by (ep_sim.hpp:139-141)."""
+    blocks = D.place_experts(num_experts * replay_factor, devices, strategy)
+    return blocks[np.arange(num_experts) * replay_factor]
+
+
+def loads_from_counts(counts, owner, devices):
+    """device_loads (ep_sim.hpp:59-72) of a no-drop routing: every selection
+    contributes P copies x 1/P = exactly 1 unit, so the double sums are exact
+    integers and independent of summation order."""
+    loads = np.zeros(devices, np.float64)
+    np.add.at(loads, np.asarray(owner), np.asarray(counts, np.float64))
+    return loads
+
+
+def post_loads_from_segments(seg_full, seg_major, owner, devices, replay_factor):
+    """device_loads of the dropped routing: a full selection keeps P copies
+    (1 unit), a major-only one copy 0 only (1/P unit) — exact for P a power
+    of two."""
+    w = 1.0 / replay_factor
+    per = np.asarray(seg_full, np.float64) + np.asarray(seg_major, np.float64) * w
+    loads = np.zeros(devices, np.float64)
+    np.add.at(loads, np.asarray(owner), per)
+    return loads
+
+
+def device_thresholds(loads, t_drop, load_aware):
+    """simulate_step (ep_sim.hpp:133-138): load-aware or uniform thresholds."""
+    if load_aware:
+        return D.load_aware_thresholds(loads, t_drop)
+    return np.full(len(loads), float(t_drop))
+
+
+def send_counts(seg, owner, devices):
+    """Rows this rank sends to each rank: the kept rows of the experts it owns."""
+    out = np.zeros(devices, np.int64)
+    np.add.at(out, np.asarray(owner), np.asarray(seg)[:, 2].astype(np.int64))
+    return out
+
+
+def counts_for_receivers(seg, owner, devices):
+    """(devices x n_local x 2) int32: for each destination rank, (full rows,
+    major-only rows) of each expert it owns, in expert order."""
+    owner = np.asarray(owner)
+    n_local = np.bincount(owner, minlength=devices).max()
+    out = np.zeros((devices, n_local, 2), np.int32)
+    for r in range(devices):
+        es = np.nonzero(owner == r)[0]
+        out[r, :len(es), 0] = seg[es, 1]
+        out[r, :len(es), 1] = seg[es, 2] - seg[es, 1]
+    return out
+
+
+def receive_segments(cnt_recv, local_experts):
+    """Segments of the receive buffer: source-rank major, then expert, each
+    (unit, start, n_full, n_tot) — the order the sources' runs arrive in."""
+    segs, start = [], 0
+    for src in range(cnt_recv.shape[0]):
+        for j, e in enumerate(local_experts):
+            nf, nm = int(cnt_recv[src, j, 0]), int(cnt_recv[src, j, 1])
+            if nf + nm:
+                segs.append((int(e), start, nf, nf + nm))
+            start += nf + nm
+    return segs, start
+
+
+def modeled_speedup(pre, post):
+    """EpReport::speedup (ep_sim.hpp:154-158)."""
+    mp, mq = float(np.max(pre)), float(np.max(post))
+    return mp / mq if mq > 0 else (float("inf") if mp > 0 else 1.0)
+
+
+# ------------------------------------------------------------ distributed
+class ExpertParallelMoE:
+    """One rank of an expert-parallel MoE layer.  Every rank holds the full
+    (replicated) layer object but evaluates only the experts it owns."""
+
+    def __init__(self, layer: D.MoeLayer, group=None, strategy: str = "contiguous"):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.layer = layer
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if strategy != "contiguous":
+            raise D.DsmoeError(1, "expert-parallel data path needs contiguous placement")
+        self.owner = owner_of_experts(layer.E, layer.P, self.world, strategy)
+        self.local = np.nonzero(self.owner == self.rank)[0]
+        self.ctx = D.Context()
+        self.ctx_exp = D.Context()
+
+    def forward(self, x, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,
+                timing=False):
+        import torch
+        dist, L = self.dist, self.layer
+        policy = policy or D.DropPolicy()
+        T = x.shape[0]
+        dev = x.device
+        # 1. global pre-drop loads
+        seg0, _, _ = D.dispatch(self.ctx, L, x, D.DropPolicy(), logits_mode=logits_mode)
+        counts = torch.from_numpy(seg0[:, 2].astype(np.int64)).to(dev)
+        dist.all_reduce(counts, group=self.group)
+        pre = loads_from_counts(counts.cpu().numpy(), self.owner, self.world)
+        t_unit, th = None, np.zeros(self.world)
+        if policy.kind != "none":
+            th = device_thresholds(pre, policy.t_drop, load_aware)
+            t_unit = torch.from_numpy(th[self.owner]).to(dev)
+        # 2. owner-threshold routing + gather
+        xp = torch.empty((T * L.K + 128, L.d), dtype=x.dtype, device=dev)
+        sp = torch.empty(T * L.K + 128, dtype=torch.float32, device=dev)
+        seg, R, st = D.dispatch(self.ctx, L, x, policy, t_unit=t_unit, rows_out=xp, scale_out=sp,
+                                logits_mode=logits_mode, with_stats=True)
+        send = send_counts(seg, self.owner, self.world)
+        # 3. exchange counts, then rows and scores
+        cnt_send = torch.from_numpy(counts_for_receivers(seg, self.owner, self.world)).to(dev)
+        cnt_recv = torch.empty_like(cnt_send)
+        dist.all_to_all_single(cnt_recv, cnt_send, group=self.group)
+        cnt_recv = cnt_recv.cpu().numpy()
+        segs, nrecv = receive_segments(cnt_recv, self.local)
+        recv = cnt_recv.sum(axis=(1, 2)).astype(np.int64)
+        xr = torch.empty((nrecv + 128, L.d), dtype=x.dtype, device=dev)
+        sr = torch.empty(nrecv + 128, dtype=torch.float32, device=dev)
+        dist.all_to_all_single(xr[:nrecv], xp[:R], recv.tolist(), send.tolist(), group=self.group)
+        dist.all_to_all_single(sr[:nrecv], sp[:R], recv.tolist(), send.tolist(), group=self.group)
+        # 4. local experts
+        yr = torch.empty_like(xr)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
+        if timing:
+            ev[0].record()
+        if segs:
+            D.expert_ffn(self.ctx_exp, L, xr, sr, segs, y_out=yr)
+        if timing:
+            ev[1].record()
+        # 5. return + combine
+        yb = torch.empty((R + 128, L.d), dtype=x.dtype, device=dev)
+        dist.all_to_all_single(yb[:R], yr[:nrecv], send.tolist(), recv.tolist(), group=self.group)
+        out = D.combine(self.ctx, L, yb, T)
+        post = torch.from_numpy(np.stack([seg[:, 1], seg[:, 2] - seg[:, 1]]).astype(np.int64)).to(dev)
+        dist.all_reduce(post, group=self.group)
+        post = post.cpu().numpy()
+        post_loads = post_loads_from_segments(post[0], post[1], self.owner, self.world, L.P)
+        rep = {"pre_loads": pre, "post_loads": post_loads, "thresholds": th, "speedup": modeled_speedup(pre, post_loads),
+               "local_drop_stats": st, "rows_sent": send, "rows_received": int(nrecv)}
+        if timing:
+            torch.cuda.synchronize()
+            rep["expert_ms"] = ev[0].elapsed_time(ev[1])
+        return out, rep
+
+
+# ---------------------------------------------------------------- emulator
+class EpEmulator:
+    """The expert-parallel data path for `devices` virtual ranks on one GPU:
+    per-rank contexts, real kernels, the all-to-alls as slice/concat copies.
+    Used to check the path against the oracle and to time each rank's expert
+    FFN under uniform vs load-aware thresholds."""
+
+    def __init__(self, layer: D.MoeLayer, devices: int):
+        self.layer = layer
+        self.D = devices
+        self.owner = owner_of_experts(layer.E, layer.P, devices)
+        self.ctx = [D.Context() for _ in range(devices)]
+        self.ctx_exp = [D.Context() for _ in range(devices)]
+
+    def forward(self, xs, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,
+                timing=False):
+        import torch
+        L, Dv = self.layer, self.D
+        policy = policy or D.DropPolicy()
+        counts = np.zeros(L.E, np.int64)
+        for r in range(Dv):
+            seg0, _, _ = D.dispatch(self.ctx[r], L, xs[r], D.DropPolicy(), logits_mode=logits_mode)
+            counts += seg0[:, 2]
+        pre = loads_from_counts(counts, self.owner, Dv)
+        t_unit, th = None, np.zeros(Dv)
+        if policy.kind != "none":
+            th = device_thresholds(pre, policy.t_drop, load_aware)
+            t_unit = torch.from_numpy(th[self.owner]).cuda()
+        xp, sp, seg, R, send = [], [], [], [], []
+        for r in range(Dv):
+            T = xs[r].shape[0]
+            a = torch.empty((T * L.K + 128, L.d), dtype=xs[r].dtype, device="cuda")
+            b = torch.empty(T * L.K + 128, dtype=torch.float32, device="cuda")
+            sg, n, _ = D.dispatch(self.ctx[r], L, xs[r], policy, t_unit=t_unit, rows_out=a, scale_out=b,
+                                  logits_mode=logits_mode)
+            xp.append(a), sp.append(b), seg.append(sg), R.append(n)
+            send.append(send_counts(sg, self.owner, Dv))
+        cnt = [counts_for_receivers(seg[r], self.owner, Dv) for r in range(Dv)]
+        offs = [np.concatenate([[0], np.cumsum(send[r])]) for r in range(Dv)]
+        ys_back = [torch.empty((R[r] + 128, L.d), dtype=xs[r].dtype, device="cuda") for r in range(Dv)]
+        expert_ms = []
+        for dst in range(Dv):
+            cnt_recv = np.stack([cnt[src][dst] for src in range(Dv)])
+            segs, nrecv = receive_segments(cnt_recv, np.nonzero(self.owner == dst)[0])
+            xr = torch.empty((nrecv + 128, L.d), dtype=xs[0].dtype, device="cuda")
+            sr = torch.empty(nrecv + 128, dtype=torch.float32, device="cuda")
+            pos = 0
+            for src in range(Dv):  # all-to-all: src's run for dst
+                a, b = offs[src][dst], offs[src][dst + 1]
+                xr[pos:pos + b - a] = xp[src][a:b]
+                sr[pos:pos + b - a] = sp[src][a:b]
+                pos += b - a
+            yr = torch.empty_like(xr)
+            if timing:
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+            if segs:
+                D.expert_ffn(self.ctx_exp[dst], L, xr, sr, segs, y_out=yr)
+            if timing:
+                e1.record()
+                torch.cuda.synchronize()
+                expert_ms.append(e0.elapsed_time(e1))
+            pos = 0
+            for src in range(Dv):  # reverse all-to-all
+                a, b = offs[src][dst], offs[src][dst + 1]
+                ys_back[src][a:b] = yr[pos:pos + b - a]
+                pos += b - a
+        outs = [D.combine(self.ctx[r], L, ys_back[r], xs[r].shape[0]) for r in range(Dv)]
+        full = np.zeros(L.E, np.int64)
+        maj = np.zeros(L.E, np.int64)
+        for r in range(Dv):
+            full += seg[r][:, 1]
+            maj += seg[r][:, 2] - seg[r][:, 1]
+        post = post_loads_from_segments(full, maj, self.owner, Dv, L.P)
+        rep = {"pre_loads": pre, "post_loads": post, "thresholds": th, "speedup": modeled_speedup(pre, post)}
+        if timing:
+            rep["expert_ms"] = expert_ms
+        return outs, rep
