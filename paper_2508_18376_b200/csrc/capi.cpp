@@ -549,7 +549,7 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
 }
 
 // K2a: chunk scan + unit segments (+ GEMM work lists) + ordered scatter
-void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool plan) {
+void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool plan, bool gather = false) {
   cudaStream_t s = C->stream;
   const long long Rcap = static_cast<long long>(T) * L->K;
   int* r_total = C->scalars.as<int>();
@@ -567,6 +567,7 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
   pa.n1 = r_total + 1;
   pa.tiles2 = C->tiles2.as<GemmTile>();
   pa.n2 = r_total + 2;
+  pa.gather = gather ? 1 : 0;
   const int nchunks = (T + kRouterChunk - 1) / kRouterChunk;
   launch_check(launch_scan_plan(C->cnt_chunk.as<int>(), nchunks, L->E, C->chunk_off.as<int>(), C->code_base.as<int>(),
                                 C->seg.as<UnitSeg>(), r_total, C->code_base.as<int>() + 2 * L->E, plan ? &pa : nullptr, num_sms(), s),
@@ -582,17 +583,18 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
 // allocated), alt A = x (shared experts), H in the context, Y = y (ld d).
 void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long long a_rows, const void* x,
                int T, const int* n1, const int* n2, long long max1, long long max2, long long h_rows, void* y,
-               const float* row_scale) {
+               const float* row_scale, const int* row_token = nullptr) {
   cudaStream_t s = C->stream;
   const int mt1 = static_cast<int>(std::min<long long>(max1, 1 << 30));
   const int mt2 = static_cast<int>(std::min<long long>(max2, 1 << 30));
   if (L->dtype == DSMOE_B200_BF16) {
     const CUtensorMap mx = make_map(x ? x : rows, x ? T : a_rows, L->d, L->d, kTileM);
-    const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, kTileM);
+    // gathered routed tiles read token rows of x through row_token (TMA gather4, box 64 x 1)
+    const CUtensorMap mxp = row_token ? make_map(x, T, L->d, L->d, 1) : make_map(rows, a_rows, L->d, L->d, kTileM);
     const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, kTileM);
     C->mark(4);
     launch_check(launch_gemm_tc(1, &mxp, &mx, &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
-                                nullptr, 256, num_sms(), s),
+                                nullptr, 256, num_sms(), s, row_token),
                  "gemm1");
     C->mark(5);
     launch_check(launch_gemm_tc(2, &mh, &mh, &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,
@@ -639,14 +641,18 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   int* r_total = C->scalars.as<int>();
   int* n1 = r_total + 1;
   int* n2 = r_total + 2;
+  // bf16: GEMM1 gathers token rows itself (TMA gather4); fp32 (SIMT): explicit gather
+  const bool fused_gather = L->dtype == DSMOE_B200_BF16;
   C->mark(2);
-  stage_permute(C, L, T, true);
+  stage_permute(C, L, T, true, fused_gather);
   C->mark(3);
-  launch_check(launch_gather(x, C->xperm.p, C->row_token.as<int32_t>(), r_total, L->d * es, num_sms(), s), "gather");
-  g_launches += 1;
+  if (!fused_gather) {
+    launch_check(launch_gather(x, C->xperm.p, C->row_token.as<int32_t>(), r_total, L->d * es, num_sms(), s), "gather");
+    g_launches += 1;
+  }
   const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
   run_gemms(C, L, C->xperm.p, Rcap + kTileM, x, T, n1, n2, C->max_tiles1(L, T), C->max_tiles2(L, T), rows, C->Y.p,
-            C->row_scale.as<float>());
+            C->row_scale.as<float>(), fused_gather ? C->row_token.as<int>() : nullptr);
   C->mark(6);
   launch_check(launch_combine(C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d, L->K,
                               L->S, static_cast<int>(Rcap), num_sms(), s),

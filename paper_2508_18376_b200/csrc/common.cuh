@@ -50,7 +50,8 @@ struct GemmTile {
   int m_valid;   // rows of this tile that belong to the segment (stores masked beyond)
   int m_live;    // rows holding real data; rows in [m_live, m_valid) store zeros. bit 30: A from alt map
 };
-constexpr int kTileAltA = 1 << 30;
+constexpr int kTileAltA = 1 << 30;     // A rows from the alternate map (shared experts: X itself)
+constexpr int kTileGatherA = 1 << 29;  // A rows gathered from X through row_token (TMA gather4)
 
 // --------------------------------------------------------------- PTX helpers
 #if defined(__CUDACC__)
@@ -97,6 +98,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* map, uint64_t
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// TMA gather4: 4 rows (arbitrary row coordinates) x box columns -> smem,
+// written as 4 consecutive 128-byte rows (swizzle applied by address).
+__device__ __forceinline__ void tma_gather4(void* dst, const void* map, uint64_t* bar, int c0, int r0, int r1,
+                                            int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
       : "memory");
 }
 

@@ -34,7 +34,7 @@ constexpr int kStageBytes = kABytes + kBBytesMax;  // 48 KB
 constexpr int kGemmThreads = 320;  // producer, MMA, 8 epilogue warps
 constexpr int kEpiThreads = 256;
 constexpr int kAccCols = 256;
-constexpr int kGemmSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kGemmSmem = kStages * kStageBytes + 128 * 256 /*output stage*/ + 1024 /*align*/ + 256 /*barriers*/;
 
 enum { kEpiF32 = 0, kEpiSwiGLU = 1, kEpiScale = 2 };
 
@@ -45,9 +45,38 @@ struct GemmArgs {
   long long ldo;           // output row stride in elements
   const float* row_scale;  // kEpiScale
   uint32_t b_bytes;        // bytes of one B box (rows * 128)
+  const int* row_token;    // gathered A tiles: token of each permuted row
 };
 
 __device__ __forceinline__ float silu_fast(float g) { return g / (1.0f + __expf(-g)); }
+
+// Output staging for coalesced stores: 128 rows x 256 B (128 bf16) in smem,
+// 16-byte chunks XOR-swizzled by row so both the per-row writes (one row per
+// thread) and the row-contiguous reads are bank-conflict free.
+constexpr int kStageOutBytes = 128 * 256;
+
+__device__ __forceinline__ void stage_put(uint8_t* buf, int r, int col, const uint32_t* pk) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = (col >> 3) + i;
+    *reinterpret_cast<uint4*>(buf + r * 256 + ((k ^ (r & 15)) << 4)) =
+        make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+  }
+}
+
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// rows < m_valid of the staged tile (width bf16 columns) -> out (row stride ld)
+__device__ __forceinline__ void copy_out(const uint8_t* buf, __nv_bfloat16* out, long long ld, int width,
+                                         int m_valid, int tid) {
+  const int cpr = width >> 3;  // 16-byte chunks per row
+  for (int i = tid; i < 128 * cpr; i += 256) {
+    const int row = i / cpr, k = i - row * cpr;
+    if (row < m_valid)
+      *reinterpret_cast<uint4*>(out + row * ld + (k << 3)) =
+          *reinterpret_cast<const uint4*>(buf + row * 256 + ((k ^ (row & 15)) << 4));
+  }
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -56,7 +85,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint8_t* stage_buf = smem + kStages * kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + kStageOutBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -90,24 +120,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
-        if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
-        const void* ma = (tl.m_live & kTileAltA) ? static_cast<const void*>(&mapA2)
-                                                 : static_cast<const void*>(&mapA);
-        for (int kb = 0; kb < tl.nkb; ++kb) {
+    // ---------------- TMA producer (whole warp: lane 0 drives the ring; for
+    // gathered A tiles every lane issues one gather4 of 4 token rows, so the
+    // 128-row A tile is assembled straight from X — no permuted copy)
+    int stage = 0;
+    uint32_t phase = 0;
+    GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
+      if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
+      const bool alt = (tl.m_live & kTileAltA) != 0;
+      const bool gather = (tl.m_live & kTileGatherA) != 0;
+      const void* ma = alt ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
+      int g0 = 0, g1 = 0, g2 = 0, g3 = 0;
+      if (gather) {  // token rows 4*lane .. 4*lane+3 of this tile (0 past the segment)
+        const int b = 4 * lane;
+        const int* rt = args.row_token + tl.a_row;
+        g0 = b + 0 < tl.m_valid ? rt[b + 0] : 0;
+        g1 = b + 1 < tl.m_valid ? rt[b + 1] : 0;
+        g2 = b + 2 < tl.m_valid ? rt[b + 2] : 0;
+        g3 = b + 3 < tl.m_valid ? rt[b + 3] : 0;
+      }
+      for (int kb = 0; kb < tl.nkb; ++kb) {
+        uint8_t* sa = smem + stage * kStageBytes;
+        if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * kStageBytes;
           mbar_expect_tx(&full[stage], kABytes + args.b_bytes);
-          tma_load_2d(sa, ma, &full[stage], kb * kTileK, tl.a_row);
+          if (!gather) tma_load_2d(sa, ma, &full[stage], kb * kTileK, tl.a_row);
           tma_load_2d(sa + kABytes, &mapB, &full[stage], kb * kTileK, tl.b_row);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (gather) tma_gather4(sa + lane * 512, &mapA, &full[stage], kb * kTileK, g0, g1, g2, g3);
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -162,48 +206,55 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool valid = r < tl.m_valid;
       const long long orow = static_cast<long long>(tl.out_row + r);
       if constexpr (MODE == kEpiSwiGLU) {
+        // h = swish(g) * u -> bf16 -> staged in smem -> coalesced row stores
         const int nc = tl.n_mma >> 1;
         const bool live = r < (tl.m_live & 0xFFFFF);
-        __nv_bfloat16* H = static_cast<__nv_bfloat16*>(args.out) + orow * args.ldo + tl.out_col;
         for (int c = 32 * half; c < nc; c += 64) {
           uint32_t g[32], u[32];
           tmem_ld32(taddr + c, g);
           tmem_ld32(taddr + nc + c, u);
           tmem_ld_wait();
-          if (valid) {
-            uint32_t pk[16];
+          uint32_t pk[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float h0 = 0.f, h1 = 0.f;
-              if (live) {
-                h0 = silu_fast(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
-                h1 = silu_fast(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
-              }
-              pk[i] = pack_bf16x2(h0, h1);
+          for (int i = 0; i < 16; ++i) {
+            float h0 = 0.f, h1 = 0.f;
+            if (live) {
+              h0 = silu_fast(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+              h1 = silu_fast(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
             }
-            uint4* dst = reinterpret_cast<uint4*>(H + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            pk[i] = pack_bf16x2(h0, h1);
           }
+          stage_put(stage_buf, r, c, pk);
         }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);  // accumulator drained: MMA may reuse it
+        epi_sync();
+        copy_out(stage_buf, static_cast<__nv_bfloat16*>(args.out) + static_cast<long long>(tl.out_row) * args.ldo +
+                                tl.out_col, args.ldo, nc, tl.m_valid, threadIdx.x - 64);
+        epi_sync();
       } else if constexpr (MODE == kEpiScale) {
+        // y = acc * raw score -> bf16, staged 128 columns at a time
         const float sc = valid ? args.row_scale[orow] : 0.f;
-        __nv_bfloat16* Y = static_cast<__nv_bfloat16*>(args.out) + orow * args.ldo + tl.out_col;
-        for (int c = 32 * half; c < tl.n_mma; c += 64) {
-          uint32_t v[32];
-          tmem_ld32(taddr + c, v);
-          tmem_ld_wait();
-          if (valid) {
+        for (int p0 = 0; p0 < tl.n_mma; p0 += 128) {
+          const int w = min(128, tl.n_mma - p0);
+          for (int c = 32 * half; c < w; c += 64) {
+            uint32_t v[32];
+            tmem_ld32(taddr + p0 + c, v);
+            tmem_ld_wait();
             uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i)
               pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]) * sc, __uint_as_float(v[2 * i + 1]) * sc);
-            uint4* dst = reinterpret_cast<uint4*>(Y + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+            stage_put(stage_buf, r, c, pk);
           }
+          if (p0 + 128 >= tl.n_mma) {
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+          epi_sync();
+          copy_out(stage_buf, static_cast<__nv_bfloat16*>(args.out) + static_cast<long long>(tl.out_row) * args.ldo +
+                                  tl.out_col + p0, args.ldo, w, tl.m_valid, threadIdx.x - 64);
+          epi_sync();
         }
       } else {
         float* O = static_cast<float*>(args.out) + orow * args.ldo + tl.out_col;
@@ -218,8 +269,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (MODE == kEpiF32) {
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -232,8 +285,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
-                   int b_box_rows, int num_sms, cudaStream_t stream) {
-  GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128)};
+                   int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token) {
+  GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128), row_token};
   const int grid = max_tiles < num_sms ? (max_tiles > 0 ? max_tiles : 1) : num_sms;
   cudaError_t err;
   switch (mode) {

@@ -56,6 +56,7 @@ struct PlanArgs {
   int* n1;
   GemmTile* tiles2;
   int* n2;
+  int gather;                  // GEMM1 routed tiles gather A rows from X through row_token
 };
 int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
                      int* r_total, int* code_tot, const PlanArgs* plan, int num_sms, cudaStream_t stream);
@@ -74,7 +75,7 @@ int launch_fill_f32(float* p, float v, long long n, cudaStream_t stream);
 int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
-                   int b_box_rows, int num_sms, cudaStream_t stream);
+                   int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token = nullptr);
 
 // gemm_simt.cu
 struct SimtArgs {

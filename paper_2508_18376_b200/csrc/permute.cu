@@ -106,7 +106,7 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     tl.nkb = a.d / kTileK;
     tl.n_mma = 2 * nc;
     tl.m_valid = m_valid;
-    tl.m_live = live | (sh ? kTileAltA : 0);
+    tl.m_live = live | (sh ? kTileAltA : (a.gather ? kTileGatherA : 0));
     a.tiles1[i] = tl;
   }
   for (int i = gtid; i < off2[nu]; i += gstride) {

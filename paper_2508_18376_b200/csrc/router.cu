@@ -51,6 +51,7 @@ __device__ __forceinline__ float expf_tab(float x, const uint64_t* tab) {
   return static_cast<float>(__dmul_rn(y, s));
 }
 
+template <int EPL>  // experts per lane, E <= 32 * EPL
 __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterArgs a) {
   extern __shared__ int s_hist[];  // 2E codes: [unit*2 + (level==2 ? 0 : 1)]
   __shared__ uint64_t tab[32];
@@ -61,31 +62,31 @@ __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterA
   if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
   if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }
   __syncthreads();
-  const int epl = (E + 31) >> 5;
+  constexpr int epl = EPL;
   unsigned long long n1 = 0, nh = 0;
   const int t = blockIdx.x * kRouterChunk + warp;  // one token per warp
   if (t < a.T) {
     const float* row = a.logits + static_cast<long long>(t) * a.ld_logits;
-    float v[kMaxEPL];
+    float v[EPL];
 #pragma unroll
-    for (int j = 0; j < kMaxEPL; ++j) {
+    for (int j = 0; j < EPL; ++j) {
       const int e = lane + 32 * j;
       v[j] = (j < epl && e < E) ? row[e] : -INFINITY;
     }
     // softmax_inplace: max (order-free), exp, ordered float sum, divide
     float mx = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < kMaxEPL; ++j) mx = (mx < v[j]) ? v[j] : mx;
+    for (int j = 0; j < EPL; ++j) mx = (mx < v[j]) ? v[j] : mx;
     for (int o = 16; o > 0; o >>= 1) {
       const float other = __shfl_xor_sync(0xffffffffu, mx, o);
       mx = (mx < other) ? other : mx;
     }
 #pragma unroll
-    for (int j = 0; j < kMaxEPL; ++j)
+    for (int j = 0; j < EPL; ++j)
       if (j < epl) v[j] = (lane + 32 * j < E) ? expf_tab(__fsub_rn(v[j], mx), tab) : 0.0f;
     float sum = 0.0f;  // ascending e, identical on every lane
 #pragma unroll
-    for (int j = 0; j < kMaxEPL; ++j) {
+    for (int j = 0; j < EPL; ++j) {
       if (j >= epl) break;
       const int lim = min(32, E - 32 * j);
 #pragma unroll 8
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterA
       }
     }
 #pragma unroll
-    for (int j = 0; j < kMaxEPL; ++j)
+    for (int j = 0; j < EPL; ++j)
       if (j < epl) v[j] = __fdiv_rn(v[j], sum);
     // topk_route: K arg-max rounds; lane s keeps selection s
     unsigned taken = 0;  // bit j: expert lane + 32 j already selected
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterA
       float bv = 0.f;
       int be = -1;
 #pragma unroll
-      for (int j = 0; j < kMaxEPL; ++j) {
+      for (int j = 0; j < EPL; ++j) {
         const int e = lane + 32 * j;
         if (j >= epl || e >= E || ((taken >> j) & 1u)) continue;
         if (be < 0 || v[j] > bv) { bv = v[j]; be = e; }
@@ -187,7 +188,16 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
   if (a.K > kMaxK || a.E > 32 * kMaxEPL || a.K < 1 || a.K > a.E) return -1;
   const int blocks = (a.T + kRouterChunk - 1) / kRouterChunk;
   const size_t smem = static_cast<size_t>(2 * a.E) * sizeof(int);
-  if (blocks > 0) router_kernel<<<blocks, kRouterChunk * 32, smem, stream>>>(a);
+  if (blocks <= 0) return 0;
+  const int epl = (a.E + 31) / 32;
+  if (epl <= 1)
+    router_kernel<1><<<blocks, kRouterChunk * 32, smem, stream>>>(a);
+  else if (epl <= 2)
+    router_kernel<2><<<blocks, kRouterChunk * 32, smem, stream>>>(a);
+  else if (epl <= 4)
+    router_kernel<4><<<blocks, kRouterChunk * 32, smem, stream>>>(a);
+  else
+    router_kernel<8><<<blocks, kRouterChunk * 32, smem, stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
