@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -641,8 +642,14 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   int* r_total = C->scalars.as<int>();
   int* n1 = r_total + 1;
   int* n2 = r_total + 2;
-  // bf16: GEMM1 gathers token rows itself (TMA gather4); fp32 (SIMT): explicit gather
-  const bool fused_gather = L->dtype == DSMOE_B200_BF16;
+  // Explicit 16-byte-vector gather into X_perm by default.  DSMOE_B200_GATHER4=1
+  // makes GEMM1 gather token rows itself with TMA tile::gather4 (bit-identical;
+  // measured 2.8x slower GEMM1 on B200: 32 gather4 issues per 128-row k-block).
+  static const bool gather4_env = [] {
+    const char* v = std::getenv("DSMOE_B200_GATHER4");
+    return v && v[0] == '1';
+  }();
+  const bool fused_gather = gather4_env && L->dtype == DSMOE_B200_BF16;
   C->mark(2);
   stage_permute(C, L, T, true, fused_gather);
   C->mark(3);
