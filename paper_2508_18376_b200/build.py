@@ -68,5 +68,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_dropin(ref_include="/root/reference/proj/include") -> str | None:
+    """C++ drop-in test (tests/cpp/test_dropin.cpp) against the reference's own
+    headers + generators (oracle/_ref/core.a).  Only where the reference
+    sources exist (this container); the binary travels to the GPU box."""
+    root = os.path.dirname(HERE)
+    core = os.path.join(root, "oracle", "_ref", "core.a")
+    if not (os.path.isdir(ref_include) and os.path.exists(core)):
+        return None
+    json_dir = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+    out = os.path.join(root, "build", "test_dropin")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I" + ref_include, "-I" + os.path.join(root, "include"),
+           "-I/usr/local/cuda/include", "-I" + json_dir, os.path.join(root, "tests", "cpp", "test_dropin.cpp"), core,
+           "-L" + HERE, "-l:libdsmoe_b200.so", "-L/usr/local/cuda/lib64", "-lcudart_static", "-ldl", "-lrt",
+           "-lpthread", "-Wl,-rpath,$ORIGIN/../paper_2508_18376_b200", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"drop-in test build failed:\n{r.stderr}")
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
