@@ -363,7 +363,8 @@ struct dsmoe_b200_ctx {
     const long long t2 = (mt + mts) * ((L->d + kTileN2 - 1) / kTileN2);
     tiles1.ensure(static_cast<size_t>(t1 + 1) * sizeof(GemmTile));
     tiles2.ensure(static_cast<size_t>(t2 + 1) * sizeof(GemmTile));
-    xperm.ensure(static_cast<size_t>(Rcap + kTileM) * L->d * es);
+    // X_perm only for the explicit-gather paths (fp32 SIMT, DSMOE_B200_GATHER=explicit)
+    if (L->dtype != DSMOE_B200_BF16 || std::getenv("DSMOE_B200_GATHER")) xperm.ensure(static_cast<size_t>(Rcap + kTileM) * L->d * es);
     H.ensure(static_cast<size_t>(rows) * L->hstride * es);
     Y.ensure(static_cast<size_t>(rows) * L->d * es);
     const size_t rs_bytes = static_cast<size_t>(rows) * 4;
@@ -590,12 +591,11 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
   const int mt2 = static_cast<int>(std::min<long long>(max2, 1 << 30));
   if (L->dtype == DSMOE_B200_BF16) {
     const CUtensorMap mx = make_map(x ? x : rows, x ? T : a_rows, L->d, L->d, kTileM);
-    // gathered routed tiles read token rows of x through row_token (TMA gather4, box 64 x 1)
-    const CUtensorMap mxp = row_token ? make_map(x, T, L->d, L->d, 1) : make_map(rows, a_rows, L->d, L->d, kTileM);
+    const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, kTileM);
     const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, kTileM);
     C->mark(4);
     launch_check(launch_gemm_tc(1, &mxp, &mx, &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
-                                nullptr, 256, num_sms(), s, row_token),
+                                nullptr, 256, num_sms(), s, row_token, x, static_cast<long long>(L->d) * 2),
                  "gemm1");
     C->mark(5);
     launch_check(launch_gemm_tc(2, &mh, &mh, &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,
@@ -642,14 +642,14 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   int* r_total = C->scalars.as<int>();
   int* n1 = r_total + 1;
   int* n2 = r_total + 2;
-  // Explicit 16-byte-vector gather into X_perm by default.  DSMOE_B200_GATHER4=1
-  // makes GEMM1 gather token rows itself with TMA tile::gather4 (bit-identical;
-  // measured 2.8x slower GEMM1 on B200: 32 gather4 issues per 128-row k-block).
-  static const bool gather4_env = [] {
-    const char* v = std::getenv("DSMOE_B200_GATHER4");
-    return v && v[0] == '1';
+  // bf16: GEMM1's producer warps gather the token rows (cp.async) straight
+  // into its A tiles; fp32 (SIMT GEMM) and DSMOE_B200_GATHER=explicit use the
+  // explicit 16-byte-vector gather into X_perm.
+  static const bool explicit_env = [] {
+    const char* v = std::getenv("DSMOE_B200_GATHER");
+    return v && std::string(v) == "explicit";
   }();
-  const bool fused_gather = gather4_env && L->dtype == DSMOE_B200_BF16;
+  const bool fused_gather = !explicit_env && L->dtype == DSMOE_B200_BF16;
   C->mark(2);
   stage_permute(C, L, T, true, fused_gather);
   C->mark(3);
@@ -658,7 +658,8 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
     g_launches += 1;
   }
   const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
-  run_gemms(C, L, C->xperm.p, Rcap + kTileM, x, T, n1, n2, C->max_tiles1(L, T), C->max_tiles2(L, T), rows, C->Y.p,
+  run_gemms(C, L, fused_gather ? x : C->xperm.p, fused_gather ? T : Rcap + kTileM, x, T, n1, n2, C->max_tiles1(L, T),
+            C->max_tiles2(L, T), rows, C->Y.p,
             C->row_scale.as<float>(), fused_gather ? C->row_token.as<int>() : nullptr);
   C->mark(6);
   launch_check(launch_combine(C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d, L->K,

@@ -51,7 +51,7 @@ struct GemmTile {
   int m_live;    // rows holding real data; rows in [m_live, m_valid) store zeros. bit 30: A from alt map
 };
 constexpr int kTileAltA = 1 << 30;     // A rows from the alternate map (shared experts: X itself)
-constexpr int kTileGatherA = 1 << 29;  // A rows gathered from X through row_token (TMA gather4)
+constexpr int kTileGatherA = 1 << 29;  // A rows gathered from X through row_token (cp.async in GEMM1)
 
 // --------------------------------------------------------------- PTX helpers
 #if defined(__CUDACC__)
@@ -101,15 +101,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* map, uint64_t
       : "memory");
 }
 
-// TMA gather4: 4 rows (arbitrary row coordinates) x box columns -> smem,
-// written as 4 consecutive 128-byte rows (swizzle applied by address).
-__device__ __forceinline__ void tma_gather4(void* dst, const void* map, uint64_t* bar, int c0, int r0, int r1,
-                                            int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
+// 16-byte cp.async global -> shared (L2 only), and the arrive-on of all of
+// this thread's prior cp.async on an mbarrier (counted in its init count).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // ---- tcgen05 / TMEM

@@ -31,7 +31,10 @@ constexpr int kStages = 4;
 constexpr int kABytes = kTileM * kTileK * 2;       // 16 KB
 constexpr int kBBytesMax = 256 * kTileK * 2;       // 32 KB
 constexpr int kStageBytes = kABytes + kBBytesMax;  // 48 KB
-constexpr int kGemmThreads = 320;  // producer, MMA, 8 epilogue warps
+constexpr int kProducerWarps = 2;   // warps 0-1: TMA + cp.async row gather
+constexpr int kMmaWarp = 2;         // warp 2: TMEM alloc + tcgen05.mma issue
+constexpr int kEpiWarp0 = 3;        // warps 3-10: epilogue
+constexpr int kGemmThreads = 352;
 constexpr int kEpiThreads = 256;
 constexpr int kAccCols = 256;
 constexpr int kGemmSmem = kStages * kStageBytes + 128 * 256 /*output stage*/ + 1024 /*align*/ + 256 /*barriers*/;
@@ -46,6 +49,8 @@ struct GemmArgs {
   const float* row_scale;  // kEpiScale
   uint32_t b_bytes;        // bytes of one B box (rows * 128)
   const int* row_token;    // gathered A tiles: token of each permuted row
+  const void* gather_src;  // gathered A tiles: X (bf16, gather_ld bytes per row)
+  long long gather_ld;
 };
 
 __device__ __forceinline__ float silu_fast(float g) { return g / (1.0f + __expf(-g)); }
@@ -98,7 +103,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 1 + kProducerWarps * 32);  // expect_tx arrive + producer arrivals
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -110,7 +115,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch(&mapA2);
     tma_prefetch(&mapB);
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tmem_alloc(tmem_slot, 2 * kAccCols);
     tmem_relinquish();
   }
@@ -119,10 +124,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    // ---------------- TMA producer (whole warp: lane 0 drives the ring; for
-    // gathered A tiles every lane issues one gather4 of 4 token rows, so the
-    // 128-row A tile is assembled straight from X — no permuted copy)
+  if (warp < kProducerWarps) {
+    // ---------------- producers (warps 0-1).  Thread 0 drives the ring and
+    // issues the TMA loads (B always; A for tiles whose rows are contiguous).
+    // For gathered tiles all 64 threads fill the A tile straight from the
+    // token rows of X with 16-byte cp.async into the SWIZZLE_128B layout the
+    // UMMA descriptor expects (no permuted copy of X in HBM); their
+    // completion arrives on the same full barrier (.noinc).
+    const int pt = threadIdx.x;  // 0..63
     int stage = 0;
     uint32_t phase = 0;
     GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
@@ -132,29 +141,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool alt = (tl.m_live & kTileAltA) != 0;
       const bool gather = (tl.m_live & kTileGatherA) != 0;
       const void* ma = alt ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
-      int g0 = 0, g1 = 0, g2 = 0, g3 = 0;
-      if (gather) {  // token rows 4*lane .. 4*lane+3 of this tile (0 past the segment)
-        const int b = 4 * lane;
+      // this thread's two rows (pt, pt + 64); rows past the segment read token 0
+      const char* src0 = nullptr;
+      const char* src1 = nullptr;
+      if (gather) {
         const int* rt = args.row_token + tl.a_row;
-        g0 = b + 0 < tl.m_valid ? rt[b + 0] : 0;
-        g1 = b + 1 < tl.m_valid ? rt[b + 1] : 0;
-        g2 = b + 2 < tl.m_valid ? rt[b + 2] : 0;
-        g3 = b + 3 < tl.m_valid ? rt[b + 3] : 0;
+        const long long t0 = pt < tl.m_valid ? rt[pt] : 0;
+        const long long t1 = pt + 64 < tl.m_valid ? rt[pt + 64] : 0;
+        src0 = static_cast<const char*>(args.gather_src) + t0 * args.gather_ld;
+        src1 = static_cast<const char*>(args.gather_src) + t1 * args.gather_ld;
       }
       for (int kb = 0; kb < tl.nkb; ++kb) {
         uint8_t* sa = smem + stage * kStageBytes;
-        if (lane == 0) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], kABytes + args.b_bytes);
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (pt == 0) {
+          mbar_expect_tx(&full[stage], (gather ? 0u : static_cast<uint32_t>(kABytes)) + args.b_bytes);
           if (!gather) tma_load_2d(sa, ma, &full[stage], kb * kTileK, tl.a_row);
           tma_load_2d(sa + kABytes, &mapB, &full[stage], kb * kTileK, tl.b_row);
         }
-        __syncwarp();
-        if (gather) tma_gather4(sa + lane * 512, &mapA, &full[stage], kb * kTileK, g0, g1, g2, g3);
+        if (gather) {
+          const uint32_t d0 = smem_u32(sa) + pt * 128, d1 = d0 + 64 * 128;
+          const int sw = pt & 7;  // (pt + 64) & 7 == pt & 7
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            cp_async16(d0 + ((j ^ sw) << 4), src0 + kb * 128 + j * 16);
+            cp_async16(d1 + ((j ^ sw) << 4), src1 + kb * 128 + j * 16);
+          }
+          cp_async_arrive_noinc(&full[stage]);
+        } else {
+          mbar_arrive(&full[stage]);
+        }
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     if (lane == 0) {
       // ---------------- MMA issuer
       int stage = 0;
@@ -192,7 +212,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ---------------- epilogue warps 2..9: two per TMEM lane quarter, 32-column
     // chunks interleaved between them
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - kEpiWarp0) >> 2;
     const int r = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -230,7 +250,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_arrive(&tempty[acc]);  // accumulator drained: MMA may reuse it
         epi_sync();
         copy_out(stage_buf, static_cast<__nv_bfloat16*>(args.out) + static_cast<long long>(tl.out_row) * args.ldo +
-                                tl.out_col, args.ldo, nc, tl.m_valid, threadIdx.x - 64);
+                                tl.out_col, args.ldo, nc, tl.m_valid, threadIdx.x - kEpiWarp0 * 32);
         epi_sync();
       } else if constexpr (MODE == kEpiScale) {
         // y = acc * raw score -> bf16, staged 128 columns at a time
@@ -253,7 +273,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           epi_sync();
           copy_out(stage_buf, static_cast<__nv_bfloat16*>(args.out) + static_cast<long long>(tl.out_row) * args.ldo +
-                                  tl.out_col + p0, args.ldo, w, tl.m_valid, threadIdx.x - 64);
+                                  tl.out_col + p0, args.ldo, w, tl.m_valid, threadIdx.x - kEpiWarp0 * 32);
           epi_sync();
         }
       } else {
@@ -278,15 +298,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, 2 * kAccCols);
+  if (warp == kMmaWarp) tmem_dealloc(tmem_base, 2 * kAccCols);
 }
 
 // ------------------------------------------------------------------ launcher
 int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
-                   int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token) {
-  GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128), row_token};
+                   int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token,
+                   const void* gather_src, long long gather_ld) {
+  GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128), row_token,
+             gather_src, gather_ld};
   const int grid = max_tiles < num_sms ? (max_tiles > 0 ? max_tiles : 1) : num_sms;
   cudaError_t err;
   switch (mode) {

@@ -75,7 +75,8 @@ int launch_fill_f32(float* p, float v, long long n, cudaStream_t stream);
 int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
-                   int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token = nullptr);
+                   int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token = nullptr,
+                   const void* gather_src = nullptr, long long gather_ld = 0);
 
 // gemm_simt.cu
 struct SimtArgs {
