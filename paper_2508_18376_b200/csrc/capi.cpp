@@ -363,8 +363,7 @@ struct dsmoe_b200_ctx {
     const long long t2 = (mt + mts) * ((L->d + kTileN2 - 1) / kTileN2);
     tiles1.ensure(static_cast<size_t>(t1 + 1) * sizeof(GemmTile));
     tiles2.ensure(static_cast<size_t>(t2 + 1) * sizeof(GemmTile));
-    // X_perm only for the explicit-gather paths (fp32 SIMT, DSMOE_B200_GATHER=explicit)
-    if (L->dtype != DSMOE_B200_BF16 || std::getenv("DSMOE_B200_GATHER")) xperm.ensure(static_cast<size_t>(Rcap + kTileM) * L->d * es);
+    xperm.ensure(static_cast<size_t>(Rcap + kTileM) * L->d * es);
     H.ensure(static_cast<size_t>(rows) * L->hstride * es);
     Y.ensure(static_cast<size_t>(rows) * L->d * es);
     const size_t rs_bytes = static_cast<size_t>(rows) * 4;
@@ -642,14 +641,15 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   int* r_total = C->scalars.as<int>();
   int* n1 = r_total + 1;
   int* n2 = r_total + 2;
-  // bf16: GEMM1's producer warps gather the token rows (cp.async) straight
-  // into its A tiles; fp32 (SIMT GEMM) and DSMOE_B200_GATHER=explicit use the
-  // explicit 16-byte-vector gather into X_perm.
-  static const bool explicit_env = [] {
+  // Explicit 16-byte-vector gather into X_perm by default.  DSMOE_B200_GATHER=fused
+  // makes GEMM1's producer warps gather the token rows with cp.async straight
+  // into the swizzled A tiles (bit-identical; measured 2x slower GEMM1 on B200
+  // at C2, the LDGSTS producer cannot keep the tensor pipe fed).
+  static const bool fused_env = [] {
     const char* v = std::getenv("DSMOE_B200_GATHER");
-    return v && std::string(v) == "explicit";
+    return v && std::string(v) == "fused";
   }();
-  const bool fused_gather = !explicit_env && L->dtype == DSMOE_B200_BF16;
+  const bool fused_gather = fused_env && L->dtype == DSMOE_B200_BF16;
   C->mark(2);
   stage_permute(C, L, T, true, fused_gather);
   C->mark(3);

@@ -297,7 +297,15 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const uint4* __restric
   for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < R; r += gridDim.x * wpb) {
     const uint4* src = x + static_cast<long long>(row_token[r]) * vec_per_row;
     uint4* dst = xp + static_cast<long long>(r) * vec_per_row;
-    for (int i = lane; i < vec_per_row; i += 32) dst[i] = __ldcs(src + i);
+    int i = lane;
+    for (; i + 7 * 32 < vec_per_row; i += 8 * 32) {  // 8 loads in flight per lane, then 8 stores
+      uint4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldg(src + i + 32 * j);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) __stcs(dst + i + 32 * j, v[j]);
+    }
+    for (; i < vec_per_row; i += 32) __stcs(dst + i, __ldg(src + i));
   }
 }
 
