@@ -11,8 +11,13 @@ d=2048, ffn=1024, reconstructed into major/minor halves, bf16, T=16384).
 `value` is at the --drop target (2T policy, threshold calibrated on the
 device); the 0/25/50% sweep and the drop speed-ups ride along in `sweep`.
 Weights are random-init of the named shapes (no checkpoints offline).
-N > 1 (torchrun): every rank runs the same module on its own tokens (weak
-scaling, no collective on this path); the expert-parallel path is ep.py.
+N > 1 (torchrun, one process per GPU): expert parallelism (ep.py) — every
+rank keeps 16384 tokens of its own (weak scaling), experts are sharded
+contiguously, load-aware thresholds from NCCL-all-reduced loads, NCCL
+all-to-all dispatch and combine; value = all ranks' tokens / max-over-ranks
+time.  N = 1 also reports `ep_emulated`: the same EP data path for 8 virtual
+ranks on this GPU under skewed routing (uniform vs load-aware vs no drop),
+each rank's expert time measured with CUDA events.
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -217,17 +222,118 @@ def cpu_reference_rate(host, T_sample, threads, seed=5):
     return T_sample / dt, dt
 
 
+def e2e_pipelined(D, ctx_stream, ctx, layer, pol, x, steps):
+    """Same metric through the public API with HOST buffers: per step the
+    token batch is copied H2D from pinned memory and the MoE output D2H to
+    pinned memory.  Copies run on their own streams, double-buffered, so the
+    copy of step i+1 / i-1 overlaps the forward of step i."""
+    import torch
+    T, d = x.shape
+    xh = [x.cpu().pin_memory() for _ in range(2)]
+    oh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
+    xd = [torch.empty_like(x) for _ in range(2)]
+    od = [torch.empty_like(x) for _ in range(2)]
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_fw = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_out:
+        e.record(s_out)
+
+    def run(n):
+        for i in range(n):
+            b = i & 1
+            with torch.cuda.stream(s_in):
+                s_in.wait_event(ev_fw[b]) if i >= 2 else None
+                xd[b].copy_(xh[b], non_blocking=True)
+                ev_in[b].record(s_in)
+            ctx_stream.wait_event(ev_in[b])
+            ctx_stream.wait_event(ev_out[b])
+            D.forward(ctx, layer, xd[b], pol, out=od[b])
+            ev_fw[b].record(ctx_stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_fw[b])
+                oh[b].copy_(od[b], non_blocking=True)
+                ev_out[b].record(s_out)
+
+    run(3)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(ctx_stream)
+    run(steps)
+    s_out.synchronize()
+    t1.record(s_out)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    return {"value": T / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": xh[0].numel() * xh[0].element_size(),
+            "d2h_bytes_per_step": oh[0].numel() * oh[0].element_size(),
+            "mode": "double-buffered H2D / forward / D2H on separate streams"}
+
+
+def ep_emulated(D, cfg="c2", devices=8, tokens_per_rank=4096, target=0.25, skew=1.5):
+    """EP data path for `devices` virtual ranks on one GPU (ep.EpEmulator):
+    skewed synthetic routing (acceptance.cpp:381-387), contiguous placement.
+    Step time of EP = the slowest rank's expert FFN (the all-to-alls are
+    copies here); compares no drop, uniform thresholds and load-aware
+    thresholds at the same t_max, and uniform at the drop rate load-aware
+    reaches (matched)."""
+    import numpy as np
+    import torch
+    from paper_2508_18376_b200 import ep
+    ctx = D.Context()
+    layer, host = build_layer(cfg, ctx)
+    gate = host[0].float()
+    d = gate.shape[0]
+    hot = gate[:, 3]
+    g = torch.Generator(device="cuda").manual_seed(7)
+    xs = []
+    for r in range(devices):
+        x = torch.randn(tokens_per_rank, d, device="cuda", generator=g)
+        x = x + (skew / hot.norm()) * hot
+        xs.append(x.to(torch.bfloat16))
+    emu = ep.EpEmulator(layer, devices)
+    # t_max for ~target drop under uniform thresholds
+    xall = torch.cat(xs)
+    pol, _ = calibrate(ctx, layer, xall, target)
+
+    def run(policy, aware):
+        best = None
+        for _ in range(3):
+            _, rep = emu.forward(xs, policy, load_aware=aware, timing=True)
+            m = max(rep["expert_ms"])
+            if best is None or m < best[0]:
+                best = (m, rep)
+        m, rep = best
+        return {"max_rank_expert_ms": m, "rank_expert_ms": rep["expert_ms"],
+                "pre_loads": rep["pre_loads"].tolist(), "post_loads": rep["post_loads"].tolist(),
+                "thresholds": [float(v) for v in rep["thresholds"]], "modeled_speedup": rep["speedup"]}
+
+    none = run(D.DropPolicy(), False)
+    uni = run(pol, False)
+    aware = run(pol, True)
+    out = {"devices": devices, "tokens_per_rank": tokens_per_rank, "t_max": pol.t_drop, "no_drop": none,
+           "uniform": uni, "load_aware": aware,
+           "speedup_load_aware_vs_no_drop": none["max_rank_expert_ms"] / aware["max_rank_expert_ms"],
+           "speedup_uniform_vs_no_drop": none["max_rank_expert_ms"] / uni["max_rank_expert_ms"],
+           "speedup_load_aware_vs_uniform_same_tmax": uni["max_rank_expert_ms"] / aware["max_rank_expert_ms"]}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=list(CONFIGS))
     ap.add_argument("--drop", type=float, default=0.25)
     ap.add_argument("--tokens", type=int, default=16384)
     ap.add_argument("--cpu-sample", type=int, default=0, help="tokens for the CPU baseline sample (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ep", action="store_true", help="skip the single-GPU EP emulation")
+    ap.add_argument("--extra", default="", help="comma list of extra configs to sweep (c3,c4)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -240,8 +346,6 @@ def main():
         if rank != 0:
             return
         import torch  # noqa: F401  (weights are generated with torch on the host CPU)
-        host = None
-        # host-side random weights of the same shapes
         gate, experts, shared = make_weights(args.config, device="cpu")
         Eh, Kh, fh = E, K, ffn
         if args.config == "c3":
@@ -249,11 +353,8 @@ def main():
             Eh, Kh, fh = E * 4, K * 4, ffn // 4
         host = (gate, experts, shared, Eh, Kh, fh)
         sample = args.cpu_sample or {"c2": 96, "c3": 8, "c4": 96}[args.config]
-        rates = []
         cpu_reference_rate(host, max(4, sample // 4), ncores)  # warm-up
-        for _ in range(args.steps):
-            rate, _ = cpu_reference_rate(host, sample, ncores)
-            rates.append(rate)
+        rates = [cpu_reference_rate(host, sample, ncores)[0] for _ in range(args.steps)]
         v = statistics.median(rates)
         print(json.dumps({"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                           "warmup": args.warmup, "ms_per_step": sample / v * 1e3, "higher_is_better": True,
@@ -275,47 +376,83 @@ def main():
         dist = None
     import paper_2508_18376_b200 as D
 
-    ctx = D.Context()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = D.Context(stream)
     layer, host = build_layer(args.config, ctx, seed=0)
     T = args.tokens
     gx = torch.Generator(device="cuda").manual_seed(99 + rank)
     x = torch.randn(T, d, device="cuda", generator=gx).to(torch.bfloat16)
     out = torch.empty_like(x)
+    peak_burst, peak_sust, hbm, peak_src = load_peaks()
 
-    # ---- drop sweep (0 / 25 / 50 %) + the headline target
+    if world > 1:
+        # ---------------- expert parallelism over NCCL
+        from paper_2508_18376_b200 import ep
+        m = ep.ExpertParallelMoE(layer)
+        pol, rate_main = calibrate(ctx, layer, x, args.drop)  # per-rank threshold (ranks agree closely)
+        t_drop = torch.tensor([pol.t_drop], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t_drop)
+        pol = D.DropPolicy.two_t_from(float(t_drop.item()) / world)
+        res = {}
+        for name, p_, aware in (("no_drop", D.DropPolicy(), False), ("uniform", pol, False), ("load_aware", pol, True)):
+            ms = time_steps(lambda: m.forward(x, p_, load_aware=aware), args.steps, args.warmup, dist)
+            res[name] = ms / args.steps
+        _, rep = m.forward(x, pol, load_aware=True)
+        ms_step = res["load_aware"]
+        value = T * world / (ms_step * 1e-3)
+        if rank == 0:
+            print(json.dumps({
+                "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic tokens N(0,1), random-init weights of the named shapes",
+                "config": {"workload": label + ", expert-parallel", "config_id": args.config, "tokens_per_gpu": T,
+                           "parallelism": f"ep{world} (contiguous placement, NCCL all-to-all)",
+                           "drop_target": args.drop, "policy": "2T load-aware",
+                           "l2": "working set > L2"},
+                "ep": {"ms_per_step": res, "speedup_load_aware_vs_no_drop": res["no_drop"] / res["load_aware"],
+                       "speedup_load_aware_vs_uniform": res["uniform"] / res["load_aware"],
+                       "pre_loads": rep["pre_loads"].tolist(), "post_loads": rep["post_loads"].tolist(),
+                       "thresholds": [float(v) for v in rep["thresholds"]], "modeled_speedup": rep["speedup"]},
+                "roofline": None, "cpu_baseline": None,
+                "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                        "note": "device-resident inputs under EP"},
+                "gpu_launches": None}))
+        dist.destroy_process_group()
+        return
+
+    # ---------------- single GPU: drop sweep (0 / 25 / 50 %) + the headline target
     targets = sorted({0.0, 0.25, 0.5, args.drop})
     sweep = {}
-    pol_main = None
+    pol_main = rate_main = None
     for tg in targets:
         pol, rate = calibrate(ctx, layer, x, tg)
-        ms = time_steps(lambda: D.forward(ctx, layer, x, pol, out=out), max(5, args.steps // 2), 3, dist)
         n = max(5, args.steps // 2)
-        sweep[f"{tg:.2f}"] = {"drop_rate": rate, "ms_per_step": ms / n, "tokens_per_s": T * world / (ms / n * 1e-3)}
+        ms = time_steps(lambda: D.forward(ctx, layer, x, pol, out=out), n, 3)
+        sweep[f"{tg:.2f}"] = {"drop_rate": rate, "t_drop": pol.t_drop, "ms_per_step": ms / n,
+                              "tokens_per_s": T / (ms / n * 1e-3)}
         if tg == args.drop:
             pol_main, rate_main = pol, rate
     base_ms = sweep["0.00"]["ms_per_step"]
-    for k, v in sweep.items():
+    for v in sweep.values():
         v["speedup_vs_0"] = base_ms / v["ms_per_step"]
 
-    # ---- headline timed region
-    launches_per_step = None
+    # ---- headline timed region (device-resident inputs)
     with ClockSampler(local) as clk:
-        ms = time_steps(lambda: D.forward(ctx, layer, x, pol_main, out=out), args.steps, args.warmup, dist)
+        ms = time_steps(lambda: D.forward(ctx, layer, x, pol_main, out=out), args.steps, args.warmup)
     launches_per_step = D.last_launch_count()
     ms_step = ms / args.steps
-    value = T * world / (ms_step * 1e-3)
+    value = T / (ms_step * 1e-3)
 
     # ---- per-kernel device times (CUDA events on the context stream)
-    ctx.set_profiling(True)
-    nprof = 10
     _, st = D.forward(ctx, layer, x, pol_main, out=out, with_stats=True)
     ctx.set_profiling(True)
-    for _ in range(nprof):
+    for _ in range(10):
         D.forward(ctx, layer, x, pol_main, out=out)
     prof = ctx.profile()
     ctx.set_profiling(False)
     per = {k: prof[k] / prof["calls"] for k in ctx.STAGES}
-    peak_burst, peak_sust, hbm, peak_src = load_peaks()
     g1_flops = st["retained_flops"] * 2.0 / 3.0   # [W1|W3]: 4*d*width per kept row
     g2_flops = st["retained_flops"] / 3.0         # W2: 2*d*width per kept row
     g1_tf = g1_flops / (per["gemm1"] * 1e-3) / 1e12
@@ -329,28 +466,17 @@ def main():
             traffic = None
     roofline = {"kernel": "gemm1 (grouped [W1|W3] GEMM + SwiGLU, tcgen05)", "bound": "tensor",
                 "achieved": g1_tf, "peak": peak_sust, "unit": "TFLOP/s", "frac": g1_tf / peak_sust,
-                "peak_kind": f"bf16 sustained ({peak_src}); burst {peak_burst}", "traffic": traffic,
-                "flops_per_launch": g1_flops, "ms_per_launch": per["gemm1"],
+                "peak_kind": f"bf16 sustained ({peak_src}); burst {peak_burst}", "frac_of_burst": g1_tf / peak_burst,
+                "traffic": traffic, "flops_per_launch": g1_flops, "ms_per_launch": per["gemm1"],
                 "gemm2": {"achieved": g2_tf, "frac": g2_tf / peak_sust, "ms_per_launch": per["gemm2"]},
                 "stages_ms": per}
 
     # ---- e2e through the public API with host buffers
-    xh = x.cpu().pin_memory()
-    oh = torch.empty_like(xh).pin_memory()
-    xd = torch.empty_like(x)
+    e2e = e2e_pipelined(D, stream, ctx, layer, pol_main, x, max(5, args.steps // 2))
 
-    def e2e_step():
-        xd.copy_(xh, non_blocking=True)
-        D.forward(ctx, layer, xd, pol_main, out=out)
-        oh.copy_(out, non_blocking=True)
-
-    e2e_ms = time_steps(e2e_step, max(5, args.steps // 2), 2, dist) / max(5, args.steps // 2)
-    e2e = {"value": T * world / (e2e_ms * 1e-3), "unit": "tokens/s",
-           "h2d_bytes_per_step": xh.numel() * xh.element_size(), "d2h_bytes_per_step": oh.numel() * oh.element_size()}
-
-    # ---- CPU baseline (rank 0 at N=1 only; bounded sample)
+    # ---- CPU baseline (bounded sample of the same layer shape)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if not args.no_cpu:
         try:
             sample = args.cpu_sample or {"c2": 64, "c3": 4, "c4": 64}[args.config]
             rate, dt = cpu_reference_rate(host, sample, ncores)
@@ -361,23 +487,47 @@ def main():
             cpu = {"value": None, "unit": "tokens/s", "cores": ncores, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
-    if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic tokens N(0,1), random-init weights of the named shapes",
-                "config": {"workload": label, "config_id": args.config, "tokens_per_gpu": T, "experts": E,
-                           "top_k": K, "d_model": d, "d_ffn": ffn, "shared": S,
-                           "drop_target": args.drop, "drop_rate": rate_main, "policy": "2T (t-0.01, t+0.01)",
-                           "l2": "working set > L2 (weights %.2f GB read per step)" % (
-                               (E * 3 * d * ffn + S * 3 * d * ffn) * 2 / 1e9),
-                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
-                "sweep": sweep, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches_per_step * args.steps,
-                "gpu_launches_per_step": launches_per_step, "clocks": clk.summary()}
-        print(json.dumps(line))
-    if dist is not None:
-        dist.destroy_process_group()
+    epx = None
+    if not args.no_ep:
+        try:
+            epx = ep_emulated(D, args.config)
+        except Exception as e:  # noqa: BLE001
+            epx = {"error": str(e)}
+
+    extra = {}
+    for c in [c for c in args.extra.split(",") if c]:
+        ctx2 = D.Context(stream)
+        l2, _ = build_layer(c, ctx2)
+        x2 = torch.randn(T, CONFIGS[c][0], device="cuda").to(torch.bfloat16)
+        o2 = torch.empty_like(x2)
+        sw = {}
+        for tg in (0.0, 0.25, 0.5):
+            p2, r2 = calibrate(ctx2, l2, x2, tg)
+            ms2 = time_steps(lambda: D.forward(ctx2, l2, x2, p2, out=o2), 10, 3) / 10
+            _, st2 = D.forward(ctx2, l2, x2, p2, out=o2, with_stats=True)
+            sw[f"{tg:.2f}"] = {"drop_rate": r2, "ms_per_step": ms2, "tokens_per_s": T / (ms2 * 1e-3),
+                               "gemm_tflops_total_step": st2["retained_flops"] / (ms2 * 1e-3) / 1e12}
+        for v in sw.values():
+            v["speedup_vs_0"] = sw["0.00"]["ms_per_step"] / v["ms_per_step"]
+        extra[c] = {"workload": CONFIGS[c][5], "sweep": sw}
+        del l2, ctx2
+
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic tokens N(0,1), random-init weights of the named shapes",
+            "config": {"workload": label, "config_id": args.config, "tokens_per_gpu": T, "experts": E,
+                       "top_k": K, "d_model": d, "d_ffn": ffn, "shared": S,
+                       "drop_target": args.drop, "drop_rate": rate_main, "policy": "2T (t-0.01, t+0.01)",
+                       "l2": "working set > L2 (weights %.2f GB read per step)" % (
+                           (E * 3 * d * ffn + S * 3 * d * ffn) * 2 / 1e9),
+                       "parallelism": "single GPU"},
+            "sweep": sweep, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step,
+            "clocks": clk.summary(), "ep_emulated": epx}
+    if extra:
+        line["extra_configs"] = extra
+    print(json.dumps(line))
 
 
 if __name__ == "__main__":
