@@ -121,6 +121,9 @@ CUtensorMap make_map(const void* base, long long rows, long long cols, long long
   return m;
 }
 
+// Rows allocated past the last permuted row: a 256-row tile may overrun.
+constexpr long long kRowSlack = 256;
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -134,6 +137,9 @@ int num_sms() {
 }  // namespace
 
 // ==================================================================== layer
+struct dsmoe_b200_layer;
+bool use_pair(const dsmoe_b200_layer* L);
+
 struct dsmoe_b200_layer {
   int d = 0, ffn = 0, E = 0, K = 0, S = 0, P = 1, prenorm = 0, dtype = DSMOE_B200_BF16;
   std::vector<int> widths, swidths;
@@ -144,6 +150,7 @@ struct dsmoe_b200_layer {
   int max_chunks = 0;
   DevBuf w13, w2t, gateT, gate_exact, d_units;
   CUtensorMap map_w13{}, map_w2t{}, map_gate{};
+  CUtensorMap map_w13_h{}, map_w2t_h{};  // 128-row boxes: half-N B tiles of the CTA-pair GEMM
   std::vector<char> block_set, shared_set;
   bool gate_set = false;
 
@@ -157,6 +164,16 @@ struct dsmoe_b200_layer {
       require(shared_set[s], DSMOE_E_INVALID_STATE, "layer: shared expert " + std::to_string(s) + " not set");
   }
 };
+
+bool use_pair(const dsmoe_b200_layer* L) {
+  // CTA-pair (cta_group::2) GEMMs for bf16 layers; DSMOE_B200_CTA_PAIR=0 selects
+  // the single-CTA kernel.
+  static const bool off = [] {
+    const char* v = std::getenv("DSMOE_B200_CTA_PAIR");
+    return v && v[0] == '0';
+  }();
+  return !off && L->dtype == DSMOE_B200_BF16;
+}
 
 namespace {
 
@@ -250,6 +267,8 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c) {
   if (L->dtype == DSMOE_B200_BF16) {
     L->map_w13 = make_map(L->w13.p, row, L->d, L->d, 256);
     L->map_w2t = make_map(L->w2t.p, static_cast<long long>(L->E + L->S) * L->d, L->hstride, L->hstride, 256);
+    L->map_w13_h = make_map(L->w13.p, row, L->d, L->d, 128);
+    L->map_w2t_h = make_map(L->w2t.p, static_cast<long long>(L->E + L->S) * L->d, L->hstride, L->hstride, 128);
     L->map_gate = make_map(L->gateT.p, L->Epad, L->d, L->d, L->Epad);
   }
   L->block_set.assign(static_cast<size_t>(L->E * P), 0);
@@ -344,7 +363,7 @@ struct dsmoe_b200_ctx {
     const int es = esize(L->dtype);
     const long long TK = static_cast<long long>(T) * L->K;
     const long long Rcap = TK;
-    const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
+    const long long rows = Rcap + static_cast<long long>(L->S) * T + kRowSlack;
     logits.ensure(static_cast<size_t>(T) * L->Epad * 4 + 16);
     sel_code.ensure(static_cast<size_t>(TK) * 4 + 16);
     sel_raw.ensure(static_cast<size_t>(TK) * 4 + 16);
@@ -354,7 +373,7 @@ struct dsmoe_b200_ctx {
     chunk_off.ensure(nchunks * 2 * L->E * 4 + 16);
     code_base.ensure(static_cast<size_t>(4 * L->E) * 4);  // [2E bases | 2E totals]
     counters.ensure(4 * sizeof(unsigned long long));
-    row_token.ensure(static_cast<size_t>(Rcap + kTileM) * 4);
+    row_token.ensure(static_cast<size_t>(Rcap + kRowSlack) * 4);
     seg.ensure(sizeof(UnitSeg) * L->E);
     scalars.ensure(4 * sizeof(int));  // r_total, n1, n2, ngate
     const long long mt = (Rcap + kTileM - 1) / kTileM + L->E;
@@ -363,7 +382,7 @@ struct dsmoe_b200_ctx {
     const long long t2 = (mt + mts) * ((L->d + kTileN2 - 1) / kTileN2);
     tiles1.ensure(static_cast<size_t>(t1 + 1) * sizeof(GemmTile));
     tiles2.ensure(static_cast<size_t>(t2 + 1) * sizeof(GemmTile));
-    xperm.ensure(static_cast<size_t>(Rcap + kTileM) * L->d * es);
+    xperm.ensure(static_cast<size_t>(Rcap + kRowSlack) * L->d * es);
     H.ensure(static_cast<size_t>(rows) * L->hstride * es);
     Y.ensure(static_cast<size_t>(rows) * L->d * es);
     const size_t rs_bytes = static_cast<size_t>(rows) * 4;
@@ -550,7 +569,8 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
 }
 
 // K2a: chunk scan + unit segments (+ GEMM work lists) + ordered scatter
-void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool plan, bool gather = false) {
+void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool plan, bool gather = false,
+                   int tile_m = kTileM) {
   cudaStream_t s = C->stream;
   const long long Rcap = static_cast<long long>(T) * L->K;
   int* r_total = C->scalars.as<int>();
@@ -569,6 +589,7 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
   pa.tiles2 = C->tiles2.as<GemmTile>();
   pa.n2 = r_total + 2;
   pa.gather = gather ? 1 : 0;
+  pa.tile_m = tile_m;
   const int nchunks = (T + kRouterChunk - 1) / kRouterChunk;
   launch_check(launch_scan_plan(C->cnt_chunk.as<int>(), nchunks, L->E, C->chunk_off.as<int>(), C->code_base.as<int>(),
                                 C->seg.as<UnitSeg>(), r_total, C->code_base.as<int>() + 2 * L->E, plan ? &pa : nullptr, num_sms(), s),
@@ -584,11 +605,22 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
 // allocated), alt A = x (shared experts), H in the context, Y = y (ld d).
 void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long long a_rows, const void* x,
                int T, const int* n1, const int* n2, long long max1, long long max2, long long h_rows, void* y,
-               const float* row_scale, const int* row_token = nullptr) {
+               const float* row_scale, const int* row_token = nullptr, bool pair = false) {
   cudaStream_t s = C->stream;
   const int mt1 = static_cast<int>(std::min<long long>(max1, 1 << 30));
   const int mt2 = static_cast<int>(std::min<long long>(max2, 1 << 30));
-  if (L->dtype == DSMOE_B200_BF16) {
+  if (pair) {  // CTA-pair tcgen05 GEMMs over M = 256 tiles
+    const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, 128);
+    const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, 128);
+    C->mark(4);
+    launch_check(launch_gemm_tc2(1, &mxp, &L->map_w13_h, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
+                                 nullptr, num_sms(), s),
+                 "gemm1 (pair)");
+    C->mark(5);
+    launch_check(launch_gemm_tc2(2, &mh, &L->map_w2t_h, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,
+                                 num_sms(), s),
+                 "gemm2 (pair)");
+  } else if (L->dtype == DSMOE_B200_BF16) {
     const CUtensorMap mx = make_map(x ? x : rows, x ? T : a_rows, L->d, L->d, kTileM);
     const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, kTileM);
     const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, kTileM);
@@ -650,17 +682,18 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
     return v && std::string(v) == "fused";
   }();
   const bool fused_gather = fused_env && L->dtype == DSMOE_B200_BF16;
+  const bool pair = use_pair(L) && !fused_gather;
   C->mark(2);
-  stage_permute(C, L, T, true, fused_gather);
+  stage_permute(C, L, T, true, fused_gather, pair ? 256 : kTileM);
   C->mark(3);
   if (!fused_gather) {
     launch_check(launch_gather(x, C->xperm.p, C->row_token.as<int32_t>(), r_total, L->d * es, num_sms(), s), "gather");
     g_launches += 1;
   }
-  const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
-  run_gemms(C, L, fused_gather ? x : C->xperm.p, fused_gather ? T : Rcap + kTileM, x, T, n1, n2, C->max_tiles1(L, T),
+  const long long rows = Rcap + static_cast<long long>(L->S) * T + kRowSlack;
+  run_gemms(C, L, fused_gather ? x : C->xperm.p, fused_gather ? T : Rcap + kRowSlack, x, T, n1, n2, C->max_tiles1(L, T),
             C->max_tiles2(L, T), rows, C->Y.p,
-            C->row_scale.as<float>(), fused_gather ? C->row_token.as<int>() : nullptr);
+            C->row_scale.as<float>(), fused_gather ? C->row_token.as<int>() : nullptr, pair);
   C->mark(6);
   launch_check(launch_combine(C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d, L->K,
                               L->S, static_cast<int>(Rcap), num_sms(), s),
@@ -1031,7 +1064,8 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
     const long long max1 = mt * L->max_chunks, max2 = mt * ((L->d + kTileN2 - 1) / kTileN2);
     C->tiles1.ensure(static_cast<size_t>(max1 + 1) * sizeof(GemmTile));
     C->tiles2.ensure(static_cast<size_t>(max2 + 1) * sizeof(GemmTile));
-    const long long h_rows = nrows + kTileM;
+    const long long h_rows = nrows + kRowSlack;
+    const bool pair = use_pair(L);
     C->H.ensure(static_cast<size_t>(h_rows) * L->hstride * esize(L->dtype));
     int* nn = C->scalars.as<int>();
     PlanArgs pa{};
@@ -1047,9 +1081,10 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
     pa.n1 = nn + 1;
     pa.tiles2 = C->tiles2.as<GemmTile>();
     pa.n2 = nn + 2;
+    pa.tile_m = pair ? 256 : kTileM;
     launch_check(launch_plan(pa, num_sms(), s), "plan");
     ++g_launches;
-    run_gemms(C, L, rows, nrows, nullptr, 0, nn + 1, nn + 2, max1, max2, h_rows, y_out, row_scale);
+    run_gemms(C, L, rows, nrows, nullptr, 0, nn + 1, nn + 2, max1, max2, h_rows, y_out, row_scale, nullptr, pair);
     // keep the caller's buffers alive until the work is done
     cuda_check(cudaStreamSynchronize(s), "sync");
   });

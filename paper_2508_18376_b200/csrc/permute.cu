@@ -32,6 +32,7 @@ constexpr int kPlanMaxUnits = 2048;
 // full rows, so FLOPs fall with the drop rate (no masks).
 __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int* off2) {
   const int nu = a.num_routed + a.num_shared;
+  const int tm = a.tile_m ? a.tile_m : kTileM;  // 128 (single CTA) or 256 (CTA pair)
   const int ntd = cdiv(a.d, kTileN2);
   auto unit_of = [&](int u) { return u < a.num_routed ? (a.seg_unit ? a.seg_unit[u] : u) : a.shared_unit0 + (u - a.num_routed); };
   auto seg_of = [&](int u) {
@@ -43,7 +44,7 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
   for (int u = threadIdx.x; u < nu; u += blockDim.x) {
     const UnitInfo& ui = a.units[unit_of(u)];
     const UnitSeg sg = seg_of(u);
-    const int mt_all = cdiv(sg.n_tot, kTileM), mt_full = cdiv(sg.n_full, kTileM);
+    const int mt_all = cdiv(sg.n_tot, tm), mt_full = cdiv(sg.n_full, tm);
     int c1 = 0;
     for (int p = 0; p < ui.nsub; ++p) c1 += cdiv(ui.sub_wpad[p], kChunk) * (p == 0 ? mt_all : mt_full);
     off1[u + 1] = c1;
@@ -74,7 +75,7 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     const UnitInfo& ui = a.units[unit_of(u)];
     const UnitSeg sg = seg_of(u);
     const bool sh = ui.shared != 0;
-    const int mt_full = cdiv(sg.n_full, kTileM);
+    const int mt_full = cdiv(sg.n_full, tm);
     int ch_all = 0;
     for (int p = 0; p < ui.nsub; ++p) ch_all += cdiv(ui.sub_wpad[p], kChunk);
     const int ch0 = cdiv(ui.sub_wpad[0], kChunk);
@@ -96,12 +97,12 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     }
     const int c = r;
     const int nc = min(kChunk, ui.sub_wpad[p] - c * kChunk);
-    const int m_valid = min(kTileM, sg.n_tot - mt * kTileM);
-    const int live = p == 0 ? m_valid : max(0, min(kTileM, sg.n_full - mt * kTileM));
+    const int m_valid = min(tm, sg.n_tot - mt * tm);
+    const int live = p == 0 ? m_valid : max(0, min(tm, sg.n_full - mt * tm));
     GemmTile tl;
-    tl.a_row = sh ? mt * kTileM : sg.start + mt * kTileM;
+    tl.a_row = sh ? mt * tm : sg.start + mt * tm;
     tl.b_row = wrow + 2 * kChunk * c;
-    tl.out_row = sg.start + mt * kTileM;
+    tl.out_row = sg.start + mt * tm;
     tl.out_col = hcol + kChunk * c;
     tl.nkb = a.d / kTileK;
     tl.n_mma = 2 * nc;
@@ -115,13 +116,13 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     const UnitSeg sg = seg_of(u);
     const int li = i - off2[u];
     const int mt = li / ntd, nt = li - mt * ntd;
-    const int m_valid = min(kTileM, sg.n_tot - mt * kTileM);
+    const int m_valid = min(tm, sg.n_tot - mt * tm);
     GemmTile tl;
-    tl.a_row = sg.start + mt * kTileM;
+    tl.a_row = sg.start + mt * tm;
     tl.b_row = ui.w2t_row + nt * kTileN2;
-    tl.out_row = sg.start + mt * kTileM;
+    tl.out_row = sg.start + mt * tm;
     tl.out_col = nt * kTileN2;
-    tl.nkb = ((mt * kTileM < sg.n_full) ? ui.hwidth : ui.sub_wpad[0]) / kTileK;
+    tl.nkb = ((mt * tm < sg.n_full) ? ui.hwidth : ui.sub_wpad[0]) / kTileK;
     tl.n_mma = min(kTileN2, a.d - nt * kTileN2);
     tl.m_valid = m_valid;
     tl.m_live = m_valid;
