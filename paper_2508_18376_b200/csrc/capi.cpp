@@ -610,14 +610,15 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
   const int mt1 = static_cast<int>(std::min<long long>(max1, 1 << 30));
   const int mt2 = static_cast<int>(std::min<long long>(max2, 1 << 30));
   if (pair) {  // CTA-pair tcgen05 GEMMs over M = 256 tiles
+    const CUtensorMap mx = make_map(x ? x : rows, x ? T : a_rows, L->d, L->d, 128);
     const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, 128);
     const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, 128);
     C->mark(4);
-    launch_check(launch_gemm_tc2(1, &mxp, &L->map_w13_h, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
+    launch_check(launch_gemm_tc2(1, &mxp, &mx, &L->map_w13_h, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
                                  nullptr, num_sms(), s),
                  "gemm1 (pair)");
     C->mark(5);
-    launch_check(launch_gemm_tc2(2, &mh, &L->map_w2t_h, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,
+    launch_check(launch_gemm_tc2(2, &mh, &mh, &L->map_w2t_h, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,
                                  num_sms(), s),
                  "gemm2 (pair)");
   } else if (L->dtype == DSMOE_B200_BF16) {

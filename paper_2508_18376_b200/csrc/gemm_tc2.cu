@@ -47,6 +47,11 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // arrive on the mbarrier at the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
@@ -101,8 +106,8 @@ __device__ __forceinline__ void copy_out2(const uint8_t* buf, __nv_bfloat16* out
 
 template <int MODE>
 __global__ void __launch_bounds__(k2Threads, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                    const Gemm2Args args) {
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
+                    const __grid_constant__ CUtensorMap mapB, const Gemm2Args args) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -131,6 +136,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
     }
     fence_mbar_init();
     tma_prefetch(&mapA);
+    tma_prefetch(&mapA2);
     tma_prefetch(&mapB);
   }
   if (warp == 1) {
@@ -153,14 +159,15 @@ __global__ void __launch_bounds__(k2Threads, 1)
         const GemmTile tl = args.tiles[t];
         const int a_row = tl.a_row + static_cast<int>(rank) * 128;
         const int b_row = tl.b_row + static_cast<int>(rank) * (tl.n_mma >> 1);
+        const void* ma = (tl.m_live & kTileAltA) ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * k2StageBytes;
           if (leader)
             mbar_expect_tx(&full[stage], 2 * k2StageBytes);
           else
-            mbar_arrive_cluster(&full[stage], 0);
-          tma_load_2d_pair(sa, &mapA, &full[stage], kb * kTileK, a_row);
+            mbar_arrive_cluster_relaxed(&full[stage], 0);
+          tma_load_2d_pair(sa, ma, &full[stage], kb * kTileK, a_row);
           tma_load_2d_pair(sa + k2ABytes, &mapB, &full[stage], kb * kTileK, b_row);
           if (++stage == k2Stages) { stage = 0; phase ^= 1; }
         }
@@ -271,7 +278,8 @@ __global__ void __launch_bounds__(k2Threads, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
 }
 
-int launch_gemm_tc2(int mode, const CUtensorMap* mapA, const CUtensorMap* mapB, const GemmTile* tiles,
+int launch_gemm_tc2(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2, const CUtensorMap* mapB,
+                    const GemmTile* tiles,
                     const int* num_tiles, int max_tiles, void* out, long long ldo, const float* row_scale, int num_sms,
                     cudaStream_t stream) {
   Gemm2Args a{tiles, num_tiles, out, ldo, row_scale};
@@ -296,14 +304,14 @@ int launch_gemm_tc2(int mode, const CUtensorMap* mapA, const CUtensorMap* mapB, 
       cudaFuncSetAttribute(gemm_tc2_kernel<k2SwiGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem);
       attr_set = true;
     }
-    e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<k2SwiGLU>, *mapA, *mapB, a);
+    e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<k2SwiGLU>, *mapA, *mapA2, *mapB, a);
   } else if (mode == k2Scale) {
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(gemm_tc2_kernel<k2Scale>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem);
       attr_set = true;
     }
-    e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<k2Scale>, *mapA, *mapB, a);
+    e = cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<k2Scale>, *mapA, *mapA2, *mapB, a);
   } else {
     return -1;
   }

@@ -80,7 +80,8 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const void* gather_src = nullptr, long long gather_ld = 0);
 
 // gemm_tc2.cu (CTA pairs, M = 256 tiles; B maps with 128-row boxes)
-int launch_gemm_tc2(int mode, const CUtensorMap* mapA, const CUtensorMap* mapB, const GemmTile* tiles,
+int launch_gemm_tc2(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2, const CUtensorMap* mapB,
+                    const GemmTile* tiles,
                     const int* num_tiles, int max_tiles, void* out, long long ldo, const float* row_scale, int num_sms,
                     cudaStream_t stream);
 
