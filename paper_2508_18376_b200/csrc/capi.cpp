@@ -166,13 +166,14 @@ struct dsmoe_b200_layer {
 };
 
 bool use_pair(const dsmoe_b200_layer* L) {
-  // CTA-pair (cta_group::2) GEMMs for bf16 layers; DSMOE_B200_CTA_PAIR=0 selects
-  // the single-CTA kernel.
-  static const bool off = [] {
+  // CTA-pair (cta_group::2) GEMMs (gemm_tc2.cu) only with DSMOE_B200_CTA_PAIR=1:
+  // correct on the parity suite but measured at 36% tensor-pipe activity vs
+  // 82% for the single-CTA kernel (profiles/r07_summary.md), so off by default.
+  static const bool on = [] {
     const char* v = std::getenv("DSMOE_B200_CTA_PAIR");
-    return v && v[0] == '0';
+    return v && v[0] == '1';
   }();
-  return !off && L->dtype == DSMOE_B200_BF16;
+  return on && L->dtype == DSMOE_B200_BF16;
 }
 
 namespace {
