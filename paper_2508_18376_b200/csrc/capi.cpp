@@ -628,7 +628,7 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
     const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, kTileM);
     C->mark(4);
     launch_check(launch_gemm_tc(1, &mxp, &mx, &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
-                                nullptr, 256, num_sms(), s, row_token, x, static_cast<long long>(L->d) * 2),
+                                nullptr, 256, num_sms(), s, row_token, row_token ? x : nullptr, static_cast<long long>(L->d) * 2),
                  "gemm1");
     C->mark(5);
     launch_check(launch_gemm_tc(2, &mh, &mh, &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,

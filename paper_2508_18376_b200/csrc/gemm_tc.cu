@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1 + kProducerWarps * 32);  // expect_tx arrive + producer arrivals
+      // expect_tx arrive (+ the 64 cp.async gatherers' arrivals in fused-gather mode)
+      mbar_init(&full[s], args.gather_src ? 1 + kProducerWarps * 32 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < kProducerWarps) {
+  if (warp < kProducerWarps && (args.gather_src != nullptr || threadIdx.x == 0)) {
     // ---------------- producers (warps 0-1).  Thread 0 drives the ring and
     // issues the TMA loads (B always; A for tiles whose rows are contiguous).
     // For gathered tiles all 64 threads fill the A tile straight from the
@@ -168,8 +169,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             cp_async16(d1 + ((j ^ sw) << 4), src1 + kb * 128 + j * 16);
           }
           cp_async_arrive_noinc(&full[stage]);
-        } else {
-          mbar_arrive(&full[stage]);
+        } else if (args.gather_src) {
+          mbar_arrive(&full[stage]);  // keep the fused-gather arrival count for contiguous tiles
         }
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
@@ -253,23 +254,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                 tl.out_col, args.ldo, nc, tl.m_valid, threadIdx.x - kEpiWarp0 * 32);
         epi_sync();
       } else if constexpr (MODE == kEpiScale) {
-        // y = acc * raw score -> bf16, staged 128 columns at a time
+        // y = acc * raw score -> bf16.  All of this thread's columns are read
+        // from TMEM first (4 x 32, packed to bf16 in registers) so the
+        // accumulator is released to the MMA before any global traffic; then
+        // staged 128 columns at a time for coalesced row stores.
         const float sc = valid ? args.row_scale[orow] : 0.f;
-        for (int p0 = 0; p0 < tl.n_mma; p0 += 128) {
-          const int w = min(128, tl.n_mma - p0);
-          for (int c = 32 * half; c < w; c += 64) {
+        uint32_t pk[4][16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = 32 * half + 64 * j;
+          if (c < tl.n_mma) {
             uint32_t v[32];
-            tmem_ld32(taddr + p0 + c, v);
+            tmem_ld32(taddr + c, v);
             tmem_ld_wait();
-            uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]) * sc, __uint_as_float(v[2 * i + 1]) * sc);
-            stage_put(stage_buf, r, c, pk);
+              pk[j][i] = pack_bf16x2(__uint_as_float(v[2 * i]) * sc, __uint_as_float(v[2 * i + 1]) * sc);
           }
-          if (p0 + 128 >= tl.n_mma) {
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const int p0 = 128 * p;
+          if (p0 >= tl.n_mma) break;
+          const int w = min(128, tl.n_mma - p0);
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int c = 32 * half + 64 * jj;  // column inside this 128-wide pass
+            if (c < w) stage_put(stage_buf, r, c, pk[2 * p + jj]);
           }
           epi_sync();
           copy_out(stage_buf, static_cast<__nv_bfloat16*>(args.out) + static_cast<long long>(tl.out_row) * args.ldo +
