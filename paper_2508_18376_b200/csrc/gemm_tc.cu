@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp < kProducerWarps) {
-    if (args.gather_src == nullptr && threadIdx.x != 0) goto producer_done;  // TMA-only: thread 0 drives the ring
+    if (args.gather_src != nullptr || threadIdx.x == 0) {  // TMA-only: thread 0 drives the ring
     // ---------------- producers (warps 0-1).  Thread 0 drives the ring and
     // issues the TMA loads (B always; A for tiles whose rows are contiguous).
     // For gathered tiles all 64 threads fill the A tile straight from the
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
-  producer_done:;
+    }
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
       // ---------------- MMA issuer
