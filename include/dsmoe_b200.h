@@ -212,6 +212,14 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, co
 int dsmoe_b200_combine(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* y_rows, int T,
                        void* out);
 
+/* dsmoe_b200_forward with flags.  DSMOE_B200_RESIDUAL: out = x + moe(x), the
+ * residual step of model_forward_dropped (dropping.hpp:271) fused into the
+ * combine kernel (out may not alias x). */
+#define DSMOE_B200_RESIDUAL 1
+int dsmoe_b200_forward_ex(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
+                          const dsmoe_b200_policy* policy, int logits_mode, int flags, void* out,
+                          dsmoe_b200_drop_stats_t* stats);
+
 /* drop_stats from host fraction arrays (n = T*K*P doubles each). */
 int dsmoe_b200_drop_stats(const double* pre_fraction, const double* post_fraction, long n,
                           int replay_factor, int num_shared, long num_tokens, int d_model,

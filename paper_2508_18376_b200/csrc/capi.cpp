@@ -668,7 +668,8 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
 }
 
 // ------------------------------------- stage: K2 permute/gather, K3, K4, K5
-void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T, void* out) {
+void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T, void* out,
+               const void* resid = nullptr) {
   cudaStream_t s = C->stream;
   const int es = esize(L->dtype);
   const long long Rcap = static_cast<long long>(T) * L->K;
@@ -698,7 +699,7 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
             C->row_scale.as<float>(), fused_gather ? C->row_token.as<int>() : nullptr, pair);
   C->mark(6);
   launch_check(launch_combine(C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d, L->K,
-                              L->S, static_cast<int>(Rcap), num_sms(), s),
+                              L->S, static_cast<int>(Rcap), num_sms(), s, resid),
                "combine");
   g_launches += 1;
 }
@@ -929,6 +930,12 @@ int dsmoe_b200_moe_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
 int dsmoe_b200_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
                        const dsmoe_b200_policy* policy, int logits_mode, void* out,
                        dsmoe_b200_drop_stats_t* stats) {
+  return dsmoe_b200_forward_ex(C, L, x, T, policy, logits_mode, 0, out, stats);
+}
+
+int dsmoe_b200_forward_ex(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                          const dsmoe_b200_policy* policy, int logits_mode, int flags, void* out,
+                          dsmoe_b200_drop_stats_t* stats) {
   return guarded([&] {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
     require_layer(L);
@@ -945,7 +952,7 @@ int dsmoe_b200_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void*
     if (need_frac) C->frac_ws.ensure(static_cast<size_t>(T) * L->K * L->P);
     C->prof_begin();
     stage_route(C, L, x, T, pol, logits_mode, nullptr, nullptr, nullptr, need_frac ? C->frac_ws.as<uint8_t>() : nullptr);
-    stage_ffn(C, L, x, T, out);
+    stage_ffn(C, L, x, T, out, (flags & DSMOE_B200_RESIDUAL) ? x : nullptr);
     C->prof_end();
     if (stats) {
       unsigned long long h[4];

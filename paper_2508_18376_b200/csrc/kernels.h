@@ -67,9 +67,9 @@ int launch_scatter(const int32_t* sel_code, const float* sel_raw, int T, int K, 
 int launch_gather(const void* x, void* xp, const int32_t* row_token, const int* r_total,
                   int row_bytes, int num_sms, cudaStream_t stream);
 int launch_combine(const void* y, int y_bf16, const int32_t* slot_pos, void* out, int T, int d, int K,
-                   int S, int shared_row0, int num_sms, cudaStream_t stream);
+                   int S, int shared_row0, int num_sms, cudaStream_t stream, const void* resid = nullptr);
 int launch_combine2(const void* y, const void* ysh, int y_bf16, const int32_t* slot_pos, void* out, int T, int d,
-                    int K, int S, int shared_row0, int num_sms, cudaStream_t stream);
+                    int K, int S, int shared_row0, int num_sms, cudaStream_t stream, const void* resid = nullptr);
 int launch_fill_f32(float* p, float v, long long n, cudaStream_t stream);
 
 // gemm_tc.cu

@@ -327,7 +327,7 @@ template <typename TY, typename TO>
 __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y, const TY* __restrict__ ysh,
                                                       const int32_t* __restrict__ slot_pos,
                                                       TO* __restrict__ out, int T, int d, int K,
-                                                      int S, int shared_row0) {
+                                                      int S, int shared_row0, const TY* __restrict__ resid) {
   constexpr int V = 16 / sizeof(TY);  // elements per 16-byte vector
   const int nvec = d / V;
   for (int t = blockIdx.x; t < T; t += gridDim.x) {
@@ -335,6 +335,12 @@ __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y, 
       float acc[V];
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[i] = 0.f;
+      if (resid) {  // residual stream x_{l+1} = x_l + moe(x_l) (dropping.hpp:271), fused
+        const uint4 q = *(reinterpret_cast<const uint4*>(resid + static_cast<long long>(t) * d) + v);
+        const TY* e = reinterpret_cast<const TY*>(&q);
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] = static_cast<float>(e[i]);
+      }
       auto add_row = [&](const TY* base, long long row) {
         const uint4 q = __ldcs(reinterpret_cast<const uint4*>(base + row * d) + v);
         const TY* e = reinterpret_cast<const TY*>(&q);
@@ -363,22 +369,23 @@ __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y, 
 
 // y: routed rows (slot_pos); ysh: buffer holding the shared-expert rows
 int launch_combine2(const void* y, const void* ysh, int y_bf16, const int32_t* slot_pos, void* out, int T, int d,
-                    int K, int S, int shared_row0, int num_sms, cudaStream_t stream) {
+                    int K, int S, int shared_row0, int num_sms, cudaStream_t stream, const void* resid) {
   const int grid = T < num_sms * 16 ? (T > 0 ? T : 1) : num_sms * 16;
   if (y_bf16)
     combine_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(y), static_cast<const __nv_bfloat16*>(ysh), slot_pos,
-        static_cast<__nv_bfloat16*>(out), T, d, K, S, shared_row0);
+        static_cast<__nv_bfloat16*>(out), T, d, K, S, shared_row0, static_cast<const __nv_bfloat16*>(resid));
   else
     combine_kernel<float, float><<<grid, 256, 0, stream>>>(static_cast<const float*>(y),
                                                            static_cast<const float*>(ysh), slot_pos,
-                                                           static_cast<float*>(out), T, d, K, S, shared_row0);
+                                                           static_cast<float*>(out), T, d, K, S, shared_row0,
+                                                           static_cast<const float*>(resid));
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
 int launch_combine(const void* y, int y_bf16, const int32_t* slot_pos, void* out, int T, int d, int K,
-                   int S, int shared_row0, int num_sms, cudaStream_t stream) {
-  return launch_combine2(y, y, y_bf16, slot_pos, out, T, d, K, S, shared_row0, num_sms, stream);
+                   int S, int shared_row0, int num_sms, cudaStream_t stream, const void* resid) {
+  return launch_combine2(y, y, y_bf16, slot_pos, out, T, d, K, S, shared_row0, num_sms, stream, resid);
 }
 
 __global__ void fill_f32_kernel(float* p, float v, long long n) {

@@ -102,6 +102,8 @@ SYMBOLS = {
                                          C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsmoe_b200_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
                                      C.c_void_p, C.POINTER(DropStatsC)]),
+    "dsmoe_b200_forward_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
+                                        C.c_int, C.c_void_p, C.POINTER(DropStatsC)]),
     "dsmoe_b200_dispatch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int),
                                       C.POINTER(DropStatsC)]),
@@ -404,18 +406,37 @@ def moe_forward(ctx: Context, layer: MoeLayer, x, routing) -> object:
 
 
 def forward(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None = None, out=None,
-            logits_mode=LOGITS_TENSOR, with_stats=False):
+            logits_mode=LOGITS_TENSOR, with_stats=False, residual=False):
     """route_and_drop + moe_forward in one device launch sequence (the
-    per-layer body of model_forward_dropped, dropping.hpp:263-274)."""
+    per-layer body of model_forward_dropped, dropping.hpp:263-274).
+    residual=True returns x + moe(x) (the residual add fused into combine)."""
     torch = _torch()
     x = _x(x, layer)
     if out is None:
         out = torch.empty_like(x)
+    if residual and out.data_ptr() == x.data_ptr():
+        raise DsmoeError(1, "forward: residual output may not alias the input")
     st = DropStatsC()
-    _chk(lib().dsmoe_b200_forward(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
-                                  C.byref((policy or DropPolicy()).c()), logits_mode,
-                                  C.c_void_p(out.data_ptr()), C.byref(st) if with_stats else None))
+    _chk(lib().dsmoe_b200_forward_ex(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
+                                     C.byref((policy or DropPolicy()).c()), logits_mode, 1 if residual else 0,
+                                     C.c_void_p(out.data_ptr()), C.byref(st) if with_stats else None))
     return (out, st.as_dict()) if with_stats else out
+
+
+def model_forward_dropped(ctx: Context, layers, x, policy: DropPolicy | None = None,
+                          logits_mode=LOGITS_TENSOR):
+    """model_forward_dropped (dropping.hpp:263-274): x_{l+1} = x_l + moe_l(x_l)
+    with per-layer route_and_drop; returns (output, [DropStats per layer])."""
+    torch = _torch()
+    cur = x
+    stats = []
+    bufs = [torch.empty_like(x), torch.empty_like(x)]
+    for i, layer in enumerate(layers):
+        nxt = bufs[i & 1]
+        _, st = forward(ctx, layer, cur, policy, out=nxt, logits_mode=logits_mode, with_stats=True, residual=True)
+        stats.append(st)
+        cur = nxt
+    return cur.clone() if layers else x.clone(), stats
 
 
 # ---------------------------------------------------------------- host math

@@ -39,3 +39,45 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def make_container_fixture():
+    """dsmoe1_small.*: a 2-layer model generated, reconstructed (abs_gate),
+    saved and inferred by the REFERENCE C ABI (oracle/_ref/libdsmoe_ref.so):
+    the container, its calibration/eval token file and dsmoe_infer's JSON."""
+    import ctypes as C
+    import json
+    ref = C.CDLL(os.path.join(ROOT, "oracle", "_ref", "libdsmoe_ref.so"))
+    ref.dsmoe_last_error.restype = C.c_char_p
+    ref.dsmoe_generate_model.argtypes = [C.c_char_p, C.c_uint64, C.c_double, C.c_int, C.POINTER(C.c_void_p)]
+    ref.dsmoe_generate_tokens.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_double, C.c_char_p]
+    ref.dsmoe_reconstruct.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.c_void_p]
+    ref.dsmoe_model_save.argtypes = [C.c_void_p, C.c_char_p]
+    ref.dsmoe_infer.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_char_p)]
+    out_dir = os.path.join(ROOT, "tests", "golden")
+
+    def ok(rc):
+        assert rc == 0, ref.dsmoe_last_error().decode()
+
+    cfg = json.dumps({"d_model": 64, "d_ffn": 128, "num_experts": 8, "top_k": 2, "num_shared_experts": 1,
+                      "gate_prenormalized": False, "num_layers": 2}).encode()
+    m = C.c_void_p()
+    ok(ref.dsmoe_generate_model(cfg, 4242, 1.0, 4, C.byref(m)))
+    tok = os.path.join(out_dir, "dsmoe1_small.tokens").encode()
+    ok(ref.dsmoe_generate_tokens(96, 64, 77, 1.0, tok))
+    rec = C.c_void_p()
+    ok(ref.dsmoe_reconstruct(m, tok, b"abs_gate", C.byref(rec), None))
+    ok(ref.dsmoe_model_save(rec, os.path.join(out_dir, "dsmoe1_small.bin").encode()))
+    res = {}
+    for name, pol in (("none", {"kind": "none"}), ("2t", {"kind": "2t", "t_drop": 0.40}),
+                      ("1t", {"kind": "1t", "t_drop": 0.35, "keep_top1": False})):
+        js = C.c_char_p()
+        ok(ref.dsmoe_infer(rec, tok, json.dumps(pol).encode(), C.byref(js)))
+        res[name] = {"policy": pol, "result": json.loads(js.value.decode())}
+    with open(os.path.join(out_dir, "dsmoe1_small.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    print("container fixture:", {k: v["result"]["drop_rate"] for k, v in res.items()})
+
+
+if __name__ == "__main__" and "--container" in sys.argv:
+    make_container_fixture()
