@@ -220,6 +220,13 @@ int dsmoe_b200_forward_ex(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, co
                           const dsmoe_b200_policy* policy, int logits_mode, int flags, void* out,
                           dsmoe_b200_drop_stats_t* stats);
 
+/* analyze_gating (dropping.hpp:207-228) on the device: Top-K (no drop, always
+ * normalized) of the layer's own gate; host outputs selection_counts[E],
+ * raw_hist[bins], norm_hist[bins] with bin = clamp(int(v * bins), 0, bins-1). */
+int dsmoe_b200_analyze_gating(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
+                              int bins, int logits_mode, long long* selection_counts, long long* raw_hist,
+                              long long* norm_hist);
+
 /* drop_stats from host fraction arrays (n = T*K*P doubles each). */
 int dsmoe_b200_drop_stats(const double* pre_fraction, const double* post_fraction, long n,
                           int replay_factor, int num_shared, long num_tokens, int d_model,

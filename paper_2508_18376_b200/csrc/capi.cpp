@@ -1118,6 +1118,45 @@ int dsmoe_b200_combine(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void*
   });
 }
 
+int dsmoe_b200_analyze_gating(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T, int bins,
+                              int logits_mode, long long* selection_counts, long long* raw_hist,
+                              long long* norm_hist) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(bins >= 2, DSMOE_E_INVALID_ARGUMENT, "analyze_gating: bins must be >= 2");
+    require(T >= 1 && x, DSMOE_E_INVALID_ARGUMENT, "analyze_gating: empty token set");
+    require(selection_counts && raw_hist && norm_hist, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    g_launches = 0;
+    C->ensure(L, T);
+    cudaStream_t s = C->stream;
+    const size_t n = static_cast<size_t>(T) * L->K * L->P;
+    DevBuf di, dr, dn, acc;
+    di.ensure(n * 4);
+    dr.ensure(n * 4);
+    dn.ensure(n * 8);
+    acc.ensure(sizeof(unsigned long long) * (L->E + 2 * bins));
+    cuda_check(cudaMemsetAsync(acc.p, 0, acc.bytes, s), "memset");
+    PolicyResolved pol;
+    pol.normalize = 1;  // analyze_gating always applies normalize_topk (dropping.hpp:211)
+    dsmoe_b200_routing out{di.as<int32_t>(), dr.as<float>(), dn.as<double>(), nullptr};
+    stage_route(C, L, x, T, pol, logits_mode, nullptr, nullptr, &out, nullptr);
+    auto* a = acc.as<unsigned long long>();
+    launch_check(launch_gating_hist(di.as<int32_t>(), dr.as<float>(), dn.as<double>(), T, L->K, L->P, L->E, bins, a,
+                                    a + L->E, a + L->E + bins, num_sms(), s),
+                 "gating histogram");
+    ++g_launches;
+    std::vector<unsigned long long> h(static_cast<size_t>(L->E + 2 * bins));
+    cuda_check(cudaMemcpyAsync(h.data(), acc.p, acc.bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    for (int e = 0; e < L->E; ++e) selection_counts[e] = static_cast<long long>(h[e]);
+    for (int b = 0; b < bins; ++b) {
+      raw_hist[b] = static_cast<long long>(h[L->E + b]);
+      norm_hist[b] = static_cast<long long>(h[L->E + bins + b]);
+    }
+  });
+}
+
 int dsmoe_b200_drop_stats(const double* pre, const double* post, long n, int P, int S, long T, int d, int ffn,
                           dsmoe_b200_drop_stats_t* st) {
   return guarded([&] {

@@ -124,3 +124,9 @@ int launch_pack_gate(int src_dt, int dst_dt, const void* gate, int d, int E, voi
                      cudaStream_t s);
 
 }  // namespace dsb
+
+namespace dsb {
+int launch_gating_hist(const int32_t* idx, const float* raw, const double* norm, int T, int K, int P, int E,
+                       int bins, unsigned long long* counts, unsigned long long* rh, unsigned long long* nh,
+                       int num_sms, cudaStream_t stream);
+}  // namespace dsb

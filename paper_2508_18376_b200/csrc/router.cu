@@ -326,3 +326,52 @@ int launch_gate_logits_exact(const void* x, int x_bf16, const float* gate, float
 }
 
 }  // namespace dsb
+
+namespace dsb {
+
+// ---------------------------------------------------------------------------
+// analyze_gating (dropping.hpp:207-228) histograms on the device: per
+// original selection (copy 0 of the replayed routing) the selected expert
+// count, and uniform-bin histograms of the raw and the normalized scores,
+// bin = clamp(int(v * bins), 0, bins - 1) with the product in double.
+// ---------------------------------------------------------------------------
+__global__ void gating_hist_kernel(const int32_t* __restrict__ idx, const float* __restrict__ raw,
+                                   const double* __restrict__ norm, int T, int K, int P, int E, int bins,
+                                   unsigned long long* __restrict__ counts, unsigned long long* __restrict__ rh,
+                                   unsigned long long* __restrict__ nh) {
+  extern __shared__ unsigned int sh[];  // E + 2 * bins
+  unsigned int* sc = sh;
+  unsigned int* sr = sh + E;
+  unsigned int* sn = sr + bins;
+  for (int i = threadIdx.x; i < E + 2 * bins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const long long n = static_cast<long long>(T) * K;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long t = i / K, s = i - t * K;
+    const long long f = t * K * P + s;
+    atomicAdd(&sc[idx[f] / P], 1u);
+    const int br = static_cast<int>(__dmul_rn(static_cast<double>(raw[f]), static_cast<double>(bins)));
+    const int bn = static_cast<int>(__dmul_rn(norm[f], static_cast<double>(bins)));
+    atomicAdd(&sr[min(max(br, 0), bins - 1)], 1u);
+    atomicAdd(&sn[min(max(bn, 0), bins - 1)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x)
+    if (sc[i]) atomicAdd(&counts[i], static_cast<unsigned long long>(sc[i]));
+  for (int i = threadIdx.x; i < bins; i += blockDim.x) {
+    if (sr[i]) atomicAdd(&rh[i], static_cast<unsigned long long>(sr[i]));
+    if (sn[i]) atomicAdd(&nh[i], static_cast<unsigned long long>(sn[i]));
+  }
+}
+
+int launch_gating_hist(const int32_t* idx, const float* raw, const double* norm, int T, int K, int P, int E,
+                       int bins, unsigned long long* counts, unsigned long long* rh, unsigned long long* nh,
+                       int num_sms, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(E + 2 * bins) * sizeof(unsigned int);
+  if (smem > 48 * 1024) return -1;
+  gating_hist_kernel<<<num_sms, 256, smem, stream>>>(idx, raw, norm, T, K, P, E, bins, counts, rh, nh);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace dsb

@@ -37,7 +37,7 @@ def main():
     print("drop_rate", st["drop_rate"])
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--container" not in sys.argv:
     main()
 
 
@@ -74,9 +74,22 @@ def make_container_fixture():
         js = C.c_char_p()
         ok(ref.dsmoe_infer(rec, tok, json.dumps(pol).encode(), C.byref(js)))
         res[name] = {"policy": pol, "result": json.loads(js.value.decode())}
+    ref.dsmoe_sweep.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_double), C.c_size_t, C.c_int,
+                                C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]
+    ref.dsmoe_analyze_gating.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_char_p),
+                                         C.POINTER(C.c_char_p)]
+    ths = [0.2, 0.3, 0.4, 0.5]
+    arr = (C.c_double * len(ths))(*ths)
+    for kind in ("1t", "2t"):
+        js, cs = C.c_char_p(), C.c_char_p()
+        ok(ref.dsmoe_sweep(rec, tok, kind.encode(), arr, len(ths), 1, C.byref(js), C.byref(cs)))
+        res["sweep_" + kind] = json.loads(js.value.decode())
+    js, cs = C.c_char_p(), C.c_char_p()
+    ok(ref.dsmoe_analyze_gating(rec, tok, 10, C.byref(js), C.byref(cs)))
+    res["gating"] = json.loads(js.value.decode())
     with open(os.path.join(out_dir, "dsmoe1_small.json"), "w") as f:
         json.dump(res, f, indent=1)
-    print("container fixture:", {k: v["result"]["drop_rate"] for k, v in res.items()})
+    print("container fixture:", {k: v["result"]["drop_rate"] for k, v in res.items() if "result" in v})
 
 
 if __name__ == "__main__" and "--container" in sys.argv:
