@@ -294,9 +294,29 @@ def ep_emulated(D, cfg="c2", devices=8, tokens_per_rank=4096, target=0.25, skew=
         x = x + (skew / hot.norm()) * hot
         xs.append(x.to(torch.bfloat16))
     emu = ep.EpEmulator(layer, devices)
-    # t_max for ~target drop under uniform thresholds
     xall = torch.cat(xs)
-    pol, _ = calibrate(ctx, layer, xall, target)
+    # uniform EP: one threshold for all ranks, calibrated to the target global drop rate
+    pol_u, rate_u = calibrate(ctx, layer, xall, target)
+    # load-aware EP (ep_sim.hpp:76-89): t_max calibrated so the GLOBAL drop rate
+    # matches the uniform run — the matched-rate comparison of SURVEY §7.3(7b)
+    seg0, _, _ = D.dispatch(ctx, layer, xall, D.DropPolicy())
+    pre = ep.loads_from_counts(seg0[:, 2], emu.owner, devices)
+
+    def aware_rate(t):
+        th = ep.device_thresholds(pre, t, True)
+        t_unit = torch.from_numpy(th[emu.owner]).cuda()
+        return D.route_and_drop(ctx, layer, xall, D.DropPolicy.two_t_from(t), t_unit=t_unit).stats["drop_rate"]
+
+    lo, hi, best = 0.0, 1.0, None
+    for _ in range(30):
+        t = 0.5 * (lo + hi)
+        r = aware_rate(t)
+        if best is None or abs(r - rate_u) < abs(best[1] - rate_u):
+            best = (t, r)
+        if abs(r - rate_u) < 0.002:
+            break
+        lo, hi = (t, hi) if r < rate_u else (lo, t)
+    pol_a, rate_a = D.DropPolicy.two_t_from(best[0]), best[1]
 
     def run(policy, aware):
         best = None
@@ -311,14 +331,17 @@ def ep_emulated(D, cfg="c2", devices=8, tokens_per_rank=4096, target=0.25, skew=
                 "thresholds": [float(v) for v in rep["thresholds"]], "modeled_speedup": rep["speedup"]}
 
     none = run(D.DropPolicy(), False)
-    uni = run(pol, False)
-    aware = run(pol, True)
-    out = {"devices": devices, "tokens_per_rank": tokens_per_rank, "t_max": pol.t_drop, "no_drop": none,
-           "uniform": uni, "load_aware": aware,
-           "speedup_load_aware_vs_no_drop": none["max_rank_expert_ms"] / aware["max_rank_expert_ms"],
-           "speedup_uniform_vs_no_drop": none["max_rank_expert_ms"] / uni["max_rank_expert_ms"],
-           "speedup_load_aware_vs_uniform_same_tmax": uni["max_rank_expert_ms"] / aware["max_rank_expert_ms"]}
-    return out
+    uni = run(pol_u, False)
+    aware = run(pol_a, True)
+    aware_same = run(pol_u, True)
+    return {"devices": devices, "tokens_per_rank": tokens_per_rank, "skew": skew,
+            "global_drop_rate": {"uniform": rate_u, "load_aware": rate_a},
+            "t": {"uniform": pol_u.t_drop, "load_aware_t_max": pol_a.t_drop},
+            "no_drop": none, "uniform": uni, "load_aware": aware, "load_aware_same_tmax": aware_same,
+            "speedup_load_aware_vs_no_drop": none["max_rank_expert_ms"] / aware["max_rank_expert_ms"],
+            "speedup_uniform_vs_no_drop": none["max_rank_expert_ms"] / uni["max_rank_expert_ms"],
+            "speedup_load_aware_vs_uniform_matched_rate": uni["max_rank_expert_ms"] / aware["max_rank_expert_ms"],
+            "speedup_load_aware_vs_uniform_same_tmax": uni["max_rank_expert_ms"] / aware_same["max_rank_expert_ms"]}
 
 
 def main():
@@ -333,6 +356,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=0, help="tokens for the CPU baseline sample (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ep", action="store_true", help="skip the single-GPU EP emulation")
+    ap.add_argument("--ep", action="store_true", help="run the NCCL expert-parallel path even at N=1")
     ap.add_argument("--extra", default="", help="comma list of extra configs to sweep (c3,c4)")
     args = ap.parse_args()
 
@@ -370,7 +394,15 @@ def main():
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
-    if world > 1:
+    use_ep = world > 1 or args.ep
+    if use_ep:
+        if "MASTER_ADDR" not in os.environ:  # --ep without torchrun: a 1-rank group
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]), RANK="0",
+                              WORLD_SIZE="1")
+            sk.close()
         dist.init_process_group("nccl")
     else:
         dist = None
@@ -386,7 +418,7 @@ def main():
     out = torch.empty_like(x)
     peak_burst, peak_sust, hbm, peak_src = load_peaks()
 
-    if world > 1:
+    if use_ep:
         # ---------------- expert parallelism over NCCL
         from paper_2508_18376_b200 import ep
         m = ep.ExpertParallelMoE(layer)
