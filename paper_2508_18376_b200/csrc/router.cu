@@ -98,27 +98,49 @@ __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterA
 #pragma unroll
     for (int j = 0; j < EPL; ++j)
       if (j < epl) v[j] = __fdiv_rn(v[j], sum);
-    // topk_route: K arg-max rounds; lane s keeps selection s
-    unsigned taken = 0;  // bit j: expert lane + 32 j already selected
-    int my_e = 0;
-    float my_raw = 0.f;
-    for (int s = 0; s < K; ++s) {
-      float bv = 0.f;
-      int be = -1;
+    // topk_route: strict >, lower index first (moe.hpp:193-205) is the
+    // descending order of key = (probability bits << 32) | ~expert — the
+    // probabilities are non-negative floats, so their bit patterns order like
+    // their values.  A warp bitonic sort of the 32*EPL keys (element i =
+    // expert i, held by lane i % 32, slot i / 32) leaves the rank-s key in
+    // slot 0 of lane s.  Padding experts get key 0 and sort last.
+    unsigned long long key[EPL];
 #pragma unroll
-      for (int j = 0; j < EPL; ++j) {
-        const int e = lane + 32 * j;
-        if (j >= epl || e >= E || ((taken >> j) & 1u)) continue;
-        if (be < 0 || v[j] > bv) { bv = v[j]; be = e; }
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-        if (oe >= 0 && (be < 0 || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
-      }
-      if (lane == s) { my_e = be; my_raw = bv; }
-      if ((be & 31) == lane) taken |= 1u << (be >> 5);
+    for (int j = 0; j < EPL; ++j) {
+      const int e = lane + 32 * j;
+      key[j] = e < E ? (static_cast<unsigned long long>(__float_as_uint(v[j])) << 32) |
+                           static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<unsigned>(e))
+                     : 0ull;
     }
+#pragma unroll
+    for (int k = 2; k <= 32 * EPL; k <<= 1) {
+#pragma unroll
+      for (int dist = k >> 1; dist > 0; dist >>= 1) {
+        if (dist >= 32) {  // partner in this lane
+#pragma unroll
+          for (int j = 0; j < EPL; ++j) {
+            const int pj = j ^ (dist >> 5);
+            if (pj > j) {
+              const bool desc = (((j * 32 + lane) & k) == 0);
+              const unsigned long long a = key[j], b = key[pj];
+              const unsigned long long hi = a > b ? a : b, lo = a > b ? b : a;
+              key[j] = desc ? hi : lo;
+              key[pj] = desc ? lo : hi;
+            }
+          }
+        } else {  // partner in lane ^ dist
+#pragma unroll
+          for (int j = 0; j < EPL; ++j) {
+            const int i = j * 32 + lane;
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, key[j], dist);
+            const bool take_max = ((i & dist) == 0) == ((i & k) == 0);
+            key[j] = take_max ? (key[j] > o ? key[j] : o) : (key[j] > o ? o : key[j]);
+          }
+        }
+      }
+    }
+    const int my_e = static_cast<int>(0xFFFFFFFFu - static_cast<unsigned>(key[0] & 0xFFFFFFFFull));
+    const float my_raw = __uint_as_float(static_cast<unsigned>(key[0] >> 32));
     // normalize_topk: ordered double sum over the K selections, then divide
     const bool active = lane < K;
     double dsum = 0.0;
