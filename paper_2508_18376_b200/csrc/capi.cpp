@@ -676,13 +676,13 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   int* r_total = C->scalars.as<int>();
   int* n1 = r_total + 1;
   int* n2 = r_total + 2;
-  // Explicit 16-byte-vector gather into X_perm by default.  DSMOE_B200_GATHER=fused
-  // makes GEMM1's producer warps gather the token rows with cp.async straight
-  // into the swizzled A tiles (bit-identical; measured 2x slower GEMM1 on B200
-  // at C2, the LDGSTS producer cannot keep the tensor pipe fed).
+  // GEMM1's gather warps read the token rows of X straight into the swizzled
+  // A tiles (gemm_tc.cu, warp-per-stage cp.async) by default;
+  // DSMOE_B200_GATHER=explicit materialises X_perm with the 16-byte-vector
+  // gather kernel first (bit-identical results).
   static const bool fused_env = [] {
     const char* v = std::getenv("DSMOE_B200_GATHER");
-    return v && std::string(v) == "fused";
+    return !(v && std::string(v) == "explicit");
   }();
   const bool fused_gather = fused_env && L->dtype == DSMOE_B200_BF16;
   const bool pair = use_pair(L) && !fused_gather;

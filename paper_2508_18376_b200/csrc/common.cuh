@@ -101,6 +101,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* map, uint64_t
       : "memory");
 }
 
+// Same, with an L2 cache-policy hint (createpolicy) on the global reads.
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const void* map, uint64_t* bar, int c0, int c1,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+
 // 16-byte cp.async global -> shared (L2 only), and the arrive-on of all of
 // this thread's prior cp.async on an mbarrier (counted in its init count).
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {

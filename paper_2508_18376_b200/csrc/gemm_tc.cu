@@ -4,14 +4,19 @@
 // (/root/reference/proj/include/dsmoe/moe.hpp:213-231) and the gate matmul of
 // gate_scores (moe.hpp:174 -> matrix.hpp:47-64) for bf16 layers.
 //
-// One CTA per SM (320 threads, warp-specialised):
+// One CTA per SM (448 threads, warp-specialised):
 //   warp 0      TMA producer: A (128 x 64) and B (N x 64) bf16 tiles, SWIZZLE_128B,
 //               4-stage smem ring guarded by full/empty mbarriers;
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256,
+//   warps 1..4  row gatherers (GEMM1 with fused gather only): warp g owns ring
+//               stage g and fills its A tile straight from the token rows of X
+//               (16-byte cp.async, one warp instruction = 4 rows x 128 B, so
+//               every request is a whole L2 line), then proxy-fences and
+//               arrives on the stage's full barrier — no permuted copy of X;
+//   warp 5      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256,
 //               K=16 per instruction), fp32 accumulators in TMEM, two
 //               accumulator stages (2 x 256 columns) so the epilogue of tile i
 //               overlaps the MMAs of tile i+1;
-//   warps 2..9  epilogue (two warps per TMEM lane quarter, alternating 32-column
+//   warps 6..13 epilogue (two warps per TMEM lane quarter, alternating 32-column
 //               chunks): tcgen05.ld 32x32b -> registers -> fused op -> global.
 // Work items (GemmTile) are produced on the device by plan_tiles (permute.cu)
 // and walked in a static round-robin over the persistent CTAs.
@@ -23,6 +28,8 @@
 //               bf16 store into H (K3);
 //   kEpiScale   y = acc * row_scale[row] (the raw gate score, moe.hpp:235-237),
 //               bf16 store into Y (K4).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace dsb {
@@ -31,10 +38,11 @@ constexpr int kStages = 4;
 constexpr int kABytes = kTileM * kTileK * 2;       // 16 KB
 constexpr int kBBytesMax = 256 * kTileK * 2;       // 32 KB
 constexpr int kStageBytes = kABytes + kBBytesMax;  // 48 KB
-constexpr int kProducerWarps = 2;   // warps 0-1: TMA + cp.async row gather
-constexpr int kMmaWarp = 2;         // warp 2: TMEM alloc + tcgen05.mma issue
-constexpr int kEpiWarp0 = 3;        // warps 3-10: epilogue
-constexpr int kGemmThreads = 352;
+constexpr int kGatherWarp0 = 1;     // warps 1-4: fused row gather, warp 1 + s owns stage s
+constexpr int kGatherWarps = kStages;
+constexpr int kMmaWarp = 5;         // warp 5: TMEM alloc + tcgen05.mma issue
+constexpr int kEpiWarp0 = 6;        // warps 6-13: epilogue
+constexpr int kGemmThreads = 448;
 constexpr int kEpiThreads = 256;
 constexpr int kAccCols = 256;
 constexpr int kGemmSmem = kStages * kStageBytes + 128 * 256 /*output stage*/ + 1024 /*align*/ + 256 /*barriers*/;
@@ -51,6 +59,7 @@ struct GemmArgs {
   const int* row_token;    // gathered A tiles: token of each permuted row
   const void* gather_src;  // gathered A tiles: X (bf16, gather_ld bytes per row)
   long long gather_ld;
+  int flags;               // bit 0: B loads evict-first in L2 (fused gather)
 };
 
 __device__ __forceinline__ float silu_fast(float g) { return g / (1.0f + __expf(-g)); }
@@ -101,10 +110,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int lane = threadIdx.x & 31;
   const int ntiles = *args.num_tiles;
 
+  const bool fused = MODE == kEpiSwiGLU && args.gather_src != nullptr;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      // expect_tx arrive (+ the 64 cp.async gatherers' arrivals in fused-gather mode)
-      mbar_init(&full[s], args.gather_src ? 1 + kProducerWarps * 32 : 1);
+      mbar_init(&full[s], fused ? 2 : 1);  // TMA expect_tx arrive (+ the stage's gather warp)
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -125,57 +134,96 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < kProducerWarps) {
-    if (args.gather_src != nullptr || threadIdx.x == 0) {  // TMA-only: thread 0 drives the ring
-    // ---------------- producers (warps 0-1).  Thread 0 drives the ring and
-    // issues the TMA loads (B always; A for tiles whose rows are contiguous).
-    // For gathered tiles all 64 threads fill the A tile straight from the
-    // token rows of X with 16-byte cp.async into the SWIZZLE_128B layout the
-    // UMMA descriptor expects (no permuted copy of X in HBM); their
-    // completion arrives on the same full barrier (.noinc).
-    const int pt = threadIdx.x;  // 0..63
-    int stage = 0;
-    uint32_t phase = 0;
-    GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
-      if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
-      const bool alt = (tl.m_live & kTileAltA) != 0;
-      const bool gather = (tl.m_live & kTileGatherA) != 0;
-      const void* ma = alt ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
-      // this thread's two rows (pt, pt + 64); rows past the segment read token 0
-      const char* src0 = nullptr;
-      const char* src1 = nullptr;
-      if (gather) {
-        const int* rt = args.row_token + tl.a_row;
-        const long long t0 = pt < tl.m_valid ? rt[pt] : 0;
-        const long long t1 = pt + 64 < tl.m_valid ? rt[pt + 64] : 0;
-        src0 = static_cast<const char*>(args.gather_src) + t0 * args.gather_ld;
-        src1 = static_cast<const char*>(args.gather_src) + t1 * args.gather_ld;
-      }
-      for (int kb = 0; kb < tl.nkb; ++kb) {
-        uint8_t* sa = smem + stage * kStageBytes;
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (pt == 0) {
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer: B always; A for tiles whose rows are
+      // contiguous (explicit X_perm, or X itself for shared experts)
+      int stage = 0;
+      uint32_t phase = 0;
+      // fused gather: weights stream through L2 evict-first so the token rows
+      // of X (gathered evict-last, ~48 reads each) stay resident
+      uint64_t pol_b;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_b));
+      GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
+        if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
+        const bool alt = (tl.m_live & kTileAltA) != 0;
+        const bool gather = fused && (tl.m_live & kTileGatherA) != 0;
+        const void* ma = alt ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
+        for (int kb = 0; kb < tl.nkb; ++kb) {
+          uint8_t* sa = smem + stage * kStageBytes;
+          mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], (gather ? 0u : static_cast<uint32_t>(kABytes)) + args.b_bytes);
           if (!gather) tma_load_2d(sa, ma, &full[stage], kb * kTileK, tl.a_row);
-          tma_load_2d(sa + kABytes, &mapB, &full[stage], kb * kTileK, tl.b_row);
+          if (fused && (args.flags & 1))
+            tma_load_2d_hint(sa + kABytes, &mapB, &full[stage], kb * kTileK, tl.b_row, pol_b);
+          else
+            tma_load_2d(sa + kABytes, &mapB, &full[stage], kb * kTileK, tl.b_row);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if (gather) {
-          const uint32_t d0 = smem_u32(sa) + pt * 128, d1 = d0 + 64 * 128;
-          const int sw = pt & 7;  // (pt + 64) & 7 == pt & 7
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            cp_async16(d0 + ((j ^ sw) << 4), src0 + kb * 128 + j * 16);
-            cp_async16(d1 + ((j ^ sw) << 4), src1 + kb * 128 + j * 16);
-          }
-          cp_async_arrive_noinc(&full[stage]);
-        } else if (args.gather_src) {
-          mbar_arrive(&full[stage]);  // keep the fused-gather arrival count for contiguous tiles
-        }
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
+  } else if (warp < kGatherWarp0 + kGatherWarps) {
+    if (fused) {
+      // ---------------- row gatherers.  Warp g fills ring stage g, i.e. the
+      // k-blocks whose running index (over this CTA's tiles) is g mod 4.
+      // Lane l copies 16-byte chunk (l & 7) of row 4i + (l >> 3) in
+      // instruction i; the chunk lands at its SWIZZLE_128B position.
+      const int gw = warp - kGatherWarp0;
+      const int rr = lane >> 3, ch = lane & 7;
+      const uint32_t sa = smem_u32(smem + gw * kStageBytes);
+      const char* X = static_cast<const char*>(args.gather_src);
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      uint32_t phase = 0;
+      int g = 0;  // running k-block index
+      // descriptor and row tokens are loaded one tile ahead: the loads of tile
+      // i+1 are in flight while tile i's k-blocks are gathered
+      auto load_tok = [&](const GemmTile& tl, int* tok) {
+        if ((tl.m_live & kTileGatherA) == 0) return;
+        const int* rt = args.row_token + tl.a_row;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tok[j] = rt[lane + 32 * j < tl.m_valid ? lane + 32 * j : 0];
+      };
+      const int t0 = blockIdx.x, gs = gridDim.x;
+      GemmTile cur = t0 < ntiles ? args.tiles[t0] : GemmTile{};
+      GemmTile nxt = t0 + gs < ntiles ? args.tiles[t0 + gs] : GemmTile{};
+      int tok[4] = {0, 0, 0, 0};
+      if (t0 < ntiles) load_tok(cur, tok);
+      for (int t = t0; t < ntiles; t += gs) {
+        int tok_n[4] = {0, 0, 0, 0};
+        if (t + gs < ntiles) load_tok(nxt, tok_n);
+        const GemmTile nxt2 = t + 2 * gs < ntiles ? args.tiles[t + 2 * gs] : GemmTile{};
+        const GemmTile& tl = cur;
+        const bool gather = (tl.m_live & kTileGatherA) != 0;
+        const int first = (gw - g) & (kStages - 1);  // first k-block of this tile owned by this warp
+        for (int kb = first; kb < tl.nkb; kb += kStages) {
+          mbar_wait(&empty[gw], phase ^ 1);
+          if (gather) {
+            const char* src = X + kb * 128 + ch * 16;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int row = 4 * i + rr;
+              const long long tk = __shfl_sync(0xffffffffu, tok[i >> 3], 4 * (i & 7) + rr);
+              const uint32_t dst = sa + row * 128 + ((ch ^ (row & 7)) << 4);
+              asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst),
+                           "l"(src + tk * args.gather_ld), "l"(pol)
+                           : "memory");
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tcgen05 reads
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[gw]);
+          phase ^= 1;
+        }
+        g += tl.nkb;
+        cur = nxt;
+        nxt = nxt2;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tok[j] = tok_n[j];
+      }
     }
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
@@ -322,8 +370,12 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
                    int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token,
                    const void* gather_src, long long gather_ld) {
+  static const int flags = [] {
+    const char* v = std::getenv("DSMOE_B200_GEMM_FLAGS");
+    return v ? std::atoi(v) : 0;
+  }();
   GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128), row_token,
-             gather_src, gather_ld};
+             gather_src, gather_ld, flags};
   const int grid = max_tiles < num_sms ? (max_tiles > 0 ? max_tiles : 1) : num_sms;
   cudaError_t err;
   switch (mode) {

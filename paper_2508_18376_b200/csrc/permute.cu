@@ -341,18 +341,30 @@ __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y, 
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] = static_cast<float>(e[i]);
       }
-      auto add_row = [&](const TY* base, long long row) {
-        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(base + row * d) + v);
+      auto add_vec = [&](const uint4& q) {
         const TY* e = reinterpret_cast<const TY*>(&q);
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] += static_cast<float>(e[i]);
       };
-      for (int s = 0; s < K; ++s) {
-        const int p = slot_pos[static_cast<long long>(t) * K + s];
-        if (p >= 0) add_row(y, p);
+      // every kept row's vector is requested before the first add (memory-level
+      // parallelism), then summed in slot order (deterministic)
+      const int32_t* sp = slot_pos + static_cast<long long>(t) * K;
+      for (int s0 = 0; s0 < K; s0 += 8) {
+        uint4 q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int p = s0 + j < K ? sp[s0 + j] : -1;
+          q[j] = p >= 0 ? __ldcs(reinterpret_cast<const uint4*>(y + static_cast<long long>(p) * d) + v)
+                        : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (s0 + j < K && sp[s0 + j] >= 0) add_vec(q[j]);
       }
       for (int s = 0; s < S; ++s)
-        add_row(ysh, static_cast<long long>(shared_row0) + static_cast<long long>(s) * T + t);
+        add_vec(__ldcs(reinterpret_cast<const uint4*>(
+                           ysh + (static_cast<long long>(shared_row0) + static_cast<long long>(s) * T + t) * d) +
+                       v));
       TO* o = out + static_cast<long long>(t) * d + static_cast<long long>(v) * V;
       if constexpr (sizeof(TO) == 2) {
         uint32_t pk[V / 2];

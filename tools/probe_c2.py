@@ -42,7 +42,7 @@ def main():
         for _ in range(3): D.forward(ctx, layer, x, pol)
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = 10
+        n = int(os.environ.get("ITERS", 30))
         s.record()
         for _ in range(n): D.forward(ctx, layer, x, pol)
         e.record(); torch.cuda.synchronize()
