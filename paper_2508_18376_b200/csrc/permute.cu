@@ -21,6 +21,45 @@ namespace dsb {
 
 __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
 
+// Block-wide exclusive scan of v[0..n) in shared memory, in place; returns
+// the total.  Every thread of the block must call it.
+__device__ int block_excl_scan(int* v, int n) {
+  __shared__ int wsum[32];
+  __shared__ int s_tot, s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int x = i < n ? v[i] : 0;
+    int incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int ws = lane < nw ? wsum[lane] : 0;
+      int wi = ws;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      if (lane < nw) wsum[lane] = wi - ws;
+      if (lane == 31) s_tot = wi;
+    }
+    __syncthreads();
+    if (i < n) v[i] = s_carry + wsum[warp] + incl - x;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += s_tot;
+    __syncthreads();
+  }
+  return s_carry;
+}
+
 // --------------------------------------------------------------------------
 // scan + plan (one block of 1024 threads)
 // --------------------------------------------------------------------------
@@ -40,25 +79,24 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     const int s = u - a.num_routed;
     return UnitSeg{a.shared_row0 + s * a.T, a.T, a.T, 0};
   };
-  // tile counts, exclusive scan (single pass: nu <= 2048, two per thread)
+  // tile counts per unit, then block-wide exclusive scans
   for (int u = threadIdx.x; u < nu; u += blockDim.x) {
     const UnitInfo& ui = a.units[unit_of(u)];
     const UnitSeg sg = seg_of(u);
     const int mt_all = cdiv(sg.n_tot, tm), mt_full = cdiv(sg.n_full, tm);
     int c1 = 0;
     for (int p = 0; p < ui.nsub; ++p) c1 += cdiv(ui.sub_wpad[p], kChunk) * (p == 0 ? mt_all : mt_full);
-    off1[u + 1] = c1;
-    off2[u + 1] = mt_all * ntd;
+    off1[u] = c1;
+    off2[u] = mt_all * ntd;
   }
   __syncthreads();
+  const int tot1 = block_excl_scan(off1, nu);
+  const int tot2 = block_excl_scan(off2, nu);
   if (threadIdx.x == 0) {
-    off1[0] = off2[0] = 0;
-    for (int u = 0; u < nu; ++u) {
-      off1[u + 1] += off1[u];
-      off2[u + 1] += off2[u];
-    }
-    if (a.n1 && blockIdx.x == 0) *a.n1 = off1[nu];
-    if (a.n2 && blockIdx.x == 0) *a.n2 = off2[nu];
+    off1[nu] = tot1;
+    off2[nu] = tot2;
+    if (a.n1 && blockIdx.x == 0) *a.n1 = tot1;
+    if (a.n2 && blockIdx.x == 0) *a.n2 = tot2;
   }
   __syncthreads();
   auto find = [&](const int* off, int i) {  // largest u with off[u] <= i
@@ -172,15 +210,16 @@ __global__ void __launch_bounds__(1024) seg_plan_kernel(const int* __restrict__ 
                                                         int* __restrict__ r_total, const PlanArgs a, int do_plan) {
   __shared__ int off1[kPlanMaxUnits + 1], off2[kPlanMaxUnits + 1];
   __shared__ UnitSeg s_seg[256];
-  if (threadIdx.x == 0) {
-    int start = 0;
-    for (int u = 0; u < E; ++u) {
-      const int nf = code_tot[2 * u], nm = code_tot[2 * u + 1];
-      s_seg[u] = UnitSeg{start, nf, nf + nm, 0};
-      start += nf + nm;
-    }
-    if (blockIdx.x == 0) *r_total = start;
+  __shared__ int s_rows[256];
+  // unit segments: rows of unit u start after all rows of units < u
+  for (int u = threadIdx.x; u < E; u += blockDim.x) s_rows[u] = code_tot[2 * u] + code_tot[2 * u + 1];
+  __syncthreads();
+  const int rtot = block_excl_scan(s_rows, E);
+  for (int u = threadIdx.x; u < E; u += blockDim.x) {
+    const int nf = code_tot[2 * u], nm = code_tot[2 * u + 1];
+    s_seg[u] = UnitSeg{s_rows[u], nf, nf + nm, 0};
   }
+  if (threadIdx.x == 0 && blockIdx.x == 0) *r_total = rtot;
   __syncthreads();
   if (blockIdx.x == 0)
     for (int u = threadIdx.x; u < E; u += blockDim.x) {

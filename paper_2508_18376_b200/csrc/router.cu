@@ -206,11 +206,163 @@ __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterA
   }
 }
 
+// Quad-per-token variant for E <= 4 * EPT (64): lane q of a token's quad
+// holds experts [q*EPT, (q+1)*EPT) in registers.  The softmax denominator is
+// one ascending-e chain of float adds handed from lane to lane (the
+// reference's summation order), the arg-max rounds reduce (value desc, index
+// asc) across the quad, and each lane finishes the slots j = q mod 4.
+// One block = 32 tokens = one scatter chunk (kRouterChunk).
+template <int EPT>
+__global__ void __launch_bounds__(kRouterChunk * 4) router_quad_kernel(const RouterArgs a) {
+  extern __shared__ int s_hist[];  // 2E
+  __shared__ uint64_t tab[32];
+  __shared__ unsigned long long s_n1, s_nh;
+  const int E = a.E, K = a.K, P = a.P;
+  const int lane = threadIdx.x & 31, q = lane & 3, qbase = lane & ~3;
+  for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) s_hist[i] = 0;
+  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+  if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }
+  __syncthreads();
+  unsigned long long n1 = 0, nh = 0;
+  const int t = blockIdx.x * kRouterChunk + (threadIdx.x >> 2);
+  const bool tok_ok = t < a.T;  // uniform across the quad
+  const int e0 = q * EPT;
+  const float* row = a.logits + static_cast<long long>(tok_ok ? t : 0) * a.ld_logits;
+  float v[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) v[i] = (tok_ok && e0 + i < E) ? row[e0 + i] : -INFINITY;
+  // softmax_inplace (matrix.hpp:68-78): max (order-free), expf, ascending-e sum, divide
+  float mx = v[0];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) mx = (mx < v[i]) ? v[i] : mx;
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    const float other = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (mx < other) ? other : mx;
+  }
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) v[i] = e0 + i < E ? expf_tab(__fsub_rn(v[i], mx), tab) : 0.0f;
+  float sum = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (q == k) {
+#pragma unroll
+      for (int i = 0; i < EPT; ++i)
+        if (e0 + i < E) sum = __fadd_rn(sum, v[i]);
+    }
+    sum = __shfl_sync(0xffffffffu, sum, qbase | k);
+  }
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) v[i] = __fdiv_rn(v[i], sum);
+  // topk_route (moe.hpp:193-205): K rounds; round winner = max value, lowest index
+  uint32_t taken = 0u;
+  float sraw[16];
+  int sel[16];
+  for (int j = 0; j < K; ++j) {
+    int be = 1 << 30;
+    float bv = 0.0f;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i)
+      if (e0 + i < E && !((taken >> i) & 1u) && (be == (1 << 30) || v[i] > bv)) { be = e0 + i; bv = v[i]; }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      if (oe != (1 << 30) && (be == (1 << 30) || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
+    }
+    if (be - e0 >= 0 && be - e0 < EPT) taken |= 1u << (be - e0);
+    sel[j] = be;
+    sraw[j] = bv;
+  }
+  // normalize_topk (dropping.hpp:60-72)
+  double dsum = 0.0;
+  if (a.normalize) {
+    for (int j = 0; j < K; ++j) dsum = __dadd_rn(dsum, static_cast<double>(sraw[j]));
+    if (tok_ok && q == 0 && !(dsum > 0.0)) atomicOr(&a.counters[2], 1ull);
+  }
+  // this lane's slots j = q, q+4, ...; top_slot = first maximum of ns (dropping.hpp:99)
+  double nsj[4];
+  double tv = -1.0;
+  int ts = 1 << 30;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int j = q + 4 * m;
+    nsj[m] = 0.0;
+    if (j < K) {
+      nsj[m] = a.normalize ? __ddiv_rn(static_cast<double>(sraw[j]), dsum) : static_cast<double>(sraw[j]);
+      if (ts == (1 << 30) || nsj[m] > tv) { tv = nsj[m]; ts = j; }
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, tv, o);
+    const int os = __shfl_xor_sync(0xffffffffu, ts, o);
+    if (os != (1 << 30) && (ts == (1 << 30) || ov > tv || (ov == tv && os < ts))) { tv = ov; ts = os; }
+  }
+  // apply_bands_fn (dropping.hpp:93-122) on this lane's slots
+  if (tok_ok) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int j = q + 4 * m;
+      if (j >= K) break;
+      const int my_e = sel[j];
+      const double ns = nsj[m];
+      int lv = 2;
+      if (a.kind != 0) {
+        double tmaj = a.t_major, tmin = a.t_minor;
+        if (a.t_unit) {
+          const double own = a.t_unit[my_e];
+          tmaj = __dadd_rn(own, a.maj_off);
+          tmin = __dadd_rn(own, a.min_off);
+        }
+        lv = ns >= tmin ? 2 : (ns >= tmaj ? 1 : 0);
+        if (a.keep_top1 && j == ts) lv = 2;
+      }
+      for (int cp = 0; cp < P; ++cp) {
+        const uint8_t fc = P == 1 ? static_cast<uint8_t>(lv) : (cp == 0 ? (lv > 0 ? 2 : 0) : (lv == 2 ? 2 : 0));
+        n1 += fc == 2;
+        nh += fc == 1;
+        const long long g = static_cast<long long>(t) * K * P + static_cast<long long>(cp) * K + j;
+        if (a.idx) a.idx[g] = my_e * P + cp;
+        if (a.raw) a.raw[g] = sraw[j];
+        if (a.norm) a.norm[g] = ns;
+        if (a.frac) a.frac[g] = fc;
+      }
+      const long long qi = static_cast<long long>(t) * K + j;
+      a.sel_code[qi] = lv > 0 ? my_e * 4 + lv : -1;
+      a.sel_raw[qi] = sraw[j];
+      if (lv > 0) atomicAdd(&s_hist[2 * my_e + (lv == 2 ? 0 : 1)], 1);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+    nh += __shfl_xor_sync(0xffffffffu, nh, o);
+  }
+  if (lane == 0 && (n1 | nh)) {
+    atomicAdd(&s_n1, n1);
+    atomicAdd(&s_nh, nh);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * E; i += blockDim.x)
+    a.cnt_chunk[static_cast<long long>(blockIdx.x) * 2 * E + i] = s_hist[i];
+  if (threadIdx.x == 0) {
+    atomicAdd(&a.counters[0], s_n1);
+    atomicAdd(&a.counters[1], s_nh);
+  }
+}
+
 int launch_router(const RouterArgs& a, cudaStream_t stream) {
   if (a.K > kMaxK || a.E > 32 * kMaxEPL || a.K < 1 || a.K > a.E) return -1;
   const int blocks = (a.T + kRouterChunk - 1) / kRouterChunk;
   const size_t smem = static_cast<size_t>(2 * a.E) * sizeof(int);
   if (blocks <= 0) return 0;
+  if (a.E <= 64 && a.K <= 16) {
+    if (a.E <= 32)
+      router_quad_kernel<8><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+    else
+      router_quad_kernel<16><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  }
   const int epl = (a.E + 31) / 32;
   if (epl <= 1)
     router_kernel<1><<<blocks, kRouterChunk * 32, smem, stream>>>(a);
