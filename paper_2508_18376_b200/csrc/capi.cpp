@@ -606,7 +606,8 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
 // allocated), alt A = x (shared experts), H in the context, Y = y (ld d).
 void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long long a_rows, const void* x,
                int T, const int* n1, const int* n2, long long max1, long long max2, long long h_rows, void* y,
-               const float* row_scale, const int* row_token = nullptr, bool pair = false) {
+               const float* row_scale, const int* row_token = nullptr, bool pair = false, long long y_rows = -1) {
+  if (y_rows < 0) y_rows = h_rows;
   cudaStream_t s = C->stream;
   const int mt1 = static_cast<int>(std::min<long long>(max1, 1 << 30));
   const int mt2 = static_cast<int>(std::min<long long>(max2, 1 << 30));
@@ -626,13 +627,17 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
     const CUtensorMap mx = make_map(x ? x : rows, x ? T : a_rows, L->d, L->d, kTileM);
     const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, kTileM);
     const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, kTileM);
+    // TMA-store targets: 32-row boxes (one per epilogue warp)
+    const CUtensorMap my = make_map(y, y_rows, L->d, L->d, 32);
+    const CUtensorMap mh32 = make_map(C->H.p, h_rows, L->hstride, L->hstride, 32);
     C->mark(4);
     launch_check(launch_gemm_tc(1, &mxp, &mx, &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
-                                nullptr, 256, num_sms(), s, row_token, row_token ? x : nullptr, static_cast<long long>(L->d) * 2),
+                                nullptr, 256, num_sms(), s, row_token, row_token ? x : nullptr, static_cast<long long>(L->d) * 2,
+                                &mh32),
                  "gemm1");
     C->mark(5);
     launch_check(launch_gemm_tc(2, &mh, &mh, &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,
-                                256, num_sms(), s),
+                                256, num_sms(), s, nullptr, nullptr, 0, &my),
                  "gemm2");
   } else {
     SimtArgs g1{};
@@ -1093,7 +1098,7 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
     pa.tile_m = pair ? 256 : kTileM;
     launch_check(launch_plan(pa, num_sms(), s), "plan");
     ++g_launches;
-    run_gemms(C, L, rows, nrows, nullptr, 0, nn + 1, nn + 2, max1, max2, h_rows, y_out, row_scale, nullptr, pair);
+    run_gemms(C, L, rows, nrows, nullptr, 0, nn + 1, nn + 2, max1, max2, h_rows, y_out, row_scale, nullptr, pair, nrows);
     // keep the caller's buffers alive until the work is done
     cuda_check(cudaStreamSynchronize(s), "sync");
   });

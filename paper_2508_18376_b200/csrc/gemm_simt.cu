@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const SimtArgs a) {
           int brow;
           bool ok = true;
           if (MODE == kSimtSwiGLU) {
-            brow = j < 32 ? sb * 32 + j : nc + sb * 32 + (j - 32);
+            brow = sb * 64 + j;  // group sb: [32 W1 rows | 32 W3 rows] (w13_row_of)
           } else {
             brow = sb * 64 + j;
             ok = brow < tl.n_mma;

@@ -59,43 +59,73 @@ struct GemmArgs {
   const int* row_token;    // gathered A tiles: token of each permuted row
   const void* gather_src;  // gathered A tiles: X (bf16, gather_ld bytes per row)
   long long gather_ld;
-  int flags;               // bit 0: B loads evict-first in L2 (fused gather)
+  int flags;               // DSMOE_B200_GEMM_FLAGS: bit 0 B loads evict-first (fused gather), bit 1 no TMA stores
+  int tma_store;           // bf16 outputs leave through mapO
 };
 
-__device__ __forceinline__ float silu_fast(float g) { return g / (1.0f + __expf(-g)); }
+// swish(g) = g * sigmoid(g) = 0.5 g (1 + tanh(g / 2)): one MUFU op (tanh.approx,
+// rel. err ~2^-11, below the bf16 rounding of h that follows).
+__device__ __forceinline__ float silu_fast(float g) {
+  const float hg = 0.5f * g;
+  float th;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(hg));
+  return fmaf(hg, th, hg);
+}
 
-// Output staging for coalesced stores: 128 rows x 256 B (128 bf16) in smem,
-// 16-byte chunks XOR-swizzled by row so both the per-row writes (one row per
-// thread) and the row-contiguous reads are bank-conflict free.
-constexpr int kStageOutBytes = 128 * 256;
+// Output staging, per epilogue warp: a 4 KB slot = its 32 rows x 64 bf16
+// columns as one TMA box (32 rows x 128 B, SWIZZLE_128B: 16-byte chunk k of
+// row rr at rr*128 + ((k ^ (rr & 7)) << 4)).  Every warp stores on its own
+// (lane 0 issues the TMA store and owns the bulk group), so the epilogue has
+// no CTA-wide barriers; rows cut by the segment end are copied out masked.
+constexpr int kWarpSlot = 32 * 128;
+constexpr int kStageOutBytes = 8 * kWarpSlot;
 
-__device__ __forceinline__ void stage_put(uint8_t* buf, int r, int col, const uint32_t* pk) {
+// columns [col, col + 32) of this lane's row (pk: 16 packed bf16 pairs)
+__device__ __forceinline__ void warp_put(uint8_t* slot, int lane, int col, const uint32_t* pk) {
+  uint8_t* rowp = slot + lane * 128;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int k = (col >> 3) + i;
-    *reinterpret_cast<uint4*>(buf + r * 256 + ((k ^ (r & 15)) << 4)) =
+    *reinterpret_cast<uint4*>(rowp + ((k ^ (lane & 7)) << 4)) =
         make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
   }
 }
 
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// wait until this warp's previous TMA store has read the slot
+__device__ __forceinline__ void warp_slot_acquire(int lane) {
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
+}
 
-// rows < m_valid of the staged tile (width bf16 columns) -> out (row stride ld)
-__device__ __forceinline__ void copy_out(const uint8_t* buf, __nv_bfloat16* out, long long ld, int width,
-                                         int m_valid, int tid) {
-  const int cpr = width >> 3;  // 16-byte chunks per row
-  for (int i = tid; i < 128 * cpr; i += 256) {
-    const int row = i / cpr, k = i - row * cpr;
-    if (row < m_valid)
-      *reinterpret_cast<uint4*>(out + row * ld + (k << 3)) =
-          *reinterpret_cast<const uint4*>(buf + row * 256 + ((k ^ (row & 15)) << 4));
+// slot -> out rows [row0, row0 + min(32, nvalid)), columns [col0, col0 + 64)
+__device__ __forceinline__ void warp_store(const uint8_t* slot, const CUtensorMap* mapO, const GemmArgs& args,
+                                           int row0, int col0, int nvalid, bool full, int lane) {
+  if (full && args.tma_store) {
+    fence_proxy_async();  // generic smem writes -> async-proxy (TMA) reads
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(mapO, smem_u32(slot), col0, row0);
+      bulk_commit();
+    }
+  } else {
+    __syncwarp();
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.out);
+    const int k = lane & 7;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int rr = 4 * i + (lane >> 3);
+      if (rr < nvalid)
+        *reinterpret_cast<uint4*>(out + static_cast<long long>(row0 + rr) * args.ldo + col0 + 8 * k) =
+            *reinterpret_cast<const uint4*>(slot + rr * 128 + ((k ^ (rr & 7)) << 4));
+    }
   }
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
-                   const __grid_constant__ CUtensorMap mapB, const GemmArgs args) {
+                   const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapO,
+                   const GemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
@@ -124,6 +154,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch(&mapA);
     tma_prefetch(&mapA2);
     tma_prefetch(&mapB);
+    if (args.tma_store) tma_prefetch(&mapO);
   }
   if (warp == kMmaWarp) {
     tmem_alloc(tmem_slot, 2 * kAccCols);
@@ -226,38 +257,39 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      const uint32_t sbase = smem_u32(smem);
-      GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
-        if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
-        const uint32_t idesc = idesc_bf16(kTileM, tl.n_mma);
-        const uint32_t dtmem = tmem_base + acc * kAccCols;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // ---------------- MMA issuer: the whole warp walks the loop (warp-uniform
+    // control, so descriptors live in uniform registers); one elected lane
+    // issues the tcgen05.mma / commit instructions.
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const uint64_t d0 = sdesc_sw128(smem_u32(smem));  // stage 0 A; + (bytes >> 4) moves the start address
+    GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
+      if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
+      const uint32_t idesc = idesc_bf16(kTileM, tl.n_mma);
+      const uint32_t dtmem = tmem_base + acc * kAccCols;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < tl.nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        for (int kb = 0; kb < tl.nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t sa = sbase + stage * kStageBytes;
-          const uint64_t adesc = sdesc_sw128(sa);
-          const uint64_t bdesc = sdesc_sw128(sa + kABytes);
+        const uint64_t adesc = d0 + static_cast<uint64_t>(stage * (kStageBytes >> 4));
+        const uint64_t bdesc = adesc + (kABytes >> 4);
+        if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kTileK / 16; ++k) {
-            // advance 16 bf16 = 32 B along K inside the 128 B swizzle row
+          for (int k = 0; k < kTileK / 16; ++k)  // 16 bf16 = 32 B along K inside the 128 B swizzle row
             umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-          }
           umma_commit(&empty[stage]);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else {
     // ---------------- epilogue warps 2..9: two per TMEM lane quarter, 32-column
@@ -265,79 +297,91 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = (warp - kEpiWarp0) >> 2;
     const int r = q * 32 + lane;
+    uint8_t* wslot = stage_buf + (warp - kEpiWarp0) * kWarpSlot;  // this warp's staging slot
     int acc = 0;
     uint32_t acc_phase = 0;
     GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
+    float sc_nxt = 0.f;  // kEpiScale: this thread's row score, loaded a tile ahead
+    if (MODE == kEpiScale && blockIdx.x < static_cast<unsigned>(ntiles) && r < nxt.m_valid)
+      sc_nxt = args.row_scale[nxt.out_row + r];
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
-      if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
+      const float sc_cur = sc_nxt;
+      if (t + static_cast<int>(gridDim.x) < ntiles) {
+        nxt = args.tiles[t + gridDim.x];
+        if (MODE == kEpiScale && r < nxt.m_valid) sc_nxt = args.row_scale[nxt.out_row + r];
+      }
+      (void)sc_cur;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (args.flags & 8) {  // diagnostics only (wrong results): no epilogue, MMA-only timing
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
       const uint32_t taddr = tmem_base + acc * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
       const bool valid = r < tl.m_valid;
       const long long orow = static_cast<long long>(tl.out_row + r);
+      // this warp's rows [32q, 32q + 32) of the tile: all inside the segment ->
+      // one TMA store per 64-column box; cut by the segment end -> masked copy
+      const bool rows_full = 32 * q + 32 <= tl.m_valid;
       if constexpr (MODE == kEpiSwiGLU) {
-        // h = swish(g) * u -> bf16 -> staged in smem -> coalesced row stores
+        // h = swish(g) * u over columns [64 half, 64 half + 64) of the nc-wide output
         const int nc = tl.n_mma >> 1;
         const bool live = r < (tl.m_live & 0xFFFFF);
-        for (int c = 32 * half; c < nc; c += 64) {
-          uint32_t g[32], u[32];
-          tmem_ld32(taddr + c, g);
-          tmem_ld32(taddr + nc + c, u);
-          tmem_ld_wait();
-          uint32_t pk[16];
+        const int c0 = 64 * half;  // output columns of this warp: groups 2 half, 2 half + 1
+        if (c0 < nc) {
+          warp_slot_acquire(lane);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float h0 = 0.f, h1 = 0.f;
-            if (live) {
-              h0 = silu_fast(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
-              h1 = silu_fast(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+          for (int gi = 0; gi < 2; ++gi) {
+            uint32_t v[64];  // [g of 32 neurons | u of the same 32]
+            tmem_ld64(taddr + 2 * c0 + 64 * gi, v);
+            tmem_ld_wait();
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float h0 = 0.f, h1 = 0.f;
+              if (live) {
+                h0 = silu_fast(__uint_as_float(v[2 * i])) * __uint_as_float(v[32 + 2 * i]);
+                h1 = silu_fast(__uint_as_float(v[2 * i + 1])) * __uint_as_float(v[32 + 2 * i + 1]);
+              }
+              pk[i] = pack_bf16x2(h0, h1);
             }
-            pk[i] = pack_bf16x2(h0, h1);
+            warp_put(wslot, lane, 32 * gi, pk);
           }
-          stage_put(stage_buf, r, c, pk);
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);  // accumulator drained: MMA may reuse it
-        epi_sync();
-        copy_out(stage_buf, static_cast<__nv_bfloat16*>(args.out) + static_cast<long long>(tl.out_row) * args.ldo +
-                                tl.out_col, args.ldo, nc, tl.m_valid, threadIdx.x - kEpiWarp0 * 32);
-        epi_sync();
+        if (c0 < nc)
+          warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c0, tl.m_valid - 32 * q, rows_full, lane);
       } else if constexpr (MODE == kEpiScale) {
-        // y = acc * raw score -> bf16.  All of this thread's columns are read
-        // from TMEM first (4 x 32, packed to bf16 in registers) so the
-        // accumulator is released to the MMA before any global traffic; then
-        // staged 128 columns at a time for coalesced row stores.
-        const float sc = valid ? args.row_scale[orow] : 0.f;
-        uint32_t pk[4][16];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int c = 32 * half + 64 * j;
-          if (c < tl.n_mma) {
-            uint32_t v[32];
-            tmem_ld32(taddr + c, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              pk[j][i] = pack_bf16x2(__uint_as_float(v[2 * i]) * sc, __uint_as_float(v[2 * i + 1]) * sc);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        // y = acc * raw score -> bf16; pass p = columns [128p + 64 half, +64),
+        // one x64 TMEM load each.  The row's score was loaded a tile ahead.
+        const float sc = valid ? sc_cur : 0.f;
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-          const int p0 = 128 * p;
-          if (p0 >= tl.n_mma) break;
-          const int w = min(128, tl.n_mma - p0);
+          const int c = 128 * p + 64 * half;
+          const bool have = c < tl.n_mma;
+          uint32_t pk[32];
+          if (have) {
+            uint32_t v[64];
+            tmem_ld64(taddr + c, v);
+            tmem_ld_wait();
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj) {
-            const int c = 32 * half + 64 * jj;  // column inside this 128-wide pass
-            if (c < w) stage_put(stage_buf, r, c, pk[2 * p + jj]);
+            for (int i = 0; i < 32; ++i)
+              pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]) * sc, __uint_as_float(v[2 * i + 1]) * sc);
           }
-          epi_sync();
-          copy_out(stage_buf, static_cast<__nv_bfloat16*>(args.out) + static_cast<long long>(tl.out_row) * args.ldo +
-                                  tl.out_col + p0, args.ldo, w, tl.m_valid, threadIdx.x - kEpiWarp0 * 32);
-          epi_sync();
+          if (p == 1) {
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+          if (have) {
+            warp_slot_acquire(lane);
+            warp_put(wslot, lane, 0, pk);
+            warp_put(wslot, lane, 32, pk + 16);
+            warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c, tl.m_valid - 32 * q, rows_full, lane);
+          }
         }
       } else {
         float* O = static_cast<float*>(args.out) + orow * args.ldo + tl.out_col;
@@ -356,9 +400,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
       }
+      (void)valid; (void)orow;
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
+  if (warp >= kEpiWarp0 && lane == 0) bulk_wait0();  // this lane's TMA stores still read its staging slot
   tc_fence_before();
   __syncthreads();
   if (warp == kMmaWarp) tmem_dealloc(tmem_base, 2 * kAccCols);
@@ -369,13 +415,14 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
                    int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token,
-                   const void* gather_src, long long gather_ld) {
+                   const void* gather_src, long long gather_ld, const CUtensorMap* mapO) {
   static const int flags = [] {
     const char* v = std::getenv("DSMOE_B200_GEMM_FLAGS");
     return v ? std::atoi(v) : 0;
   }();
   GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128), row_token,
-             gather_src, gather_ld, flags};
+             gather_src, gather_ld, flags, mapO != nullptr && mode != kEpiF32 && !(flags & 2) ? 1 : 0};
+  const CUtensorMap* mo = mapO ? mapO : mapB;
   const int grid = max_tiles < num_sms ? (max_tiles > 0 ? max_tiles : 1) : num_sms;
   cudaError_t err;
   switch (mode) {
@@ -387,7 +434,7 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                            kGemmSmem);                                                        \
       attr = true;                                                                            \
     }                                                                                         \
-    gemm_tc_kernel<M><<<grid, kGemmThreads, kGemmSmem, stream>>>(*mapA, *mapA2, *mapB, a);    \
+    gemm_tc_kernel<M><<<grid, kGemmThreads, kGemmSmem, stream>>>(*mapA, *mapA2, *mapB, *mo, a);    \
     break;                                                                                    \
   }
     DSB_LAUNCH(kEpiF32)

@@ -226,10 +226,11 @@ __global__ void __launch_bounds__(k2Threads, 1)
       if constexpr (MODE == k2SwiGLU) {
         const int nc = tl.n_mma >> 1;
         const int live = max(0, min(128, (tl.m_live & 0xFFFFF) - row0));
-        for (int c = 32 * half; c < nc; c += 64) {
+        for (int grp = half; grp < nc / kGroup; grp += 2) {  // [g | u] groups (w13_row_of)
+          const int c = kGroup * grp;
           uint32_t g[32], u[32];
-          tmem_ld32(taddr + c, g);
-          tmem_ld32(taddr + nc + c, u);
+          tmem_ld32(taddr + 2 * c, g);
+          tmem_ld32(taddr + 2 * c + kGroup, u);
           tmem_ld_wait();
           uint32_t pk[16];
 #pragma unroll

@@ -77,7 +77,8 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
                    int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token = nullptr,
-                   const void* gather_src = nullptr, long long gather_ld = 0);
+                   const void* gather_src = nullptr, long long gather_ld = 0,
+                   const CUtensorMap* mapO = nullptr);
 
 // gemm_tc2.cu (CTA pairs, M = 256 tiles; B maps with 128-row boxes)
 int launch_gemm_tc2(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2, const CUtensorMap* mapB,

@@ -23,9 +23,8 @@ __device__ __forceinline__ T from_f(float v) { return static_cast<T>(v); }
 
 // dst row of neuron n inside a sub-block packed at `base` with padded width wpad
 __device__ __forceinline__ long long w13_row(long long base, int wpad, int n, int which) {
-  const int c = n / kChunk, i = n - c * kChunk;
-  const int nc = min(kChunk, wpad - c * kChunk);
-  return base + 2LL * kChunk * c + (which ? nc : 0) + i;
+  (void)wpad;
+  return w13_row_of(base, n, which);
 }
 
 // W13 pack.  src w1/w3: d x ld row-major; neurons are columns order[col0 + n]

@@ -35,9 +35,8 @@ __device__ __forceinline__ long long imp_w13_row(const ImpUnit& u, int n, int wh
   const int i = second ? n - u.h0 : n;
   const int wpad = second ? u.wpad1 : u.wpad0;
   const long long base = second ? u.base1 : u.base0;
-  const int c = i / kChunk, ii = i - c * kChunk;
-  const int nc = min(kChunk, wpad - c * kChunk);
-  return base + 2LL * kChunk * c + (which ? nc : 0) + ii;
+  (void)wpad;
+  return w13_row_of(base, i, which);
 }
 
 template <typename T>
