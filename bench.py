@@ -152,16 +152,19 @@ def build_layer(cfg, ctx, calib_tokens=512, seed=0):
     return rec, host
 
 
-def calibrate(ctx, layer, x, target, tol=0.005):
-    """Threshold bisection to a target drop rate (acceptance.cpp:342-352 method)."""
+def calibrate(ctx, layer, x, target, tol=0.005, kind="2t"):
+    """Threshold bisection to a target drop rate (acceptance.cpp:342-352 method).
+    kind "2t": band (t-0.01, t+0.01), minor halves drop first; "1t": whole
+    selections below t drop (drop_1t, dropping.hpp:133)."""
     import paper_2508_18376_b200 as D
     if target <= 0:
         return D.DropPolicy(), 0.0
+    mk = D.DropPolicy.two_t_from if kind == "2t" else D.DropPolicy.one_t
     lo, hi = 0.0, 1.0
     best = None
     for _ in range(40):
         t = 0.5 * (lo + hi)
-        st = D.route_and_drop(ctx, layer, x, D.DropPolicy.two_t_from(t)).stats
+        st = D.route_and_drop(ctx, layer, x, mk(t)).stats
         if best is None or abs(st["drop_rate"] - target) < abs(best[1] - target):
             best = (t, st["drop_rate"])
         if abs(st["drop_rate"] - target) <= tol:
@@ -170,7 +173,7 @@ def calibrate(ctx, layer, x, target, tol=0.005):
             lo = t
         else:
             hi = t
-    return D.DropPolicy.two_t_from(best[0]), best[1]
+    return mk(best[0]), best[1]
 
 
 # ---------------------------------------------------------------- timing
@@ -469,6 +472,14 @@ def main():
     base_ms = sweep["0.00"]["ms_per_step"]
     for v in sweep.values():
         v["speedup_vs_0"] = base_ms / v["ms_per_step"]
+    # 1T (tensor-level drop of whole selections): rows leave the permutation too
+    sweep_1t = {}
+    for tg in (0.25, 0.5):
+        pol, rate = calibrate(ctx, layer, x, tg, kind="1t")
+        n = max(5, args.steps // 2)
+        ms = time_steps(lambda: D.forward(ctx, layer, x, pol, out=out), n, 3)
+        sweep_1t[f"{tg:.2f}"] = {"drop_rate": rate, "t_drop": pol.t_drop, "ms_per_step": ms / n,
+                                 "tokens_per_s": T / (ms / n * 1e-3), "speedup_vs_0": base_ms / (ms / n)}
 
     # ---- headline timed region (device-resident inputs)
     with ClockSampler(local) as clk:
@@ -510,7 +521,7 @@ def main():
     cpu = None
     if not args.no_cpu:
         try:
-            sample = args.cpu_sample or {"c2": 64, "c3": 4, "c4": 64}[args.config]
+            sample = args.cpu_sample or {"c2": 1024, "c3": 32, "c4": 1024}[args.config]
             rate, dt = cpu_reference_rate(host, sample, ncores)
             cpu = {"value": rate, "unit": "tokens/s", "cores": ncores, "kind": "reference",
                    "sample": f"{sample} tokens of the same layer shape (route_and_drop + moe_forward of "
@@ -554,7 +565,7 @@ def main():
                        "l2": "working set > L2 (weights %.2f GB read per step)" % (
                            (E * 3 * d * ffn + S * 3 * d * ffn) * 2 / 1e9),
                        "parallelism": "single GPU"},
-            "sweep": sweep, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "sweep": sweep, "sweep_1t": sweep_1t, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step,
             "clocks": clk.summary(), "ep_emulated": epx}
     if extra:
