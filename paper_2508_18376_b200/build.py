@@ -49,6 +49,29 @@ def _compile(src, verbose=False):
     return r.stderr
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Same library with extra -D flags into build/variants/lib<name>.so (A/B runs)."""
+    out_dir = os.path.join(os.path.dirname(HERE), "build", "variants", name)
+    os.makedirs(out_dir, exist_ok=True)
+    srcs = sources()
+
+    def comp(src):
+        o = os.path.join(out_dir, src + ".o")
+        cmd = [NVCC, *ARCH, *COMMON, *PER_FILE.get(src, []), *defines, "-c", os.path.join(CSRC, src), "-o", o]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        return o
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
+        objs = list(ex.map(comp, srcs))
+    lib = os.path.join(out_dir, "libdsmoe_b200.so")
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    return lib
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     newest = max(_deps_mtime(), os.path.getmtime(os.path.join(os.path.dirname(HERE), "include", "dsmoe_b200.h")))
@@ -90,4 +113,7 @@ def build_dropin(ref_include="/root/reference/proj/include") -> str | None:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":  # --variant NAME -DX=1 ...
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -106,16 +106,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D bf16 tensor map: `rows` x `cols` (row stride `ld` elements), box
 // 64 columns x box_rows rows, 128-byte swizzle (the UMMA descriptor layout).
-CUtensorMap make_map(const void* base, long long rows, long long cols, long long ld, int box_rows) {
+CUtensorMap make_map(const void* base, long long rows, long long cols, long long ld, int box_rows,
+                     int box_cols = 64) {
   CUtensorMap m;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
-  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                 box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   require(r == CUDA_SUCCESS, DSMOE_E_INTERNAL,
           "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
   return m;
@@ -628,8 +629,8 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
     const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, kTileM);
     const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, kTileM);
     // TMA-store targets: 32-row boxes (one per epilogue warp)
-    const CUtensorMap my = make_map(y, y_rows, L->d, L->d, 32);
-    const CUtensorMap mh32 = make_map(C->H.p, h_rows, L->hstride, L->hstride, 32);
+    const CUtensorMap my = make_map(y, y_rows, L->d, L->d, 32, gemm_tc_store_box_cols());
+    const CUtensorMap mh32 = make_map(C->H.p, h_rows, L->hstride, L->hstride, 32, gemm_tc_store_box_cols());
     C->mark(4);
     launch_check(launch_gemm_tc(1, &mxp, &mx, &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
                                 nullptr, 256, num_sms(), s, row_token, row_token ? x : nullptr, static_cast<long long>(L->d) * 2,

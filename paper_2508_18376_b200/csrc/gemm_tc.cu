@@ -4,20 +4,23 @@
 // (/root/reference/proj/include/dsmoe/moe.hpp:213-231) and the gate matmul of
 // gate_scores (moe.hpp:174 -> matrix.hpp:47-64) for bf16 layers.
 //
-// One CTA per SM (448 threads, warp-specialised):
-//   warp 0      TMA producer: A (128 x 64) and B (N x 64) bf16 tiles, SWIZZLE_128B,
-//               4-stage smem ring guarded by full/empty mbarriers;
-//   warps 1..4  row gatherers (GEMM1 with fused gather only): warp g owns ring
-//               stage g and fills its A tile straight from the token rows of X
+// One CTA per SM (warp-specialised, 32 x (1 + kAStages + 1 + 8) threads):
+//   warp 0      TMA producer: B (N x 64) weight tiles into a kBStages-deep ring,
+//               and A (128 x 64) when the rows are contiguous (explicit X_perm,
+//               H, or x itself for shared experts) into a kAStages-deep ring;
+//               SWIZZLE_128B, full/empty mbarriers per ring;
+//   warps 1..   row gatherers (GEMM1 with fused gather only): warp g owns A
+//               stage g and fills it straight from the token rows of X
 //               (16-byte cp.async, one warp instruction = 4 rows x 128 B, so
 //               every request is a whole L2 line), then proxy-fences and
-//               arrives on the stage's full barrier — no permuted copy of X;
-//   warp 5      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N<=256,
-//               K=16 per instruction), fp32 accumulators in TMEM, two
-//               accumulator stages (2 x 256 columns) so the epilogue of tile i
-//               overlaps the MMAs of tile i+1;
-//   warps 6..13 epilogue (two warps per TMEM lane quarter, alternating 32-column
-//               chunks): tcgen05.ld 32x32b -> registers -> fused op -> global.
+//               arrives — no permuted copy of X in HBM.  The A ring is the
+//               deeper one: gather latency is what the MMA waits on;
+//   MMA warp    TMEM allocator + warp-uniform loop, an elected lane issues
+//               tcgen05.mma (M=128, N<=256, K=16), fp32 accumulators in TMEM,
+//               two accumulator stages (2 x 256 columns) so the epilogue of
+//               tile i overlaps the MMAs of tile i+1;
+//   8 epilogue  two warps per TMEM lane quarter: tcgen05.ld 32x32b.x64 ->
+//   warps       registers -> fused op -> bf16 -> per-warp smem slot -> TMA store.
 // Work items (GemmTile) are produced on the device by plan_tiles (permute.cu)
 // and walked in a static round-robin over the persistent CTAs.
 //
@@ -34,18 +37,36 @@
 
 namespace dsb {
 
-constexpr int kStages = 4;
+// Separate operand rings: A (128 x 64 rows of tokens) is the latency-critical
+// one under the fused gather, so it is deeper than the B (weights) ring.
+#ifndef DSB_A_STAGES
+#define DSB_A_STAGES 5
+#endif
+#ifndef DSB_B_STAGES
+#define DSB_B_STAGES 4
+#endif
+// 1: epilogue warps stage 32 x 64 tiles in smem and leave with TMA stores;
+// 0: each thread stores its row's 64-byte runs straight from registers (the
+//    32 KB of staging go to the operand rings instead)
+#ifndef DSB_STAGE_OUT
+#define DSB_STAGE_OUT 2
+#endif
+constexpr int kAStages = DSB_A_STAGES;
+constexpr int kBStages = DSB_B_STAGES;
 constexpr int kABytes = kTileM * kTileK * 2;       // 16 KB
 constexpr int kBBytesMax = 256 * kTileK * 2;       // 32 KB
-constexpr int kStageBytes = kABytes + kBBytesMax;  // 48 KB
-constexpr int kGatherWarp0 = 1;     // warps 1-4: fused row gather, warp 1 + s owns stage s
-constexpr int kGatherWarps = kStages;
-constexpr int kMmaWarp = 5;         // warp 5: TMEM alloc + tcgen05.mma issue
-constexpr int kEpiWarp0 = 6;        // warps 6-13: epilogue
-constexpr int kGemmThreads = 448;
+constexpr int kGatherWarp0 = 1;                    // warps 1..kAStages: fused row gather, warp 1 + s owns A stage s
+constexpr int kGatherWarps = kAStages;
+constexpr int kMmaWarp = kGatherWarp0 + kGatherWarps;  // TMEM alloc + tcgen05.mma issue
+constexpr int kEpiWarp0 = kMmaWarp + 1;                // 8 epilogue warps
+constexpr int kGemmThreads = (kEpiWarp0 + 8) * 32;
 constexpr int kEpiThreads = 256;
 constexpr int kAccCols = 256;
-constexpr int kGemmSmem = kStages * kStageBytes + 128 * 256 /*output stage*/ + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kRingBytes = kAStages * kABytes + kBStages * kBBytesMax;
+constexpr bool kStageOut = DSB_STAGE_OUT != 0;
+constexpr int kGemmSmem = kRingBytes + (DSB_STAGE_OUT == 1 ? 8 * 32 * 128 : DSB_STAGE_OUT == 2 ? 8 * 32 * 64 : 0) +
+                          1024 /*align*/ + 256 /*barriers*/;
+static_assert(kGemmSmem <= 227 * 1024, "shared memory budget");
 
 enum { kEpiF32 = 0, kEpiSwiGLU = 1, kEpiScale = 2 };
 
@@ -72,21 +93,30 @@ __device__ __forceinline__ float silu_fast(float g) {
   return fmaf(hg, th, hg);
 }
 
-// Output staging, per epilogue warp: a 4 KB slot = its 32 rows x 64 bf16
-// columns as one TMA box (32 rows x 128 B, SWIZZLE_128B: 16-byte chunk k of
-// row rr at rr*128 + ((k ^ (rr & 7)) << 4)).  Every warp stores on its own
-// (lane 0 issues the TMA store and owns the bulk group), so the epilogue has
-// no CTA-wide barriers; rows cut by the segment end are copied out masked.
-constexpr int kWarpSlot = 32 * 128;
-constexpr int kStageOutBytes = 8 * kWarpSlot;
+// Output staging, per epilogue warp (DSB_STAGE_OUT 1): a 4 KB slot = its 32
+// rows x 64 bf16 columns as one TMA box (rows of 128 B, SWIZZLE_128B: 16-byte
+// chunk k of row rr at rr*128 + ((k ^ (rr & 7)) << 4)); DSB_STAGE_OUT 2: a
+// 2 KB slot of 32 rows x 32 columns (rows of 64 B, SWIZZLE_64B: chunk k at
+// rr*64 + ((k ^ ((rr >> 1) & 3)) << 4)), which leaves 16 KB more for the
+// operand rings.  Every warp stores on its own (lane 0 issues the TMA store
+// and owns the bulk group), so the epilogue has no CTA-wide barriers; rows cut
+// by the segment end are copied out masked.
+constexpr int kBoxCols = DSB_STAGE_OUT == 2 ? 32 : 64;
+constexpr int kRowBytes = kBoxCols * 2;
+constexpr int kWarpSlot = 32 * kRowBytes;
+constexpr int kStageOutBytes = kStageOut ? 8 * kWarpSlot : 0;
 
-// columns [col, col + 32) of this lane's row (pk: 16 packed bf16 pairs)
+__device__ __forceinline__ int swz(int rr, int k) {
+  return kBoxCols == 64 ? (k ^ (rr & 7)) : (k ^ ((rr >> 1) & 3));
+}
+
+// columns [col, col + 32) of the slot's box for this lane's row (pk: 16 packed bf16 pairs)
 __device__ __forceinline__ void warp_put(uint8_t* slot, int lane, int col, const uint32_t* pk) {
-  uint8_t* rowp = slot + lane * 128;
+  uint8_t* rowp = slot + lane * kRowBytes;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int k = (col >> 3) + i;
-    *reinterpret_cast<uint4*>(rowp + ((k ^ (lane & 7)) << 4)) =
+    *reinterpret_cast<uint4*>(rowp + (swz(lane, k) << 4)) =
         make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
   }
 }
@@ -97,7 +127,7 @@ __device__ __forceinline__ void warp_slot_acquire(int lane) {
   __syncwarp();
 }
 
-// slot -> out rows [row0, row0 + min(32, nvalid)), columns [col0, col0 + 64)
+// slot -> out rows [row0, row0 + min(32, nvalid)), columns [col0, col0 + kBoxCols)
 __device__ __forceinline__ void warp_store(const uint8_t* slot, const CUtensorMap* mapO, const GemmArgs& args,
                                            int row0, int col0, int nvalid, bool full, int lane) {
   if (full && args.tma_store) {
@@ -110,15 +140,27 @@ __device__ __forceinline__ void warp_store(const uint8_t* slot, const CUtensorMa
   } else {
     __syncwarp();
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(args.out);
-    const int k = lane & 7;
+    constexpr int kChunks = kRowBytes / 16;  // 16-byte chunks per row
+    constexpr int kRowsPerPass = 32 / kChunks;
+    const int k = lane % kChunks;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int rr = 4 * i + (lane >> 3);
+    for (int i = 0; i < kChunks; ++i) {
+      const int rr = kRowsPerPass * i + lane / kChunks;
       if (rr < nvalid)
         *reinterpret_cast<uint4*>(out + static_cast<long long>(row0 + rr) * args.ldo + col0 + 8 * k) =
-            *reinterpret_cast<const uint4*>(slot + rr * 128 + ((k ^ (rr & 7)) << 4));
+            *reinterpret_cast<const uint4*>(slot + rr * kRowBytes + (swz(rr, k) << 4));
     }
   }
+}
+
+// box columns the TMA-store map must use (host side builds the map)
+int gemm_tc_store_box_cols() { return kBoxCols; }
+
+// direct path: columns [col, col + 32) of output row `row` from registers
+__device__ __forceinline__ void row_put(const GemmArgs& args, long long row, int col, const uint32_t* pk) {
+  uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.out) + row * args.ldo + col);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
 }
 
 template <int MODE>
@@ -129,10 +171,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
-  uint8_t* stage_buf = smem + kStages * kStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + kStageOutBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
+  uint8_t* ringA = smem;                              // kAStages x 16 KB
+  uint8_t* ringB = smem + kAStages * kABytes;         // kBStages x 32 KB
+  uint8_t* stage_buf = smem + kRingBytes;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(stage_buf + kStageOutBytes);
+  uint64_t* emptyA = fullA + kAStages;
+  uint64_t* fullB = emptyA + kAStages;
+  uint64_t* emptyB = fullB + kBStages;
+  uint64_t* tfull = emptyB + kBStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -142,9 +188,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const bool fused = MODE == kEpiSwiGLU && args.gather_src != nullptr;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], fused ? 2 : 1);  // TMA expect_tx arrive (+ the stage's gather warp)
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < kAStages; ++s) {
+      mbar_init(&fullA[s], 1);  // one arrive(.expect_tx): the TMA producer, or the stage's gather warp
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < kBStages; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -167,12 +217,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer: B always; A for tiles whose rows are
-      // contiguous (explicit X_perm, or X itself for shared experts)
-      int stage = 0;
-      uint32_t phase = 0;
-      // fused gather: weights stream through L2 evict-first so the token rows
-      // of X (gathered evict-last, ~48 reads each) stay resident
+      // ---------------- TMA producer: B always; A too unless the gather warps own it
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
       uint64_t pol_b;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_b));
       GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
@@ -180,30 +227,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
         if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
         const bool alt = (tl.m_live & kTileAltA) != 0;
-        const bool gather = fused && (tl.m_live & kTileGatherA) != 0;
         const void* ma = alt ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
         for (int kb = 0; kb < tl.nkb; ++kb) {
-          uint8_t* sa = smem + stage * kStageBytes;
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], (gather ? 0u : static_cast<uint32_t>(kABytes)) + args.b_bytes);
-          if (!gather) tma_load_2d(sa, ma, &full[stage], kb * kTileK, tl.a_row);
+          if (!fused) {
+            mbar_wait(&emptyA[sa], pa ^ 1);
+            mbar_expect_tx(&fullA[sa], kABytes);
+            tma_load_2d(ringA + sa * kABytes, ma, &fullA[sa], kb * kTileK, tl.a_row);
+            if (++sa == kAStages) { sa = 0; pa ^= 1; }
+          }
+          mbar_wait(&emptyB[sb], pb ^ 1);
+          mbar_expect_tx(&fullB[sb], args.b_bytes);
           if (fused && (args.flags & 1))
-            tma_load_2d_hint(sa + kABytes, &mapB, &full[stage], kb * kTileK, tl.b_row, pol_b);
+            tma_load_2d_hint(ringB + sb * kBBytesMax, &mapB, &fullB[sb], kb * kTileK, tl.b_row, pol_b);
           else
-            tma_load_2d(sa + kABytes, &mapB, &full[stage], kb * kTileK, tl.b_row);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+            tma_load_2d(ringB + sb * kBBytesMax, &mapB, &fullB[sb], kb * kTileK, tl.b_row);
+          if (++sb == kBStages) { sb = 0; pb ^= 1; }
         }
       }
     }
   } else if (warp < kGatherWarp0 + kGatherWarps) {
     if (fused) {
-      // ---------------- row gatherers.  Warp g fills ring stage g, i.e. the
-      // k-blocks whose running index (over this CTA's tiles) is g mod 4.
+      // ---------------- row gatherers.  Warp g fills A stage g, i.e. the
+      // k-blocks whose running index (over this CTA's tiles) is g mod kAStages.
       // Lane l copies 16-byte chunk (l & 7) of row 4i + (l >> 3) in
-      // instruction i; the chunk lands at its SWIZZLE_128B position.
+      // instruction i; the chunk lands at its SWIZZLE_128B position.  Tiles
+      // whose rows are contiguous in X (shared experts) are one TMA load.
       const int gw = warp - kGatherWarp0;
       const int rr = lane >> 3, ch = lane & 7;
-      const uint32_t sa = smem_u32(smem + gw * kStageBytes);
+      uint8_t* sa_ptr = ringA + gw * kABytes;
+      const uint32_t sa = smem_u32(sa_ptr);
       const char* X = static_cast<const char*>(args.gather_src);
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -228,9 +280,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const GemmTile nxt2 = t + 2 * gs < ntiles ? args.tiles[t + 2 * gs] : GemmTile{};
         const GemmTile& tl = cur;
         const bool gather = (tl.m_live & kTileGatherA) != 0;
-        const int first = (gw - g) & (kStages - 1);  // first k-block of this tile owned by this warp
-        for (int kb = first; kb < tl.nkb; kb += kStages) {
-          mbar_wait(&empty[gw], phase ^ 1);
+        const void* ma = (tl.m_live & kTileAltA) ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
+        int first = (gw - g) % kAStages;  // first k-block of this tile owned by this warp
+        if (first < 0) first += kAStages;
+        for (int kb = first; kb < tl.nkb; kb += kAStages) {
+          mbar_wait(&emptyA[gw], phase ^ 1);
           if (gather) {
             const char* src = X + kb * 128 + ch * 16;
 #pragma unroll
@@ -243,10 +297,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                            : "memory");
             }
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tcgen05 reads
+            fence_proxy_async();  // generic writes -> tcgen05 reads
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&fullA[gw]);
+          } else if (lane == 0) {
+            mbar_expect_tx(&fullA[gw], kABytes);
+            tma_load_2d(sa_ptr, ma, &fullA[gw], kb * kTileK, tl.a_row);
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive(&full[gw]);
           phase ^= 1;
         }
         g += tl.nkb;
@@ -260,11 +318,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ---------------- MMA issuer: the whole warp walks the loop (warp-uniform
     // control, so descriptors live in uniform registers); one elected lane
     // issues the tcgen05.mma / commit instructions.
-    int stage = 0;
-    uint32_t phase = 0;
+    int sa = 0, sb = 0;
+    uint32_t pa = 0, pb = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    const uint64_t d0 = sdesc_sw128(smem_u32(smem));  // stage 0 A; + (bytes >> 4) moves the start address
+    const uint64_t da0 = sdesc_sw128(smem_u32(ringA));  // + (bytes >> 4) moves the start address
+    const uint64_t db0 = sdesc_sw128(smem_u32(ringB));
     GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
@@ -274,18 +333,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < tl.nkb; ++kb) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait(&fullA[sa], pa);
+        mbar_wait(&fullB[sb], pb);
         tc_fence_after();
-        const uint64_t adesc = d0 + static_cast<uint64_t>(stage * (kStageBytes >> 4));
-        const uint64_t bdesc = adesc + (kABytes >> 4);
+        const uint64_t adesc = da0 + static_cast<uint64_t>(sa * (kABytes >> 4));
+        const uint64_t bdesc = db0 + static_cast<uint64_t>(sb * (kBBytesMax >> 4));
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kTileK / 16; ++k)  // 16 bf16 = 32 B along K inside the 128 B swizzle row
             umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-          umma_commit(&empty[stage]);
+          umma_commit(&emptyA[sa]);
+          umma_commit(&emptyB[sb]);
         }
         __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (++sa == kAStages) { sa = 0; pa ^= 1; }
+        if (++sb == kBStages) { sb = 0; pb ^= 1; }
       }
       if (elect_one()) umma_commit(&tfull[acc]);
       __syncwarp();
@@ -332,9 +394,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const bool live = r < (tl.m_live & 0xFFFFF);
         const int c0 = 64 * half;  // output columns of this warp: groups 2 half, 2 half + 1
         if (c0 < nc) {
-          warp_slot_acquire(lane);
+          if (kStageOut && kBoxCols == 64) warp_slot_acquire(lane);
 #pragma unroll
           for (int gi = 0; gi < 2; ++gi) {
+            if (kStageOut && kBoxCols == 32) warp_slot_acquire(lane);
             uint32_t v[64];  // [g of 32 neurons | u of the same 32]
             tmem_ld64(taddr + 2 * c0 + 64 * gi, v);
             tmem_ld_wait();
@@ -348,12 +411,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               }
               pk[i] = pack_bf16x2(h0, h1);
             }
-            warp_put(wslot, lane, 32 * gi, pk);
+            if (kStageOut && kBoxCols == 32) {
+              warp_put(wslot, lane, 0, pk);
+              warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c0 + 32 * gi, tl.m_valid - 32 * q,
+                         rows_full, lane);
+            } else if (kStageOut)
+              warp_put(wslot, lane, 32 * gi, pk);
+            else if (valid)
+              row_put(args, orow, tl.out_col + c0 + 32 * gi, pk);
           }
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);  // accumulator drained: MMA may reuse it
-        if (c0 < nc)
+        if (kStageOut && kBoxCols == 64 && c0 < nc)
           warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c0, tl.m_valid - 32 * q, rows_full, lane);
       } else if constexpr (MODE == kEpiScale) {
         // y = acc * raw score -> bf16; pass p = columns [128p + 64 half, +64),
@@ -376,11 +446,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
           }
-          if (have) {
+          if (have && kStageOut && kBoxCols == 64) {
             warp_slot_acquire(lane);
             warp_put(wslot, lane, 0, pk);
             warp_put(wslot, lane, 32, pk + 16);
             warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c, tl.m_valid - 32 * q, rows_full, lane);
+          } else if (have && kStageOut) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              warp_slot_acquire(lane);
+              warp_put(wslot, lane, 0, pk + 16 * hh);
+              warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c + 32 * hh, tl.m_valid - 32 * q,
+                         rows_full, lane);
+            }
+          } else if (have && valid) {
+            row_put(args, orow, tl.out_col + c, pk);
+            row_put(args, orow, tl.out_col + c + 32, pk + 16);
           }
         }
       } else {

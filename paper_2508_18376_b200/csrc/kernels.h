@@ -80,6 +80,8 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const void* gather_src = nullptr, long long gather_ld = 0,
                    const CUtensorMap* mapO = nullptr);
 
+int gemm_tc_store_box_cols();  // TMA-store box width the gemm_tc build expects (64: SW128, 32: SW64)
+
 // gemm_tc2.cu (CTA pairs, M = 256 tiles; B maps with 128-row boxes)
 int launch_gemm_tc2(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2, const CUtensorMap* mapB,
                     const GemmTile* tiles,

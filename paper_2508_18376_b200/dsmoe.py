@@ -127,10 +127,13 @@ def lib():
     there is no fallback path."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+        # DSMOE_B200_LIB: an alternative in-tree build of the same library
+        # (tools/build_variant.sh compiles GEMM pipeline-depth variants for A/B)
+        path = os.environ.get("DSMOE_B200_LIB") or LIB_PATH
+        if not os.path.exists(path):
+            raise ImportError(f"{path} missing: run __graft_entry__.build() "
                               "(python -m paper_2508_18376_b200.build)")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         for name, (res, args) in SYMBOLS.items():
             fn = getattr(L, name)
             fn.restype = res
