@@ -150,12 +150,13 @@ void dsmoe_b200_ctx_free(dsmoe_b200_ctx* ctx);
 int dsmoe_b200_ctx_check(dsmoe_b200_ctx* ctx);
 
 /* Per-stage device timing for dsmoe_b200_forward (CUDA events on the
- * context's stream; each profiled call synchronises).  Stages: 0 gate logits,
+ * context's stream, recorded without synchronising — a ring of event sets is
+ * resolved when the profile is read, so it can run inside a timed loop).  Stages: 0 gate logits,
  * 1 router, 2 permute + tile plan, 3 gather, 4 grouped GEMM1 ([W1|W3] +
  * SwiGLU), 5 grouped GEMM2 (W2 + score), 6 combine.  ms receives the summed
  * milliseconds per stage since profiling was (re)enabled. */
 int dsmoe_b200_ctx_set_profiling(dsmoe_b200_ctx* ctx, int on);
-int dsmoe_b200_ctx_profile(const dsmoe_b200_ctx* ctx, double* ms, int n, long* calls);
+int dsmoe_b200_ctx_profile(dsmoe_b200_ctx* ctx, double* ms, int n, long* calls);
 
 /* The token permutation of the last forward on this context (host copies,
  * any pointer may be NULL): row_token[r] = token of permuted row r (r <

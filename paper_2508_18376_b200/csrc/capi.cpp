@@ -323,41 +323,65 @@ struct dsmoe_b200_ctx {
   long long scale_fill_key = -1;
   unsigned long long last_err_flags = 0;
   // optional per-stage CUDA-event timing (bench.py): 0 gate, 1 router,
-  // 2 permute+plan, 3 gather, 4 gemm1, 5 gemm2, 6 combine
+  // 2 permute+plan, 3 gather, 4 gemm1, 5 gemm2, 6 combine.  Non-blocking: each
+  // forward records into its own event set from a ring; the sets are resolved
+  // (synchronised and summed) only when the profile is read or the ring is
+  // full, so timing can run inside a back-to-back timed loop.
   static constexpr int kStages = 7;
+  static constexpr int kRing = 256;
+  struct EvSet {
+    cudaEvent_t ev[kStages + 1] = {};
+    bool hit[kStages + 1] = {};
+  };
   bool profiling = false;
-  cudaEvent_t ev[kStages + 1] = {};
-  bool ev_hit[kStages + 1] = {};
+  std::vector<EvSet> ring;
+  int ring_head = 0, ring_pending = 0;
+  EvSet* cur = nullptr;
   double prof_ms[kStages] = {};
   long prof_calls = 0;
   void mark(int i) {
-    if (!profiling) return;
-    cuda_check(cudaEventRecord(ev[i], stream), "event");
-    ev_hit[i] = true;
+    if (!profiling || !cur) return;
+    cuda_check(cudaEventRecord(cur->ev[i], stream), "event");
+    cur->hit[i] = true;
   }
   void prof_begin() {
     if (!profiling) return;
-    for (auto& h : ev_hit) h = false;
+    if (ring.empty()) {
+      ring.resize(kRing);
+      for (auto& es : ring)
+        for (auto& e : es.ev) cuda_check(cudaEventCreate(&e), "event create");
+    }
+    if (ring_pending == kRing) resolve();
+    cur = &ring[(ring_head + ring_pending) % kRing];
+    for (auto& h : cur->hit) h = false;
   }
   void prof_end() {
-    if (!profiling) return;
+    if (!profiling || !cur) return;
     mark(kStages);
-    cuda_check(cudaEventSynchronize(ev[kStages]), "event sync");
-    int prev = -1;
-    for (int i = 0; i <= kStages; ++i) {
-      if (!ev_hit[i]) continue;
-      if (prev >= 0) {
-        float ms = 0.f;
-        cuda_check(cudaEventElapsedTime(&ms, ev[prev], ev[i]), "elapsed");
-        prof_ms[prev] += ms;
+    cur = nullptr;
+    ++ring_pending;
+  }
+  void resolve() {
+    for (; ring_pending > 0; --ring_pending, ring_head = (ring_head + 1) % kRing) {
+      EvSet& es = ring[ring_head];
+      cuda_check(cudaEventSynchronize(es.ev[kStages]), "event sync");
+      int prev = -1;
+      for (int i = 0; i <= kStages; ++i) {
+        if (!es.hit[i]) continue;
+        if (prev >= 0) {
+          float ms = 0.f;
+          cuda_check(cudaEventElapsedTime(&ms, es.ev[prev], es.ev[i]), "elapsed");
+          prof_ms[prev] += ms;
+        }
+        prev = i;
       }
-      prev = i;
+      ++prof_calls;
     }
-    ++prof_calls;
   }
   ~dsmoe_b200_ctx() {
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
+    for (auto& es : ring)
+      for (auto& e : es.ev)
+        if (e) cudaEventDestroy(e);
   }
 
   // workspace for T tokens on layer L
@@ -825,17 +849,17 @@ int dsmoe_b200_ctx_check(dsmoe_b200_ctx* C) {
 int dsmoe_b200_ctx_set_profiling(dsmoe_b200_ctx* C, int on) {
   return guarded([&] {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
-    if (on && !C->ev[0])
-      for (auto& e : C->ev) cuda_check(cudaEventCreate(&e), "event create");
+    C->resolve();
     C->profiling = on != 0;
     for (double& v : C->prof_ms) v = 0.0;
     C->prof_calls = 0;
   });
 }
 
-int dsmoe_b200_ctx_profile(const dsmoe_b200_ctx* C, double* ms, int n, long* calls) {
+int dsmoe_b200_ctx_profile(dsmoe_b200_ctx* C, double* ms, int n, long* calls) {
   return guarded([&] {
     require(C && ms, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    C->resolve();
     for (int i = 0; i < n && i < dsmoe_b200_ctx::kStages; ++i) ms[i] = C->prof_ms[i];
     if (calls) *calls = C->prof_calls;
   });
