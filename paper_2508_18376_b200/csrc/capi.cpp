@@ -617,6 +617,23 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
   pa.gather = gather ? 1 : 0;
   pa.tile_m = tile_m;
   const int nchunks = (T + kRouterChunk - 1) / kRouterChunk;
+  // one cooperative launch by default; DSMOE_B200_PERMUTE=split runs the
+  // three-kernel path (scan_codes, seg_plan, scatter) — identical results
+  static const bool split = [] {
+    const char* v = std::getenv("DSMOE_B200_PERMUTE");
+    return v && std::string(v) == "split";
+  }();
+  if (!split) {
+    launch_check(launch_permute_fused(C->cnt_chunk.as<int>(), nchunks, L->E, C->chunk_off.as<int>(),
+                                      C->code_base.as<int>(), C->seg.as<UnitSeg>(), r_total,
+                                      C->code_base.as<int>() + 2 * L->E, C->sel_code.as<int32_t>(),
+                                      C->sel_raw.as<float>(), T, L->K, C->row_token.as<int32_t>(),
+                                      C->row_scale.as<float>(), C->slot_pos.as<int32_t>(), plan ? &pa : nullptr,
+                                      num_sms(), s),
+                 "permute");
+    g_launches += 1;
+    return;
+  }
   launch_check(launch_scan_plan(C->cnt_chunk.as<int>(), nchunks, L->E, C->chunk_off.as<int>(), C->code_base.as<int>(),
                                 C->seg.as<UnitSeg>(), r_total, C->code_base.as<int>() + 2 * L->E, plan ? &pa : nullptr, num_sms(), s),
                "scan/plan");

@@ -51,24 +51,36 @@ namespace dsb {
 #ifndef DSB_STAGE_OUT
 #define DSB_STAGE_OUT 2
 #endif
-constexpr int kAStages = DSB_A_STAGES;
-constexpr int kBStages = DSB_B_STAGES;
 constexpr int kABytes = kTileM * kTileK * 2;       // 16 KB
 constexpr int kBBytesMax = 256 * kTileK * 2;       // 32 KB
-constexpr int kGatherWarp0 = 1;                    // warps 1..kAStages: fused row gather, warp 1 + s owns A stage s
-constexpr int kGatherWarps = kAStages;
-constexpr int kMmaWarp = kGatherWarp0 + kGatherWarps;  // TMEM alloc + tcgen05.mma issue
-constexpr int kEpiWarp0 = kMmaWarp + 1;                // 8 epilogue warps
-constexpr int kGemmThreads = (kEpiWarp0 + 8) * 32;
 constexpr int kEpiThreads = 256;
 constexpr int kAccCols = 256;
-constexpr int kRingBytes = kAStages * kABytes + kBStages * kBBytesMax;
 constexpr bool kStageOut = DSB_STAGE_OUT != 0;
-constexpr int kGemmSmem = kRingBytes + (DSB_STAGE_OUT == 1 ? 8 * 32 * 128 : DSB_STAGE_OUT == 2 ? 8 * 32 * 64 : 0) +
-                          1024 /*align*/ + 256 /*barriers*/;
-static_assert(kGemmSmem <= 227 * 1024, "shared memory budget");
+constexpr int kStageSmem = DSB_STAGE_OUT == 1 ? 8 * 32 * 128 : DSB_STAGE_OUT == 2 ? 8 * 32 * 64 : 0;
 
-enum { kEpiF32 = 0, kEpiSwiGLU = 1, kEpiScale = 2 };
+enum { kEpiF32 = 0, kEpiSwiGLU = 1, kEpiScale = 2, kEpiF32Wide = 3 };
+
+// Per-mode pipeline geometry.  GEMM1/GEMM2: A (tokens) ring DSB_A_STAGES deep,
+// B (weights, N <= 256 rows) ring DSB_B_STAGES deep; gather warps only where
+// the fused gather runs (GEMM1).  Gate logits (N = Epad <= 64): 8 KB B slots,
+// so both rings can be 8 deep — the gate GEMM is a 64 MB stream of x with
+// little math, and in-flight bytes are what bound it.
+template <int MODE>
+struct Geo {
+  static constexpr bool kGate = MODE == kEpiF32;
+  static constexpr int NA = kGate ? 8 : DSB_A_STAGES;
+  static constexpr int NB = kGate ? 8 : DSB_B_STAGES;
+  static constexpr int BSLOT = kGate ? 64 * kTileK * 2 : kBBytesMax;
+  static constexpr int NGW = MODE == kEpiSwiGLU ? NA : 0;  // gather warps, warp 1 + s owns A stage s
+  static constexpr int GW0 = 1;
+  static constexpr int MMA = GW0 + NGW;  // TMEM alloc + tcgen05.mma issue
+  static constexpr int EPI0 = MMA + 1;   // 8 epilogue warps
+  static constexpr int THREADS = (EPI0 + 8) * 32;
+  static constexpr int RING = NA * kABytes + NB * BSLOT;
+  static constexpr int STAGE = (MODE == kEpiF32 || MODE == kEpiF32Wide) ? 0 : kStageSmem;
+  static constexpr int SMEM = RING + STAGE + 1024 /*align*/ + 512 /*barriers*/;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
 
 struct GemmArgs {
   const GemmTile* tiles;
@@ -104,7 +116,6 @@ __device__ __forceinline__ float silu_fast(float g) {
 constexpr int kBoxCols = DSB_STAGE_OUT == 2 ? 32 : 64;
 constexpr int kRowBytes = kBoxCols * 2;
 constexpr int kWarpSlot = 32 * kRowBytes;
-constexpr int kStageOutBytes = kStageOut ? 8 * kWarpSlot : 0;
 
 __device__ __forceinline__ int swz(int rr, int k) {
   return kBoxCols == 64 ? (k ^ (rr & 7)) : (k ^ ((rr >> 1) & 3));
@@ -164,15 +175,20 @@ __device__ __forceinline__ void row_put(const GemmArgs& args, long long row, int
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapO,
                    const GemmArgs args) {
+  using G = Geo<MODE>;
+  constexpr int kAStages = G::NA, kBStages = G::NB, kBSlot = G::BSLOT;
+  constexpr int kGatherWarp0 = G::GW0, kGatherWarps = G::NGW, kMmaWarp = G::MMA, kEpiWarp0 = G::EPI0;
+  constexpr int kRingBytes = G::RING;
+  constexpr int kStageOutBytes = G::STAGE;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* ringA = smem;                              // kAStages x 16 KB
-  uint8_t* ringB = smem + kAStages * kABytes;         // kBStages x 32 KB
+  uint8_t* ringB = smem + kAStages * kABytes;         // kBStages x kBSlot
   uint8_t* stage_buf = smem + kRingBytes;
   uint64_t* fullA = reinterpret_cast<uint64_t*>(stage_buf + kStageOutBytes);
   uint64_t* emptyA = fullA + kAStages;
@@ -186,7 +202,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int lane = threadIdx.x & 31;
   const int ntiles = *args.num_tiles;
 
-  const bool fused = MODE == kEpiSwiGLU && args.gather_src != nullptr;
+  const bool fused = MODE == kEpiSwiGLU && kGatherWarps > 0 && args.gather_src != nullptr;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kAStages; ++s) {
       mbar_init(&fullA[s], 1);  // one arrive(.expect_tx): the TMA producer, or the stage's gather warp
@@ -238,9 +254,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&emptyB[sb], pb ^ 1);
           mbar_expect_tx(&fullB[sb], args.b_bytes);
           if (fused && (args.flags & 1))
-            tma_load_2d_hint(ringB + sb * kBBytesMax, &mapB, &fullB[sb], kb * kTileK, tl.b_row, pol_b);
+            tma_load_2d_hint(ringB + sb * kBSlot, &mapB, &fullB[sb], kb * kTileK, tl.b_row, pol_b);
           else
-            tma_load_2d(ringB + sb * kBBytesMax, &mapB, &fullB[sb], kb * kTileK, tl.b_row);
+            tma_load_2d(ringB + sb * kBSlot, &mapB, &fullB[sb], kb * kTileK, tl.b_row);
           if (++sb == kBStages) { sb = 0; pb ^= 1; }
         }
       }
@@ -337,7 +353,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&fullB[sb], pb);
         tc_fence_after();
         const uint64_t adesc = da0 + static_cast<uint64_t>(sa * (kABytes >> 4));
-        const uint64_t bdesc = db0 + static_cast<uint64_t>(sb * (kBBytesMax >> 4));
+        const uint64_t bdesc = db0 + static_cast<uint64_t>(sb * (kBSlot >> 4));
         if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kTileK / 16; ++k)  // 16 bf16 = 32 B along K inside the 128 B swizzle row
@@ -477,7 +493,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
-      if constexpr (MODE == kEpiF32) {
+      if constexpr (MODE == kEpiF32 || MODE == kEpiF32Wide) {
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
       }
@@ -502,7 +518,9 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
     return v ? std::atoi(v) : 0;
   }();
   GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128), row_token,
-             gather_src, gather_ld, flags, mapO != nullptr && mode != kEpiF32 && !(flags & 2) ? 1 : 0};
+             gather_src, gather_ld, flags, mapO != nullptr && mode != kEpiF32 && mode != kEpiF32Wide && !(flags & 2) ? 1 : 0};
+  // gate logits with more than 64 output columns need the wide B slots
+  if (mode == kEpiF32 && b_box_rows > 64) mode = kEpiF32Wide;
   const CUtensorMap* mo = mapO ? mapO : mapB;
   const int grid = max_tiles < num_sms ? (max_tiles > 0 ? max_tiles : 1) : num_sms;
   cudaError_t err;
@@ -512,13 +530,14 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
     static bool attr = false;                                                                 \
     if (!attr) {                                                                              \
       cudaFuncSetAttribute(gemm_tc_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                           kGemmSmem);                                                        \
+                           Geo<M>::SMEM);                                                     \
       attr = true;                                                                            \
     }                                                                                         \
-    gemm_tc_kernel<M><<<grid, kGemmThreads, kGemmSmem, stream>>>(*mapA, *mapA2, *mapB, *mo, a);    \
+    gemm_tc_kernel<M><<<grid, Geo<M>::THREADS, Geo<M>::SMEM, stream>>>(*mapA, *mapA2, *mapB, *mo, a); \
     break;                                                                                    \
   }
     DSB_LAUNCH(kEpiF32)
+    DSB_LAUNCH(kEpiF32Wide)
     DSB_LAUNCH(kEpiSwiGLU)
     DSB_LAUNCH(kEpiScale)
 #undef DSB_LAUNCH

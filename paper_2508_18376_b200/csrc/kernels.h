@@ -62,6 +62,11 @@ struct PlanArgs {
 int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
                      int* r_total, int* code_tot, const PlanArgs* plan, int num_sms, cudaStream_t stream);
 int launch_plan(const PlanArgs& a, int num_sms, cudaStream_t stream);
+// scan + segments + ordered scatter (+ work lists) in one cooperative launch
+int launch_permute_fused(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
+                         int* r_total, int* code_tot, const int32_t* sel_code, const float* sel_raw, int T, int K,
+                         int32_t* row_token, float* row_scale, int32_t* slot_pos, const PlanArgs* plan, int num_sms,
+                         cudaStream_t stream);
 int launch_scatter(const int32_t* sel_code, const float* sel_raw, int T, int K, int E, const int* chunk_off,
                    const int* code_base, int32_t* row_token, float* row_scale, int32_t* slot_pos, cudaStream_t stream);
 int launch_gather(const void* x, void* xp, const int32_t* row_token, const int* r_total,

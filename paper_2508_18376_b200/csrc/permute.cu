@@ -15,6 +15,8 @@
 //   scatter          -> one block per chunk: rank of each kept slot inside its
 //                       chunk (warp __match_any + per-warp prefix), final row
 //   gather           -> X_perm[row] = X[token(row)], 16-byte vectors
+#include <cooperative_groups.h>
+
 #include "kernels.h"
 
 namespace dsb {
@@ -320,6 +322,174 @@ int launch_scatter(const int32_t* sel_code, const float* sel_raw, int T, int K, 
     scatter_kernel<<<nchunks, threads, smem, stream>>>(sel_code, sel_raw, T, K, E, chunk_off, code_base, row_token,
                                                        row_scale, slot_pos);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// --------------------------------------------------------------------------
+// Fused permutation: scan_codes + seg_plan + scatter in ONE cooperative launch
+// (one CTA per SM, grid-wide barrier between the phases):
+//   A  exclusive scan of every (unit, level) code over the 32-token chunks
+//      -> chunk offsets + per-code totals;
+//   -- grid sync --
+//   B  every CTA derives the unit segments from the totals in shared memory
+//      (CTA 0 publishes them), scatters its share of the chunks (ordered
+//      ranks, the scatter_kernel algorithm) and builds its share of the GEMM
+//      work lists (plan_body).
+// Saves two launches and the kernel boundaries between three latency-bound
+// kernels; results are identical to the three-kernel path.
+// --------------------------------------------------------------------------
+struct PermuteArgs {
+  const int* cnt_chunk;
+  int nchunks, E;
+  int* chunk_off;
+  int* code_tot;
+  int* code_base;
+  UnitSeg* seg;
+  int* r_total;
+  const int32_t* sel_code;
+  const float* sel_raw;
+  int T, K;
+  int32_t* row_token;
+  float* row_scale;
+  int32_t* slot_pos;
+  PlanArgs plan;
+  int do_plan;
+};
+
+__global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a) {
+  namespace cg = cooperative_groups;
+  extern __shared__ int dsm[];  // [2E bases | 4 x (2E carry | 8 x 2E warp counts)]
+  __shared__ int off1[kPlanMaxUnits + 1], off2[kPlanMaxUnits + 1];
+  __shared__ UnitSeg s_seg[256];
+  __shared__ int s_rows[256];
+  __shared__ int warp_sum[32];
+  __shared__ int s_carry;
+  const int ncode = 2 * a.E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // ---- phase A: per-code exclusive scans over chunks (scan_codes_kernel)
+  for (int c = blockIdx.x; c < ncode; c += gridDim.x) {
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int ch0 = 0; ch0 < a.nchunks; ch0 += blockDim.x) {
+      const int ch = ch0 + threadIdx.x;
+      const int v = ch < a.nchunks ? a.cnt_chunk[static_cast<long long>(ch) * ncode + c] : 0;
+      int incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (lane == 31) warp_sum[warp] = incl;
+      __syncthreads();
+      int before = s_carry;
+      for (int w = 0; w < warp; ++w) before += warp_sum[w];
+      if (ch < a.nchunks) a.chunk_off[static_cast<long long>(ch) * ncode + c] = before + incl - v;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < nwarps; ++w) t += warp_sum[w];
+        s_carry += t;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) a.code_tot[c] = s_carry;
+    __syncthreads();
+  }
+  cg::this_grid().sync();
+  // ---- phase B1: unit segments (every CTA, in shared memory)
+  for (int u = threadIdx.x; u < a.E; u += blockDim.x) s_rows[u] = a.code_tot[2 * u] + a.code_tot[2 * u + 1];
+  __syncthreads();
+  const int rtot = block_excl_scan(s_rows, a.E);
+  int* base = dsm;
+  int* carry = dsm + ncode;
+  for (int u = threadIdx.x; u < a.E; u += blockDim.x) {
+    const int nf = a.code_tot[2 * u], nm = a.code_tot[2 * u + 1];
+    s_seg[u] = UnitSeg{s_rows[u], nf, nf + nm, 0};
+    base[2 * u] = s_rows[u];
+    base[2 * u + 1] = s_rows[u] + nf;
+    if (blockIdx.x == 0) {
+      a.seg[u] = s_seg[u];
+      a.code_base[2 * u] = s_rows[u];
+      a.code_base[2 * u + 1] = s_rows[u] + nf;
+    }
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) *a.r_total = rtot;
+  __syncthreads();
+  // ---- phase B2: ordered scatter (scatter_kernel's algorithm); the CTA's
+  // 1024 threads work on kGroups chunks at once, 256 threads (8 warps) each
+  {
+    constexpr int kGroups = 4, kGW = 8;  // chunks in flight per CTA, warps per chunk
+    const int grp = warp / kGW, gwarp = warp % kGW, gtid = threadIdx.x % (kGW * 32);
+    int* gcarry = carry + grp * (ncode + kGW * ncode);
+    int* gwcnt = gcarry + ncode;
+    const long long slots_per_chunk = static_cast<long long>(kRouterChunk) * a.K;
+    const int passes = static_cast<int>((slots_per_chunk + kGW * 32 - 1) / (kGW * 32));
+    for (int c0 = blockIdx.x * kGroups; c0 < a.nchunks; c0 += gridDim.x * kGroups) {
+      const int chunk = c0 + grp;
+      const bool have = chunk < a.nchunks;
+      for (int c = gtid; c < ncode; c += kGW * 32)
+        gcarry[c] = have ? a.chunk_off[static_cast<long long>(chunk) * ncode + c] + base[c] : 0;
+      const long long s0 = static_cast<long long>(chunk) * slots_per_chunk;
+      const long long s1 = have ? min(static_cast<long long>(a.T) * a.K, s0 + slots_per_chunk) : s0;
+      for (int ps = 0; ps < passes; ++ps) {
+        const long long p0 = s0 + static_cast<long long>(ps) * kGW * 32;
+        for (int i = gtid; i < kGW * ncode; i += kGW * 32) gwcnt[i] = 0;
+        __syncthreads();
+        const long long i = p0 + gtid;
+        const int code = i < s1 ? a.sel_code[i] : -1;
+        const int c = code < 0 ? -1 : (code >> 2) * 2 + ((code & 3) == 2 ? 0 : 1);
+        const unsigned mg = __match_any_sync(0xffffffffu, c);
+        const int rank_w = __popc(mg & ((1u << lane) - 1u));
+        if (c >= 0 && rank_w == 0) gwcnt[gwarp * ncode + c] = __popc(mg);
+        __syncthreads();
+        for (int cc = gtid; cc < ncode; cc += kGW * 32) {
+          int run = gcarry[cc];
+          for (int w = 0; w < kGW; ++w) {
+            const int v = gwcnt[w * ncode + cc];
+            gwcnt[w * ncode + cc] = run;
+            run += v;
+          }
+          gcarry[cc] = run;
+        }
+        __syncthreads();
+        if (i < s1) {
+          if (c >= 0) {
+            const int pos = gwcnt[gwarp * ncode + c] + rank_w;
+            a.row_token[pos] = static_cast<int32_t>(i / a.K);
+            a.row_scale[pos] = a.sel_raw[i];
+            a.slot_pos[i] = pos;
+          } else {
+            a.slot_pos[i] = -1;
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // ---- phase B3: this CTA's share of the GEMM work lists
+  if (a.do_plan) plan_body(a.plan, s_seg, off1, off2);
+}
+
+int launch_permute_fused(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
+                         int* r_total, int* code_tot, const int32_t* sel_code, const float* sel_raw, int T, int K,
+                         int32_t* row_token, float* row_scale, int32_t* slot_pos, const PlanArgs* plan, int num_sms,
+                         cudaStream_t stream) {
+  if (E > 256) return -1;
+  PermuteArgs a{cnt_chunk, nchunks, E, chunk_off, code_tot, code_base, seg, r_total, sel_code, sel_raw, T, K,
+                row_token, row_scale, slot_pos, plan ? *plan : PlanArgs{}, plan != nullptr};
+  const int threads = 1024;
+  const size_t smem = static_cast<size_t>(2 * E) * (1 + 4 * (1 + 8)) * sizeof(int);
+  static size_t attr_set = 0;
+  if (smem > 32 * 1024 && smem > attr_set) {
+    cudaFuncSetAttribute(permute_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr_set = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, permute_fused_kernel, threads, smem);
+  if (per_sm < 1) return -3;
+  const int grid = num_sms;  // one CTA per SM: every CTA is co-resident (cooperative launch checks it)
+  void* args[] = {&a};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(permute_fused_kernel), dim3(grid),
+                                                    dim3(threads), args, smem, stream);
+  return e == cudaSuccess ? 0 : -2;
 }
 
 // --------------------------------------------------------------------------
