@@ -212,19 +212,19 @@ __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterA
 // reference's summation order), the arg-max rounds reduce (value desc, index
 // asc) across the quad, and each lane finishes the slots j = q mod 4.
 // One block = 32 tokens = one scatter chunk (kRouterChunk).
-template <int EPT>
-__global__ void __launch_bounds__(kRouterChunk * 4) router_quad_kernel(const RouterArgs a) {
+template <int EPT, int LPT>
+__global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const RouterArgs a) {
   extern __shared__ int s_hist[];  // 2E
   __shared__ uint64_t tab[32];
   __shared__ unsigned long long s_n1, s_nh;
   const int E = a.E, K = a.K, P = a.P;
-  const int lane = threadIdx.x & 31, q = lane & 3, qbase = lane & ~3;
+  const int lane = threadIdx.x & 31, q = lane % LPT, qbase = lane - q;
   for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) s_hist[i] = 0;
   if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
   if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }
   __syncthreads();
   unsigned long long n1 = 0, nh = 0;
-  const int t = blockIdx.x * kRouterChunk + (threadIdx.x >> 2);
+  const int t = blockIdx.x * kRouterChunk + threadIdx.x / LPT;
   const bool tok_ok = t < a.T;  // uniform across the quad
   const int e0 = q * EPT;
   const float* row = a.logits + static_cast<long long>(tok_ok ? t : 0) * a.ld_logits;
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kRouterChunk * 4) router_quad_kernel(const Rou
 #pragma unroll
   for (int i = 0; i < EPT; ++i) mx = (mx < v[i]) ? v[i] : mx;
 #pragma unroll
-  for (int o = 1; o < 4; o <<= 1) {
+  for (int o = 1; o < LPT; o <<= 1) {
     const float other = __shfl_xor_sync(0xffffffffu, mx, o);
     mx = (mx < other) ? other : mx;
   }
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kRouterChunk * 4) router_quad_kernel(const Rou
   for (int i = 0; i < EPT; ++i) v[i] = e0 + i < E ? expf_tab(__fsub_rn(v[i], mx), tab) : 0.0f;
   float sum = 0.0f;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < LPT; ++k) {
     if (q == k) {
 #pragma unroll
       for (int i = 0; i < EPT; ++i)
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kRouterChunk * 4) router_quad_kernel(const Rou
     for (int i = 0; i < EPT; ++i)
       if (e0 + i < E && !((taken >> i) & 1u) && (be == (1 << 30) || v[i] > bv)) { be = e0 + i; bv = v[i]; }
 #pragma unroll
-    for (int o = 1; o < 4; o <<= 1) {
+    for (int o = 1; o < LPT; o <<= 1) {
       const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int oe = __shfl_xor_sync(0xffffffffu, be, o);
       if (oe != (1 << 30) && (be == (1 << 30) || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
@@ -280,13 +280,14 @@ __global__ void __launch_bounds__(kRouterChunk * 4) router_quad_kernel(const Rou
     for (int j = 0; j < K; ++j) dsum = __dadd_rn(dsum, static_cast<double>(sraw[j]));
     if (tok_ok && q == 0 && !(dsum > 0.0)) atomicOr(&a.counters[2], 1ull);
   }
-  // this lane's slots j = q, q+4, ...; top_slot = first maximum of ns (dropping.hpp:99)
-  double nsj[4];
+  // this lane's slots j = q, q+LPT, ...; top_slot = first maximum of ns (dropping.hpp:99)
+  constexpr int kSl = 16 / LPT;  // K <= 16
+  double nsj[kSl];
   double tv = -1.0;
   int ts = 1 << 30;
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    const int j = q + 4 * m;
+  for (int m = 0; m < kSl; ++m) {
+    const int j = q + LPT * m;
     nsj[m] = 0.0;
     if (j < K) {
       nsj[m] = a.normalize ? __ddiv_rn(static_cast<double>(sraw[j]), dsum) : static_cast<double>(sraw[j]);
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(kRouterChunk * 4) router_quad_kernel(const Rou
     }
   }
 #pragma unroll
-  for (int o = 1; o < 4; o <<= 1) {
+  for (int o = 1; o < LPT; o <<= 1) {
     const double ov = __shfl_xor_sync(0xffffffffu, tv, o);
     const int os = __shfl_xor_sync(0xffffffffu, ts, o);
     if (os != (1 << 30) && (ts == (1 << 30) || ov > tv || (ov == tv && os < ts))) { tv = ov; ts = os; }
@@ -302,8 +303,8 @@ __global__ void __launch_bounds__(kRouterChunk * 4) router_quad_kernel(const Rou
   // apply_bands_fn (dropping.hpp:93-122) on this lane's slots
   if (tok_ok) {
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int j = q + 4 * m;
+    for (int m = 0; m < kSl; ++m) {
+      const int j = q + LPT * m;
       if (j >= K) break;
       const int my_e = sel[j];
       const double ns = nsj[m];
@@ -358,9 +359,9 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
   if (blocks <= 0) return 0;
   if (a.E <= 64 && a.K <= 16) {
     if (a.E <= 32)
-      router_quad_kernel<8><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+      router_quad_kernel<8, 4><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
     else
-      router_quad_kernel<16><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+      router_quad_kernel<16, 4><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : -2;
   }
   const int epl = (a.E + 31) / 32;
