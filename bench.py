@@ -431,10 +431,22 @@ def main():
         pol = D.DropPolicy.two_t_from(float(t_drop.item()) / world)
         res = {}
         for name, p_, aware in (("no_drop", D.DropPolicy(), False), ("uniform", pol, False), ("load_aware", pol, True)):
-            ms = time_steps(lambda: m.forward(x, p_, load_aware=aware), args.steps, args.warmup, dist)
+            ms = time_steps(lambda: m.forward(x, p_, load_aware=aware, stats=False), args.steps, args.warmup, dist)
             res[name] = ms / args.steps
         _, rep = m.forward(x, pol, load_aware=True)
         ms_step = res["load_aware"]
+        # ETP vs S-ETP (comm.py): the scenario's payloads moved with each scheme's
+        # NCCL collectives (tp = 2 partial sub-experts per expert when N is even)
+        comm_res = None
+        try:
+            from paper_2508_18376_b200 import comm as CM
+            tp = 2 if world % 2 == 0 else 1
+            scj = {"ep": world // tp, "tp": tp, "tokens_per_device": T * K // 8, "bytes_per_token": d * 2,
+                   "alpha": 1e-5, "beta": 4.5e11, "num_experts": E, "seed": 1}
+            comm_res = CM.CommBench(CM.CommScenario.from_json(scj)).run(iters=10, warmup=2)
+            comm_res["scenario"] = scj
+        except Exception as e:  # noqa: BLE001 — the EP line must still print
+            comm_res = {"error": str(e)}
         value = T * world / (ms_step * 1e-3)
         if rank == 0:
             print(json.dumps({
@@ -450,6 +462,7 @@ def main():
                        "speedup_load_aware_vs_uniform": res["uniform"] / res["load_aware"],
                        "pre_loads": rep["pre_loads"].tolist(), "post_loads": rep["post_loads"].tolist(),
                        "thresholds": [float(v) for v in rep["thresholds"]], "modeled_speedup": rep["speedup"]},
+                "comm_etp_vs_setp": comm_res,
                 "roofline": None, "cpu_baseline": None,
                 "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                         "note": "device-resident inputs under EP"},

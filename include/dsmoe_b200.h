@@ -59,6 +59,8 @@ extern "C" {
 
 #define DSMOE_B200_LOGITS_TENSOR 0 /* gate logits on tcgen05 (bf16 layers) */
 #define DSMOE_B200_LOGITS_EXACT 1  /* serial-k fp32, bit-equal to matmul (matrix.hpp:47) */
+#define DSMOE_B200_LOGITS_REUSE 2  /* the logits of the previous call on this context (same layer, same T):
+                                      re-route a batch under new thresholds without the gate GEMM */
 
 #define DSMOE_B200_METRIC_GATE 0 /* Metric (reconstruct.hpp:13) */
 #define DSMOE_B200_METRIC_ABS_GATE 1

@@ -320,6 +320,9 @@ struct dsmoe_b200_ctx {
       scalars;
   DevBuf tiles1, tiles2, tiles_gate, xperm, H, Y, frac_ws, vseg, vseg_unit;
   int gate_tiles_T = -1, gate_tiles_Epad = -1, gate_tiles_d = -1;
+  // logits left in `logits` by the last routing on this context (LOGITS_REUSE)
+  const void* logits_layer = nullptr;
+  int logits_T = -1, logits_ld = 0;
   long long scale_fill_key = -1;
   unsigned long long last_err_flags = 0;
   // optional per-stage CUDA-event timing (bench.py): 0 gate, 1 router,
@@ -528,6 +531,12 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   const float* lg = logits_in;
   int ld = L->E;
   C->mark(0);
+  if (!lg && logits_mode == DSMOE_B200_LOGITS_REUSE) {
+    require(C->logits_layer == L && C->logits_T == T, DSMOE_E_INVALID_STATE,
+            "logits reuse: the previous routing on this context was for another layer or batch");
+    lg = C->logits.as<float>();
+    ld = C->logits_ld;
+  }
   if (!lg) {
     const bool tc = logits_mode == DSMOE_B200_LOGITS_TENSOR && L->dtype == DSMOE_B200_BF16;
     if (tc) {
@@ -558,6 +567,9 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
     }
     ++g_launches;
     lg = C->logits.as<float>();
+    C->logits_layer = L;
+    C->logits_T = T;
+    C->logits_ld = ld;
   }
   if (logits_out && logits_out != lg) {
     cuda_check(cudaMemcpy2DAsync(logits_out, L->E * 4, lg, ld * 4, L->E * 4, T, cudaMemcpyDeviceToDevice, s),

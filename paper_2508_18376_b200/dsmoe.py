@@ -32,7 +32,7 @@ LIB_PATH = os.path.join(HERE, "libdsmoe_b200.so")
 F32, BF16 = 0, 1
 KIND = {"none": 0, "1t": 1, "2t": 2}
 METRIC = {"gate": 0, "abs_gate": 1, "gate_up": 2, "abs_gate_up": 3}
-LOGITS_TENSOR, LOGITS_EXACT = 0, 1
+LOGITS_TENSOR, LOGITS_EXACT, LOGITS_REUSE = 0, 1, 2
 STATUS = {0: "ok", 1: "invalid_argument", 2: "shape_mismatch", 3: "invalid_state", 4: "io_error",
           5: "bad_magic", 6: "truncated", 7: "schema_error", 8: "internal"}
 

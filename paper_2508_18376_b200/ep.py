@@ -130,7 +130,9 @@ class ExpertParallelMoE:
         self.ctx_exp = D.Context()
 
     def forward(self, x, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,
-                timing=False):
+                timing=False, stats=True):
+        """One EP step; stats=False skips the post-drop load report (one
+        all-reduce + host sync), which the timed bench loop does not need."""
         import torch
         dist, L = self.dist, self.layer
         policy = policy or D.DropPolicy()
@@ -148,8 +150,9 @@ class ExpertParallelMoE:
         # 2. owner-threshold routing + gather
         xp = torch.empty((T * L.K + 128, L.d), dtype=x.dtype, device=dev)
         sp = torch.empty(T * L.K + 128, dtype=torch.float32, device=dev)
+        # same batch, new thresholds: re-route from the logits step 1 left on this context
         seg, R, st = D.dispatch(self.ctx, L, x, policy, t_unit=t_unit, rows_out=xp, scale_out=sp,
-                                logits_mode=logits_mode, with_stats=True)
+                                logits_mode=D.LOGITS_REUSE, with_stats=stats)
         send = send_counts(seg, self.owner, self.world)
         # 3. exchange counts, then rows and scores
         cnt_send = torch.from_numpy(counts_for_receivers(seg, self.owner, self.world)).to(dev)
@@ -175,6 +178,12 @@ class ExpertParallelMoE:
         yb = torch.empty((R + 128, L.d), dtype=x.dtype, device=dev)
         dist.all_to_all_single(yb[:R], yr[:nrecv], send.tolist(), recv.tolist(), group=self.group)
         out = D.combine(self.ctx, L, yb, T)
+        if not stats:
+            rep = {"pre_loads": pre, "thresholds": th, "rows_sent": send, "rows_received": int(nrecv)}
+            if timing:
+                torch.cuda.synchronize()
+                rep["expert_ms"] = ev[0].elapsed_time(ev[1])
+            return out, rep
         post = torch.from_numpy(np.stack([seg[:, 1], seg[:, 2] - seg[:, 1]]).astype(np.int64)).to(dev)
         dist.all_reduce(post, group=self.group)
         post = post.cpu().numpy()
@@ -221,7 +230,7 @@ class EpEmulator:
             a = torch.empty((T * L.K + 128, L.d), dtype=xs[r].dtype, device="cuda")
             b = torch.empty(T * L.K + 128, dtype=torch.float32, device="cuda")
             sg, n, _ = D.dispatch(self.ctx[r], L, xs[r], policy, t_unit=t_unit, rows_out=a, scale_out=b,
-                                  logits_mode=logits_mode)
+                                  logits_mode=D.LOGITS_REUSE)
             xp.append(a), sp.append(b), seg.append(sg), R.append(n)
             send.append(send_counts(sg, self.owner, Dv))
         cnt = [counts_for_receivers(seg[r], self.owner, Dv) for r in range(Dv)]
