@@ -435,6 +435,16 @@ def main():
             res[name] = ms / args.steps
         _, rep = m.forward(x, pol, load_aware=True)
         ms_step = res["load_aware"]
+        # skewed routing (acceptance.cpp:381-387: every token biased toward one
+        # hot expert): where load-aware thresholds matter; t_max for load-aware
+        # is the uniform t (the reference's comparison at equal t_max)
+        hot = host[0].float()[:, 3].cuda()
+        x_sk = (x.float() + (1.5 / hot.norm()) * hot).to(torch.bfloat16)
+        n_sk = max(10, args.steps // 4)
+        res_sk = {}
+        for name, p_, aware in (("no_drop", D.DropPolicy(), False), ("uniform", pol, False), ("load_aware", pol, True)):
+            res_sk[name] = time_steps(lambda: m.forward(x_sk, p_, load_aware=aware, stats=False), n_sk, 3, dist) / n_sk
+        _, rep_sk = m.forward(x_sk, pol, load_aware=True)
         # ETP vs S-ETP (comm.py): the scenario's payloads moved with each scheme's
         # NCCL collectives (tp = 2 partial sub-experts per expert when N is even)
         comm_res = None
@@ -462,6 +472,10 @@ def main():
                        "speedup_load_aware_vs_uniform": res["uniform"] / res["load_aware"],
                        "pre_loads": rep["pre_loads"].tolist(), "post_loads": rep["post_loads"].tolist(),
                        "thresholds": [float(v) for v in rep["thresholds"]], "modeled_speedup": rep["speedup"]},
+                "ep_skewed": {"ms_per_step": res_sk, "speedup_load_aware_vs_no_drop": res_sk["no_drop"] / res_sk["load_aware"],
+                              "speedup_load_aware_vs_uniform": res_sk["uniform"] / res_sk["load_aware"],
+                              "pre_loads": rep_sk["pre_loads"].tolist(), "post_loads": rep_sk["post_loads"].tolist(),
+                              "modeled_speedup": rep_sk["speedup"]},
                 "comm_etp_vs_setp": comm_res,
                 "roofline": None, "cpu_baseline": None,
                 "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
