@@ -551,9 +551,22 @@ __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y, 
         for (int i = 0; i < V; ++i) acc[i] = static_cast<float>(e[i]);
       }
       auto add_vec = [&](const uint4& q) {
-        const TY* e = reinterpret_cast<const TY*>(&q);
+        if constexpr (sizeof(TY) == 2) {
+          // bf16 pairs -> float2 (exact: a bf16 is the top half of an fp32),
+          // packed fp32x2 adds (same per-element IEEE rounding as scalar adds)
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(&q);
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i] += static_cast<float>(e[i]);
+          for (int i = 0; i < V / 2; ++i) {
+            const float2 f = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u));
+            const float2 r = __fadd2_rn(make_float2(acc[2 * i], acc[2 * i + 1]), f);
+            acc[2 * i] = r.x;
+            acc[2 * i + 1] = r.y;
+          }
+        } else {
+          const TY* e = reinterpret_cast<const TY*>(&q);
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] += static_cast<float>(e[i]);
+        }
       };
       // every kept row's vector is requested before the first add (memory-level
       // parallelism), then summed in slot order (deterministic)
