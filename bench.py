@@ -145,11 +145,42 @@ def build_layer(cfg, ctx, calib_tokens=512, seed=0):
     base = D.MoeLayer(d, ffn, E, K, gate, experts, shared, dtype="bf16")
     calib = torch.randn(calib_tokens, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(98))
     calib = calib.to(torch.bfloat16)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     r = D.route_and_drop(ctx, base, calib)
     vals = D.profile_importance(ctx, base, calib, r.indices, "abs_gate")
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
     rec, _ = D.reconstruct_experts(ctx, base, vals)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    OFFLINE[cfg] = {"calib_tokens": calib_tokens, "metric": "abs_gate", "profile_ms": (t1 - t0) * 1e3,
+                    "reconstruct_ms": (t2 - t1) * 1e3}
     host = (gate, experts, shared, E, K, ffn)
     return rec, host
+
+
+OFFLINE = {}  # offline partition timings of build_layer (profile_importance + reconstruct_experts)
+
+
+def cpu_reconstruction_rate(host, T_sample, seed=6):
+    """The reference's profile_importance (reconstruct.hpp:99-149, serial) on
+    T_sample calibration tokens of the same (bf16-valued) base layer."""
+    import numpy as np
+    import oracle as O
+    gate, experts, shared, E, K, ffn = host
+    d = gate.shape[0]
+    f = lambda t: t.float().cpu().numpy()
+    L = O.Layer(d, ffn, E, K, f(gate), [tuple(f(w) for w in ex) for ex in experts],
+                [tuple(f(w) for w in s) for s in shared])
+    R = O.RefLayer.from_layer(L)
+    x = O.bf16_round(np.random.default_rng(seed).standard_normal((T_sample, d), dtype=np.float32))
+    r = R.route_and_drop(x, K, 1)
+    t0 = time.perf_counter()
+    R.profile_importance(x, r.idx, E, ffn, "abs_gate")
+    dt = time.perf_counter() - t0
+    del R
+    return T_sample / dt, dt
 
 
 def calibrate(ctx, layer, x, target, tol=0.005, kind="2t"):
@@ -571,6 +602,17 @@ def main():
             cpu = {"value": None, "unit": "tokens/s", "cores": ncores, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    offline = dict(OFFLINE.get(args.config, {}))
+    if offline:
+        offline["gpu_calib_tokens_per_s"] = offline["calib_tokens"] / ((offline["profile_ms"]) * 1e-3)
+        if not args.no_cpu:
+            try:
+                rate_c, dt_c = cpu_reconstruction_rate(host, 16)
+                offline["cpu_reference"] = {"calib_tokens_per_s": rate_c, "sample": "16 calibration tokens",
+                                            "seconds": dt_c, "cores": 1}
+            except Exception as e:  # noqa: BLE001
+                offline["cpu_reference"] = {"error": str(e)}
+
     epx = None
     if not args.no_ep:
         try:
@@ -619,7 +661,7 @@ def main():
                        "parallelism": "single GPU"},
             "sweep": sweep, "sweep_1t": sweep_1t, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step,
-            "clocks": clk.summary(), "ep_emulated": epx}
+            "clocks": clk.summary(), "ep_emulated": epx, "offline_reconstruction": offline}
     if extra:
         line["extra_configs"] = extra
     print(json.dumps(line))
