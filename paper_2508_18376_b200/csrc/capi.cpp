@@ -139,7 +139,7 @@ int num_sms() {
 
 // ==================================================================== layer
 struct dsmoe_b200_layer;
-bool use_pair(const dsmoe_b200_layer* L);
+int pair_mask(const dsmoe_b200_layer* L);
 
 struct dsmoe_b200_layer {
   int d = 0, ffn = 0, E = 0, K = 0, S = 0, P = 1, prenorm = 0, dtype = DSMOE_B200_BF16;
@@ -166,15 +166,19 @@ struct dsmoe_b200_layer {
   }
 };
 
-bool use_pair(const dsmoe_b200_layer* L) {
-  // CTA-pair (cta_group::2) GEMMs (gemm_tc2.cu) only with DSMOE_B200_CTA_PAIR=1:
-  // correct on the parity suite but measured at 36% tensor-pipe activity vs
-  // 82% for the single-CTA kernel (profiles/r07_summary.md), so off by default.
-  static const bool on = [] {
+int pair_mask(const dsmoe_b200_layer* L) {
+  // Which grouped GEMMs run on CTA pairs (tcgen05 cta_group::2, M = 256
+  // tiles): bit 0 GEMM1, bit 1 GEMM2.  Default: GEMM2 only — measured 15%
+  // fewer cycles than single-CTA tiles, while GEMM1 (long K, fused gather)
+  // gains nothing (profiles/r12_summary.md).  DSMOE_B200_CTA_PAIR: digits
+  // '1' / '2' select GEMM1 / GEMM2, "0" none.
+  static const int mask = [] {
     const char* v = std::getenv("DSMOE_B200_CTA_PAIR");
-    return v && v[0] == '1';
+    if (!v) return 2;
+    const std::string sv(v);
+    return (sv.find('1') != std::string::npos ? 1 : 0) | (sv.find('2') != std::string::npos ? 2 : 0);
   }();
-  return on && L->dtype == DSMOE_B200_BF16;
+  return L->dtype == DSMOE_B200_BF16 ? mask : 0;
 }
 
 namespace {
@@ -405,7 +409,7 @@ struct dsmoe_b200_ctx {
     row_token.ensure(static_cast<size_t>(Rcap + kRowSlack) * 4);
     seg.ensure(sizeof(UnitSeg) * L->E);
     scalars.ensure(4 * sizeof(int));  // r_total, n1, n2, ngate
-    const long long mt = (Rcap + kTileM - 1) / kTileM + L->E;
+    const long long mt = (Rcap + kTileM - 1) / kTileM + 2LL * L->E;  // + per-unit ceil and full/major split
     const long long mts = static_cast<long long>(L->S) * ((T + kTileM - 1) / kTileM);
     const long long t1 = (mt + mts) * L->max_chunks;
     const long long t2 = (mt + mts) * ((L->d + kTileN2 - 1) / kTileN2);
@@ -430,13 +434,13 @@ struct dsmoe_b200_ctx {
   }
   long long max_tiles1(const dsmoe_b200_layer* L, int T) const {
     const long long Rcap = static_cast<long long>(T) * L->K;
-    const long long mt = (Rcap + kTileM - 1) / kTileM + L->E;
+    const long long mt = (Rcap + kTileM - 1) / kTileM + 2LL * L->E;
     const long long mts = static_cast<long long>(L->S) * ((T + kTileM - 1) / kTileM);
     return (mt + mts) * L->max_chunks;
   }
   long long max_tiles2(const dsmoe_b200_layer* L, int T) const {
     const long long Rcap = static_cast<long long>(T) * L->K;
-    const long long mt = (Rcap + kTileM - 1) / kTileM + L->E;
+    const long long mt = (Rcap + kTileM - 1) / kTileM + 2LL * L->E;
     const long long mts = static_cast<long long>(L->S) * ((T + kTileM - 1) / kTileM);
     return (mt + mts) * ((L->d + kTileN2 - 1) / kTileN2);
   }
@@ -608,7 +612,7 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
 
 // K2a: chunk scan + unit segments (+ GEMM work lists) + ordered scatter
 void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool plan, bool gather = false,
-                   int tile_m = kTileM) {
+                   int tile_m = kTileM, int tile_m2 = kTileM) {
   cudaStream_t s = C->stream;
   const long long Rcap = static_cast<long long>(T) * L->K;
   int* r_total = C->scalars.as<int>();
@@ -628,6 +632,7 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
   pa.n2 = r_total + 2;
   pa.gather = gather ? 1 : 0;
   pa.tile_m = tile_m;
+  pa.tile_m2 = tile_m2;
   const int nchunks = (T + kRouterChunk - 1) / kRouterChunk;
   // one cooperative launch by default; DSMOE_B200_PERMUTE=split runs the
   // three-kernel path (scan_codes, seg_plan, scatter) — identical results
@@ -660,24 +665,15 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
 // allocated), alt A = x (shared experts), H in the context, Y = y (ld d).
 void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long long a_rows, const void* x,
                int T, const int* n1, const int* n2, long long max1, long long max2, long long h_rows, void* y,
-               const float* row_scale, const int* row_token = nullptr, bool pair = false, long long y_rows = -1) {
+               const float* row_scale, const int* row_token = nullptr, int pair = 0, long long y_rows = -1) {
   if (y_rows < 0) y_rows = h_rows;
   cudaStream_t s = C->stream;
   const int mt1 = static_cast<int>(std::min<long long>(max1, 1 << 30));
   const int mt2 = static_cast<int>(std::min<long long>(max2, 1 << 30));
-  if (pair) {  // CTA-pair tcgen05 GEMMs over M = 256 tiles
-    const CUtensorMap mx = make_map(x ? x : rows, x ? T : a_rows, L->d, L->d, 128);
-    const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, 128);
-    const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, 128);
-    C->mark(4);
-    launch_check(launch_gemm_tc2(1, &mxp, &mx, &L->map_w13_h, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
-                                 nullptr, num_sms(), s),
-                 "gemm1 (pair)");
-    C->mark(5);
-    launch_check(launch_gemm_tc2(2, &mh, &mh, &L->map_w2t_h, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,
-                                 num_sms(), s),
-                 "gemm2 (pair)");
-  } else if (L->dtype == DSMOE_B200_BF16) {
+  if (L->dtype == DSMOE_B200_BF16) {
+    // pair & 1 / pair & 2: GEMM1 / GEMM2 on CTA pairs (M = 256 tiles, B split
+    // in two 128-row halves, one per CTA)
+    const bool p1 = (pair & 1) != 0, p2 = (pair & 2) != 0;
     const CUtensorMap mx = make_map(x ? x : rows, x ? T : a_rows, L->d, L->d, kTileM);
     const CUtensorMap mxp = make_map(rows, a_rows, L->d, L->d, kTileM);
     const CUtensorMap mh = make_map(C->H.p, h_rows, L->hstride, L->hstride, kTileM);
@@ -685,13 +681,13 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
     const CUtensorMap my = make_map(y, y_rows, L->d, L->d, 32, gemm_tc_store_box_cols());
     const CUtensorMap mh32 = make_map(C->H.p, h_rows, L->hstride, L->hstride, 32, gemm_tc_store_box_cols());
     C->mark(4);
-    launch_check(launch_gemm_tc(1, &mxp, &mx, &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1, C->H.p, L->hstride,
-                                nullptr, 256, num_sms(), s, row_token, row_token ? x : nullptr, static_cast<long long>(L->d) * 2,
-                                &mh32),
+    launch_check(launch_gemm_tc(1, &mxp, &mx, p1 ? &L->map_w13_h : &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1,
+                                C->H.p, L->hstride, nullptr, p1 ? 128 : 256, num_sms(), s, row_token,
+                                row_token ? x : nullptr, static_cast<long long>(L->d) * 2, &mh32, p1 ? 1 : 0),
                  "gemm1");
     C->mark(5);
-    launch_check(launch_gemm_tc(2, &mh, &mh, &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, y, L->d, row_scale,
-                                256, num_sms(), s, nullptr, nullptr, 0, &my),
+    launch_check(launch_gemm_tc(2, &mh, &mh, p2 ? &L->map_w2t_h : &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, y,
+                                L->d, row_scale, p2 ? 128 : 256, num_sms(), s, nullptr, nullptr, 0, &my, p2 ? 1 : 0),
                  "gemm2");
   } else {
     SimtArgs g1{};
@@ -744,9 +740,9 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
     return !(v && std::string(v) == "explicit");
   }();
   const bool fused_gather = fused_env && L->dtype == DSMOE_B200_BF16;
-  const bool pair = use_pair(L) && !fused_gather;
+  const int pair = pair_mask(L);
   C->mark(2);
-  stage_permute(C, L, T, true, fused_gather, pair ? 256 : kTileM);
+  stage_permute(C, L, T, true, fused_gather, (pair & 1) ? 256 : kTileM, (pair & 2) ? 256 : kTileM);
   C->mark(3);
   if (!fused_gather) {
     launch_check(launch_gather(x, C->xperm.p, C->row_token.as<int32_t>(), r_total, L->d * es, num_sms(), s), "gather");
@@ -1122,7 +1118,7 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
                   static_cast<long long>(seg_start[i]) + seg_ntot[i] <= nrows,
               DSMOE_E_INVALID_ARGUMENT, "expert_ffn: segment outside the row buffer");
       sg[i] = UnitSeg{seg_start[i], seg_nfull[i], seg_ntot[i], 0};
-      mt += (seg_ntot[i] + kTileM - 1) / kTileM;
+      mt += (seg_ntot[i] + kTileM - 1) / kTileM + 1;  // + the full / major-only split of GEMM2
     }
     C->vseg.ensure(sizeof(UnitSeg) * nseg);
     C->vseg_unit.ensure(sizeof(int) * nseg);
@@ -1133,7 +1129,7 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
     C->tiles1.ensure(static_cast<size_t>(max1 + 1) * sizeof(GemmTile));
     C->tiles2.ensure(static_cast<size_t>(max2 + 1) * sizeof(GemmTile));
     const long long h_rows = nrows + kRowSlack;
-    const bool pair = use_pair(L);
+    const int pair = pair_mask(L);
     C->H.ensure(static_cast<size_t>(h_rows) * L->hstride * esize(L->dtype));
     int* nn = C->scalars.as<int>();
     PlanArgs pa{};
@@ -1149,7 +1145,8 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
     pa.n1 = nn + 1;
     pa.tiles2 = C->tiles2.as<GemmTile>();
     pa.n2 = nn + 2;
-    pa.tile_m = pair ? 256 : kTileM;
+    pa.tile_m = (pair & 1) ? 256 : kTileM;
+    pa.tile_m2 = (pair & 2) ? 256 : kTileM;
     launch_check(launch_plan(pa, num_sms(), s), "plan");
     ++g_launches;
     run_gemms(C, L, rows, nrows, nullptr, 0, nn + 1, nn + 2, max1, max2, h_rows, y_out, row_scale, nullptr, pair, nrows);

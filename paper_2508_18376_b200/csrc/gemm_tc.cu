@@ -65,12 +65,14 @@ enum { kEpiF32 = 0, kEpiSwiGLU = 1, kEpiScale = 2, kEpiF32Wide = 3 };
 // the fused gather runs (GEMM1).  Gate logits (N = Epad <= 64): 8 KB B slots,
 // so both rings can be 8 deep — the gate GEMM is a 64 MB stream of x with
 // little math, and in-flight bytes are what bound it.
-template <int MODE>
+template <int MODE, bool PAIR = false>
 struct Geo {
   static constexpr bool kGate = MODE == kEpiF32;
-  static constexpr int NA = kGate ? 8 : DSB_A_STAGES;
-  static constexpr int NB = kGate ? 8 : DSB_B_STAGES;
-  static constexpr int BSLOT = kGate ? 64 * kTileK * 2 : kBBytesMax;
+  // CTA pair: each CTA stages its 128 A rows and HALF of the B rows (<= 128,
+  // 16 KB slots), so both rings can be 6 deep in the same shared memory
+  static constexpr int NA = PAIR ? 6 : kGate ? 8 : DSB_A_STAGES;
+  static constexpr int NB = PAIR ? 6 : kGate ? 8 : DSB_B_STAGES;
+  static constexpr int BSLOT = PAIR ? 128 * kTileK * 2 : kGate ? 64 * kTileK * 2 : kBBytesMax;
   static constexpr int NGW = MODE == kEpiSwiGLU ? NA : 0;  // gather warps, warp 1 + s owns A stage s
   static constexpr int GW0 = 1;
   static constexpr int MMA = GW0 + NGW;  // TMEM alloc + tcgen05.mma issue
@@ -174,12 +176,12 @@ __device__ __forceinline__ void row_put(const GemmArgs& args, long long row, int
   for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
+template <int MODE, bool PAIR>
+__global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapO,
                    const GemmArgs args) {
-  using G = Geo<MODE>;
+  using G = Geo<MODE, PAIR>;
   constexpr int kAStages = G::NA, kBStages = G::NB, kBSlot = G::BSLOT;
   constexpr int kGatherWarp0 = G::GW0, kGatherWarps = G::NGW, kMmaWarp = G::MMA, kEpiWarp0 = G::EPI0;
   constexpr int kRingBytes = G::RING;
@@ -201,11 +203,21 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int ntiles = *args.num_tiles;
+  // CTA pair: tiles are M = 256; this CTA owns rows [128 rank, 128 rank + 128)
+  // and the B rows [rank * N/2, (rank + 1) * N/2); the leader issues the MMAs.
+  const int rank = PAIR ? static_cast<int>(pair_rank()) : 0;
+  const bool leader = rank == 0;
+  const int t0 = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int gs = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  const int row_off = 128 * rank;
 
   const bool fused = MODE == kEpiSwiGLU && kGatherWarps > 0 && args.gather_src != nullptr;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kAStages; ++s) {
-      mbar_init(&fullA[s], 1);  // one arrive(.expect_tx): the TMA producer, or the stage's gather warp
+      // TMA-fed stages: one arrive.expect_tx (pair: the leader's, for both CTAs'
+      // bytes; the peer's TMA only completes bytes on it).  Gathered stages:
+      // one arrive per CTA's gather warp.
+      mbar_init(&fullA[s], (PAIR && fused) ? 2 : 1);
       mbar_init(&emptyA[s], 1);
     }
     for (int s = 0; s < kBStages; ++s) {
@@ -214,7 +226,7 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], kEpiThreads);
+      mbar_init(&tempty[s], PAIR ? 16 : kEpiThreads);  // pair: one arrive per epilogue warp of both CTAs
     }
     fence_mbar_init();
     tma_prefetch(&mapA);
@@ -223,13 +235,42 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
     if (args.tma_store) tma_prefetch(&mapO);
   }
   if (warp == kMmaWarp) {
-    tmem_alloc(tmem_slot, 2 * kAccCols);
-    tmem_relinquish();
+    if constexpr (PAIR)
+      tmem_alloc_pair(tmem_slot, 2 * kAccCols);
+    else {
+      tmem_alloc(tmem_slot, 2 * kAccCols);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    pair_sync();  // the peer's barriers exist before any remote arrive
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // "operand ready": own barrier (single CTA) / the leader's (pair)
+  auto ready_arrive = [&](uint64_t* bar) {
+    if constexpr (PAIR)
+      pair_arrive_leader(bar);
+    else
+      mbar_arrive(bar);
+  };
+  // one CTA's TMA load of `bytes` into `dst`, counted on the (leader's) full barrier
+  // peer_arrives: the barrier also counts one arrival from the peer CTA (gathered A ring)
+  auto load_op = [&](void* dst, const void* map, uint64_t* bar, int c0, int c1, uint32_t bytes,
+                     bool peer_arrives = false) {
+    if constexpr (PAIR) {
+      if (leader)
+        mbar_expect_tx(bar, 2 * bytes);
+      else if (peer_arrives)
+        pair_arrive_leader(bar);
+      tma_load_2d_to_leader(dst, map, bar, c0, c1);
+    } else {
+      mbar_expect_tx(bar, bytes);
+      tma_load_2d(dst, map, bar, c0, c1);
+    }
+  };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -238,25 +279,26 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
       uint32_t pa = 0, pb = 0;
       uint64_t pol_b;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_b));
-      GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      GemmTile nxt = t0 < ntiles ? args.tiles[t0] : GemmTile{};
+      for (int t = t0; t < ntiles; t += gs) {
         const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
-        if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
+        if (t + gs < ntiles) nxt = args.tiles[t + gs];
         const bool alt = (tl.m_live & kTileAltA) != 0;
         const void* ma = alt ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
+        const int brow = tl.b_row + (PAIR ? rank * (tl.n_mma >> 1) : 0);
         for (int kb = 0; kb < tl.nkb; ++kb) {
           if (!fused) {
             mbar_wait(&emptyA[sa], pa ^ 1);
-            mbar_expect_tx(&fullA[sa], kABytes);
-            tma_load_2d(ringA + sa * kABytes, ma, &fullA[sa], kb * kTileK, tl.a_row);
+            load_op(ringA + sa * kABytes, ma, &fullA[sa], kb * kTileK, tl.a_row + row_off, kABytes);
             if (++sa == kAStages) { sa = 0; pa ^= 1; }
           }
           mbar_wait(&emptyB[sb], pb ^ 1);
-          mbar_expect_tx(&fullB[sb], args.b_bytes);
-          if (fused && (args.flags & 1))
-            tma_load_2d_hint(ringB + sb * kBSlot, &mapB, &fullB[sb], kb * kTileK, tl.b_row, pol_b);
-          else
-            tma_load_2d(ringB + sb * kBSlot, &mapB, &fullB[sb], kb * kTileK, tl.b_row);
+          if (!PAIR && fused && (args.flags & 1)) {
+            mbar_expect_tx(&fullB[sb], args.b_bytes);
+            tma_load_2d_hint(ringB + sb * kBSlot, &mapB, &fullB[sb], kb * kTileK, brow, pol_b);
+          } else {
+            load_op(ringB + sb * kBSlot, &mapB, &fullB[sb], kb * kTileK, brow, args.b_bytes);
+          }
           if (++sb == kBStages) { sb = 0; pb ^= 1; }
         }
       }
@@ -281,11 +323,13 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
       // i+1 are in flight while tile i's k-blocks are gathered
       auto load_tok = [&](const GemmTile& tl, int* tok) {
         if ((tl.m_live & kTileGatherA) == 0) return;
-        const int* rt = args.row_token + tl.a_row;
+        const int* rt = args.row_token + tl.a_row;  // this CTA's rows start at row_off
 #pragma unroll
-        for (int j = 0; j < 4; ++j) tok[j] = rt[lane + 32 * j < tl.m_valid ? lane + 32 * j : 0];
+        for (int j = 0; j < 4; ++j) {
+          const int i = row_off + lane + 32 * j;
+          tok[j] = rt[i < tl.m_valid ? i : 0];
+        }
       };
-      const int t0 = blockIdx.x, gs = gridDim.x;
       GemmTile cur = t0 < ntiles ? args.tiles[t0] : GemmTile{};
       GemmTile nxt = t0 + gs < ntiles ? args.tiles[t0 + gs] : GemmTile{};
       int tok[4] = {0, 0, 0, 0};
@@ -313,12 +357,14 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
                            : "memory");
             }
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-            fence_proxy_async();  // generic writes -> tcgen05 reads
+            if constexpr (PAIR)  // the leader's MMA reads this CTA's smem
+              asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+            else
+              fence_proxy_async();  // generic writes -> tcgen05 reads
             __syncwarp();
-            if (lane == 0) mbar_arrive(&fullA[gw]);
+            if (lane == 0) ready_arrive(&fullA[gw]);
           } else if (lane == 0) {
-            mbar_expect_tx(&fullA[gw], kABytes);
-            tma_load_2d(sa_ptr, ma, &fullA[gw], kb * kTileK, tl.a_row);
+            load_op(sa_ptr, ma, &fullA[gw], kb * kTileK, tl.a_row + row_off, kABytes, true);
           }
           __syncwarp();
           phase ^= 1;
@@ -340,32 +386,51 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
     uint32_t acc_phase = 0;
     const uint64_t da0 = sdesc_sw128(smem_u32(ringA));  // + (bytes >> 4) moves the start address
     const uint64_t db0 = sdesc_sw128(smem_u32(ringB));
-    GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    GemmTile nxt = t0 < ntiles ? args.tiles[t0] : GemmTile{};
+    for (int t = t0; t < ntiles && leader; t += gs) {
       const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
-      if (t + static_cast<int>(gridDim.x) < ntiles) nxt = args.tiles[t + gridDim.x];
-      const uint32_t idesc = idesc_bf16(kTileM, tl.n_mma);
+      if (t + gs < ntiles) nxt = args.tiles[t + gs];
+      const uint32_t idesc = idesc_bf16(PAIR ? 2 * kTileM : kTileM, tl.n_mma);
       const uint32_t dtmem = tmem_base + acc * kAccCols;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < tl.nkb; ++kb) {
-        mbar_wait(&fullA[sa], pa);
-        mbar_wait(&fullB[sb], pb);
+        if (PAIR && fused) {  // the peer's gathered rows are released at cluster scope
+          mbar_wait_cluster(&fullA[sa], pa);
+          mbar_wait(&fullB[sb], pb);
+        } else {
+          mbar_wait(&fullA[sa], pa);
+          mbar_wait(&fullB[sb], pb);
+        }
         tc_fence_after();
         const uint64_t adesc = da0 + static_cast<uint64_t>(sa * (kABytes >> 4));
         const uint64_t bdesc = db0 + static_cast<uint64_t>(sb * (kBSlot >> 4));
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kTileK / 16; ++k)  // 16 bf16 = 32 B along K inside the 128 B swizzle row
-            umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-          umma_commit(&emptyA[sa]);
-          umma_commit(&emptyB[sb]);
+          for (int k = 0; k < kTileK / 16; ++k) {  // 16 bf16 = 32 B along K inside the 128 B swizzle row
+            if constexpr (PAIR)
+              umma_bf16_pair(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            else
+              umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          if constexpr (PAIR) {
+            umma_commit_pair(&emptyA[sa]);
+            umma_commit_pair(&emptyB[sb]);
+          } else {
+            umma_commit(&emptyA[sa]);
+            umma_commit(&emptyB[sb]);
+          }
         }
         __syncwarp();
         if (++sa == kAStages) { sa = 0; pa ^= 1; }
         if (++sb == kBStages) { sb = 0; pb ^= 1; }
       }
-      if (elect_one()) umma_commit(&tfull[acc]);
+      if (elect_one()) {
+        if constexpr (PAIR)
+          umma_commit_pair(&tfull[acc]);
+        else
+          umma_commit(&tfull[acc]);
+      }
       __syncwarp();
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -378,23 +443,39 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
     uint8_t* wslot = stage_buf + (warp - kEpiWarp0) * kWarpSlot;  // this warp's staging slot
     int acc = 0;
     uint32_t acc_phase = 0;
-    GemmTile nxt = blockIdx.x < static_cast<unsigned>(ntiles) ? args.tiles[blockIdx.x] : GemmTile{};
+    // accumulator drained: MMA may reuse it (pair: one release-arrive per warp
+    // on the leader's barrier)
+    auto release_acc = [&](int a) {
+      tc_fence_before();
+      if constexpr (PAIR) {
+        __syncwarp();
+        if (lane == 0) pair_arrive_leader(&tempty[a]);
+      } else {
+        mbar_arrive(&tempty[a]);
+      }
+    };
+    GemmTile nxt = t0 < ntiles ? args.tiles[t0] : GemmTile{};
     float sc_nxt = 0.f;  // kEpiScale: this thread's row score, loaded a tile ahead
-    if (MODE == kEpiScale && blockIdx.x < static_cast<unsigned>(ntiles) && r < nxt.m_valid)
-      sc_nxt = args.row_scale[nxt.out_row + r];
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
+    if (MODE == kEpiScale && t0 < ntiles && row_off + r < nxt.m_valid)
+      sc_nxt = args.row_scale[nxt.out_row + row_off + r];
+    for (int t = t0; t < ntiles; t += gs) {
+      GemmTile tl = nxt;  // descriptor prefetched one tile ahead
       const float sc_cur = sc_nxt;
-      if (t + static_cast<int>(gridDim.x) < ntiles) {
-        nxt = args.tiles[t + gridDim.x];
-        if (MODE == kEpiScale && r < nxt.m_valid) sc_nxt = args.row_scale[nxt.out_row + r];
+      if (t + gs < ntiles) {
+        nxt = args.tiles[t + gs];
+        if (MODE == kEpiScale && row_off + r < nxt.m_valid) sc_nxt = args.row_scale[nxt.out_row + row_off + r];
+      }
+      if constexpr (PAIR) {  // this CTA's half of the 256-row tile
+        tl.out_row += row_off;
+        tl.m_valid -= row_off;
+        const int live = (tl.m_live & 0xFFFFF) - row_off;
+        tl.m_live = (tl.m_live & ~0xFFFFF) | (live > 0 ? live : 0);
       }
       (void)sc_cur;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (args.flags & 8) {  // diagnostics only (wrong results): no epilogue, MMA-only timing
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        release_acc(acc);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
@@ -437,8 +518,7 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
               row_put(args, orow, tl.out_col + c0 + 32 * gi, pk);
           }
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);  // accumulator drained: MMA may reuse it
+        release_acc(acc);
         if (kStageOut && kBoxCols == 64 && c0 < nc)
           warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c0, tl.m_valid - 32 * q, rows_full, lane);
       } else if constexpr (MODE == kEpiScale) {
@@ -458,10 +538,7 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
             for (int i = 0; i < 32; ++i)
               pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]) * sc, __uint_as_float(v[2 * i + 1]) * sc);
           }
-          if (p == 1) {
-            tc_fence_before();
-            mbar_arrive(&tempty[acc]);
-          }
+          if (p == 1) release_acc(acc);
           if (have && kStageOut && kBoxCols == 64) {
             warp_slot_acquire(lane);
             warp_put(wslot, lane, 0, pk);
@@ -493,18 +570,20 @@ __global__ void __launch_bounds__(Geo<MODE>::THREADS, 1)
           }
         }
       }
-      if constexpr (MODE == kEpiF32 || MODE == kEpiF32Wide) {
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-      }
+      if constexpr (MODE == kEpiF32 || MODE == kEpiF32Wide) release_acc(acc);
       (void)valid; (void)orow;
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
   if (warp >= kEpiWarp0 && lane == 0) bulk_wait0();  // this lane's TMA stores still read its staging slot
   tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) tmem_dealloc(tmem_base, 2 * kAccCols);
+  if constexpr (PAIR) {
+    pair_sync();  // the leader's MMAs read the peer's smem until its last commit
+    if (warp == kMmaWarp) tmem_dealloc_pair(tmem_base, 2 * kAccCols);
+  } else {
+    __syncthreads();
+    if (warp == kMmaWarp) tmem_dealloc(tmem_base, 2 * kAccCols);
+  }
 }
 
 // ------------------------------------------------------------------ launcher
@@ -512,7 +591,7 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
                    int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token,
-                   const void* gather_src, long long gather_ld, const CUtensorMap* mapO) {
+                   const void* gather_src, long long gather_ld, const CUtensorMap* mapO, int pair) {
   static const int flags = [] {
     const char* v = std::getenv("DSMOE_B200_GEMM_FLAGS");
     return v ? std::atoi(v) : 0;
@@ -524,16 +603,51 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
   const CUtensorMap* mo = mapO ? mapO : mapB;
   const int grid = max_tiles < num_sms ? (max_tiles > 0 ? max_tiles : 1) : num_sms;
   cudaError_t err;
+  if (pair) {  // 2-CTA clusters, one M = 256 tile per pair
+    if (mode != kEpiSwiGLU && mode != kEpiScale) return -1;
+    int clusters = num_sms / 2;
+    if (max_tiles < clusters) clusters = max_tiles > 0 ? max_tiles : 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+#define DSB_LAUNCH_PAIR(M)                                                                         \
+  {                                                                                                \
+    static bool attr = false;                                                                      \
+    if (!attr) {                                                                                   \
+      cudaFuncSetAttribute(gemm_tc_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                           Geo<M, true>::SMEM);                                                    \
+      attr = true;                                                                                 \
+    }                                                                                              \
+    cfg.blockDim = dim3(Geo<M, true>::THREADS);                                                    \
+    cfg.dynamicSmemBytes = Geo<M, true>::SMEM;                                                     \
+    err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<M, true>, *mapA, *mapA2, *mapB, *mo, a);         \
+  }
+    if (mode == kEpiSwiGLU)
+      DSB_LAUNCH_PAIR(kEpiSwiGLU)
+    else
+      DSB_LAUNCH_PAIR(kEpiScale)
+#undef DSB_LAUNCH_PAIR
+    if (err != cudaSuccess) return static_cast<int>(err);
+    err = cudaGetLastError();
+    return err == cudaSuccess ? 0 : static_cast<int>(err);
+  }
   switch (mode) {
 #define DSB_LAUNCH(M)                                                                         \
   case M: {                                                                                   \
     static bool attr = false;                                                                 \
     if (!attr) {                                                                              \
-      cudaFuncSetAttribute(gemm_tc_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+      cudaFuncSetAttribute(gemm_tc_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            Geo<M>::SMEM);                                                     \
       attr = true;                                                                            \
     }                                                                                         \
-    gemm_tc_kernel<M><<<grid, Geo<M>::THREADS, Geo<M>::SMEM, stream>>>(*mapA, *mapA2, *mapB, *mo, a); \
+    gemm_tc_kernel<M, false><<<grid, Geo<M>::THREADS, Geo<M>::SMEM, stream>>>(*mapA, *mapA2, *mapB, *mo, a); \
     break;                                                                                    \
   }
     DSB_LAUNCH(kEpiF32)

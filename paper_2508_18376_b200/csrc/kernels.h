@@ -57,7 +57,8 @@ struct PlanArgs {
   GemmTile* tiles2;
   int* n2;
   int gather;                  // GEMM1 routed tiles gather A rows from X through row_token
-  int tile_m;                  // M rows per tile: 128 (gemm_tc) or 256 (gemm_tc2, CTA pair); 0 -> 128
+  int tile_m;                  // GEMM1 rows per tile: 128 (single CTA) or 256 (CTA pair); 0 -> 128
+  int tile_m2;                 // GEMM2 rows per tile; 0 -> tile_m
 };
 int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
                      int* r_total, int* code_tot, const PlanArgs* plan, int num_sms, cudaStream_t stream);
@@ -83,15 +84,9 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
                    int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token = nullptr,
                    const void* gather_src = nullptr, long long gather_ld = 0,
-                   const CUtensorMap* mapO = nullptr);
+                   const CUtensorMap* mapO = nullptr, int pair = 0);
 
 int gemm_tc_store_box_cols();  // TMA-store box width the gemm_tc build expects (64: SW128, 32: SW64)
-
-// gemm_tc2.cu (CTA pairs, M = 256 tiles; B maps with 128-row boxes)
-int launch_gemm_tc2(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2, const CUtensorMap* mapB,
-                    const GemmTile* tiles,
-                    const int* num_tiles, int max_tiles, void* out, long long ldo, const float* row_scale, int num_sms,
-                    cudaStream_t stream);
 
 // gemm_simt.cu
 struct SimtArgs {

@@ -73,7 +73,8 @@ constexpr int kPlanMaxUnits = 2048;
 // full rows, so FLOPs fall with the drop rate (no masks).
 __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int* off2) {
   const int nu = a.num_routed + a.num_shared;
-  const int tm = a.tile_m ? a.tile_m : kTileM;  // 128 (single CTA) or 256 (CTA pair)
+  const int tm = a.tile_m ? a.tile_m : kTileM;     // GEMM1 rows per tile: 128 (single CTA) or 256 (CTA pair)
+  const int tm2 = a.tile_m2 ? a.tile_m2 : tm;      // GEMM2 rows per tile
   const int ntd = cdiv(a.d, kTileN2);
   auto unit_of = [&](int u) { return u < a.num_routed ? (a.seg_unit ? a.seg_unit[u] : u) : a.shared_unit0 + (u - a.num_routed); };
   auto seg_of = [&](int u) {
@@ -89,7 +90,9 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     int c1 = 0;
     for (int p = 0; p < ui.nsub; ++p) c1 += cdiv(ui.sub_wpad[p], kChunk) * (p == 0 ? mt_all : mt_full);
     off1[u] = c1;
-    off2[u] = mt_all * ntd;
+    // GEMM2: the full rows and the major-only rows tile separately, so a tile
+    // never mixes K = full width with K = major width
+    off2[u] = (cdiv(sg.n_full, tm2) + cdiv(sg.n_tot - sg.n_full, tm2)) * ntd;
   }
   __syncthreads();
   const int tot1 = block_excl_scan(off1, nu);
@@ -156,13 +159,16 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     const UnitSeg sg = seg_of(u);
     const int li = i - off2[u];
     const int mt = li / ntd, nt = li - mt * ntd;
-    const int m_valid = min(tm, sg.n_tot - mt * tm);
+    const int mt_f = cdiv(sg.n_full, tm2);
+    const bool full = mt < mt_f;
+    const int row0 = full ? mt * tm2 : sg.n_full + (mt - mt_f) * tm2;
+    const int m_valid = min(tm2, (full ? sg.n_full : sg.n_tot) - row0);
     GemmTile tl;
-    tl.a_row = sg.start + mt * tm;
+    tl.a_row = sg.start + row0;
     tl.b_row = ui.w2t_row + nt * kTileN2;
-    tl.out_row = sg.start + mt * tm;
+    tl.out_row = sg.start + row0;
     tl.out_col = nt * kTileN2;
-    tl.nkb = ((mt * tm < sg.n_full) ? ui.hwidth : ui.sub_wpad[0]) / kTileK;
+    tl.nkb = (full ? ui.hwidth : ui.sub_wpad[0]) / kTileK;
     tl.n_mma = min(kTileN2, a.d - nt * kTileN2);
     tl.m_valid = m_valid;
     tl.m_live = m_valid;
