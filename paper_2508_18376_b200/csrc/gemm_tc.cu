@@ -21,12 +21,19 @@
 //               tile i overlaps the MMAs of tile i+1;
 //   8 epilogue  two warps per TMEM lane quarter: tcgen05.ld 32x32b.x64 ->
 //   warps       registers -> fused op -> bf16 -> per-warp smem slot -> TMA store.
-// Work items (GemmTile) are produced on the device by plan_tiles (permute.cu)
+// Work items (GemmTile) are produced on the device by plan_body (permute.cu)
 // and walked in a static round-robin over the persistent CTAs.
 //
+// PAIR = true (GEMM2 by default): a 2-CTA cluster runs one M = 256 tile with
+// tcgen05.mma.cta_group::2 issued by the leader; each CTA stages its own 128
+// A rows and half of the B rows; TMA bytes of both CTAs are counted by one
+// leader arrive.expect_tx, MMA completion is multicast to both CTAs' empty /
+// accumulator barriers, epilogue warps release the accumulator with one
+// remote arrive each on the leader's barrier.
+//
 // Epilogue modes
-//   kEpiF32     fp32 store (gate logits, K0);
-//   kEpiSwiGLU  h = swish(g) * u over the [g | u] column halves of the tile,
+//   kEpiF32     fp32 store (gate logits, K0; kEpiF32Wide for > 64 experts);
+//   kEpiSwiGLU  h = swish(g) * u over [32 g | 32 u] column groups of the tile,
 //               rows >= m_live store zeros (major-only rows of a minor chunk),
 //               bf16 store into H (K3);
 //   kEpiScale   y = acc * row_scale[row] (the raw gate score, moe.hpp:235-237),
