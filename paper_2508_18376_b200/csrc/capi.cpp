@@ -1150,8 +1150,9 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
     launch_check(launch_plan(pa, num_sms(), s), "plan");
     ++g_launches;
     run_gemms(C, L, rows, nrows, nullptr, 0, nn + 1, nn + 2, max1, max2, h_rows, y_out, row_scale, nullptr, pair, nrows);
-    // keep the caller's buffers alive until the work is done
-    cuda_check(cudaStreamSynchronize(s), "sync");
+    // no host sync: the segment tables were staged by cudaMemcpyAsync from
+    // pageable memory (copied before the call returns); rows / y_out are the
+    // caller's device buffers, ordered on the context stream
   });
 }
 
