@@ -111,6 +111,48 @@ def modeled_speedup(pre, post):
 
 
 # ------------------------------------------------------------ distributed
+class _Coll:
+    """The three collectives the EP step needs.  NCCL: native on device
+    tensors.  Any other backend (gloo — the multi-process tests, several
+    ranks sharing one GPU): host copies, all-to-all as posted isend/irecv."""
+
+    def __init__(self, dist, group):
+        self.dist, self.group = dist, group
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+    def all_reduce(self, t):
+        if self.nccl:
+            self.dist.all_reduce(t, group=self.group)
+            return t
+        h = t.cpu()
+        self.dist.all_reduce(h, group=self.group)
+        return h.to(t.device)
+
+    def all_to_all(self, out, inp, out_splits, in_splits):
+        """out/inp: first-dim splits (rows) per peer, as in all_to_all_single."""
+        if self.nccl:
+            self.dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+            return
+        hi, ho = inp.contiguous().cpu(), out.cpu()
+        reqs, keep, so, ro = [], [], 0, 0
+        for peer in range(self.world):
+            ns, nr = int(in_splits[peer]), int(out_splits[peer])
+            if peer == self.rank:
+                ho[ro:ro + nr] = hi[so:so + ns]
+            else:
+                if ns:
+                    keep.append(hi[so:so + ns])
+                    reqs.append(self.dist.isend(keep[-1], peer, group=self.group))
+                if nr:  # first-dim slices of a contiguous tensor: irecv writes in place
+                    reqs.append(self.dist.irecv(ho[ro:ro + nr], peer, group=self.group))
+            so += ns
+            ro += nr
+        for q in reqs:
+            q.wait()
+        out.copy_(ho.to(out.device))
+
+
 class ExpertParallelMoE:
     """One rank of an expert-parallel MoE layer.  Every rank holds the full
     (replicated) layer object but evaluates only the experts it owns."""
@@ -128,6 +170,7 @@ class ExpertParallelMoE:
         self.local = np.nonzero(self.owner == self.rank)[0]
         self.ctx = D.Context()
         self.ctx_exp = D.Context()
+        self.coll = _Coll(dist, group)
 
     def forward(self, x, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,
                 timing=False, stats=True):
@@ -141,7 +184,7 @@ class ExpertParallelMoE:
         # 1. global pre-drop loads
         seg0, _, _ = D.dispatch(self.ctx, L, x, D.DropPolicy(), logits_mode=logits_mode)
         counts = torch.from_numpy(seg0[:, 2].astype(np.int64)).to(dev)
-        dist.all_reduce(counts, group=self.group)
+        counts = self.coll.all_reduce(counts)
         pre = loads_from_counts(counts.cpu().numpy(), self.owner, self.world)
         t_unit, th = None, np.zeros(self.world)
         if policy.kind != "none":
@@ -157,14 +200,14 @@ class ExpertParallelMoE:
         # 3. exchange counts, then rows and scores
         cnt_send = torch.from_numpy(counts_for_receivers(seg, self.owner, self.world)).to(dev)
         cnt_recv = torch.empty_like(cnt_send)
-        dist.all_to_all_single(cnt_recv, cnt_send, group=self.group)
+        self.coll.all_to_all(cnt_recv, cnt_send, [1] * self.world, [1] * self.world)
         cnt_recv = cnt_recv.cpu().numpy()
         segs, nrecv = receive_segments(cnt_recv, self.local)
         recv = cnt_recv.sum(axis=(1, 2)).astype(np.int64)
         xr = torch.empty((nrecv + 128, L.d), dtype=x.dtype, device=dev)
         sr = torch.empty(nrecv + 128, dtype=torch.float32, device=dev)
-        dist.all_to_all_single(xr[:nrecv], xp[:R], recv.tolist(), send.tolist(), group=self.group)
-        dist.all_to_all_single(sr[:nrecv], sp[:R], recv.tolist(), send.tolist(), group=self.group)
+        self.coll.all_to_all(xr[:nrecv], xp[:R], recv.tolist(), send.tolist())
+        self.coll.all_to_all(sr[:nrecv], sp[:R], recv.tolist(), send.tolist())
         # 4. local experts
         yr = torch.empty_like(xr)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
@@ -176,7 +219,7 @@ class ExpertParallelMoE:
             ev[1].record()
         # 5. return + combine
         yb = torch.empty((R + 128, L.d), dtype=x.dtype, device=dev)
-        dist.all_to_all_single(yb[:R], yr[:nrecv], send.tolist(), recv.tolist(), group=self.group)
+        self.coll.all_to_all(yb[:R], yr[:nrecv], send.tolist(), recv.tolist())
         out = D.combine(self.ctx, L, yb, T)
         if not stats:
             rep = {"pre_loads": pre, "thresholds": th, "rows_sent": send, "rows_received": int(nrecv)}
@@ -185,7 +228,7 @@ class ExpertParallelMoE:
                 rep["expert_ms"] = ev[0].elapsed_time(ev[1])
             return out, rep
         post = torch.from_numpy(np.stack([seg[:, 1], seg[:, 2] - seg[:, 1]]).astype(np.int64)).to(dev)
-        dist.all_reduce(post, group=self.group)
+        post = self.coll.all_reduce(post)
         post = post.cpu().numpy()
         post_loads = post_loads_from_segments(post[0], post[1], self.owner, self.world, L.P)
         rep = {"pre_loads": pre, "post_loads": post_loads, "thresholds": th, "speedup": modeled_speedup(pre, post_loads),
