@@ -427,7 +427,9 @@ def main():
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
+    # one process per GPU; DSMOE_B200_EP_BACKEND=gloo (smoke tests of the N > 1
+    # path with several ranks sharing one GPU) maps ranks onto the visible GPUs
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     use_ep = world > 1 or args.ep
     if use_ep:
         if "MASTER_ADDR" not in os.environ:  # --ep without torchrun: a 1-rank group
@@ -437,7 +439,7 @@ def main():
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]), RANK="0",
                               WORLD_SIZE="1")
             sk.close()
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("DSMOE_B200_EP_BACKEND", "nccl"))
     else:
         dist = None
     import paper_2508_18376_b200 as D

@@ -273,8 +273,8 @@ class CommBench:
         self.rank = dist.get_rank(group)
         if self.world != sc.devices():
             raise ValueError(f"comm bench: world {self.world} != ep x tp {sc.devices()}")
-        self.device = device
         self.nccl = dist.get_backend(group) == "nccl"
+        self.device = device if self.nccl else "cpu"  # gloo point-to-point moves host tensors
         tp = sc.tp_degree
         g, r = divmod(self.rank, tp)
         self.tp_group = None
