@@ -215,6 +215,32 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, co
 int dsmoe_b200_combine(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* y_rows, int T,
                        void* out);
 
+/* EP with one row per (token, destination rank) instead of one per kept
+ * selection.  Sender: after dsmoe_b200_dispatch (rows_out may be NULL) routed
+ * the batch on this context, ep_pack places every token once per rank that
+ * owns one of its kept selections: send_rows (device, >= T*min(nranks,K)
+ * rows, layer dtype) destination-major with tokens ascending; one record per
+ * kept selection (rec_code = expert*4 + level, rec_row = row within the
+ * destination's block, rec_raw = raw score; device, >= T*K) destination-major;
+ * counts (host, 2*nranks) = rows then records per destination.  owner (host,
+ * E) = rank of each expert.  Synchronises the stream. */
+int dsmoe_b200_ep_pack(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T, int nranks,
+                       const int32_t* owner, void* send_rows, int32_t* rec_code, int32_t* rec_row, float* rec_raw,
+                       int64_t* counts);
+/* Receiver: U rows and S records gathered from nranks sources (source s owns
+ * rows [src_row_base[s], src_row_base[s+1]) and records [src_rec_base[s],
+ * src_rec_base[s+1]); host arrays of nranks+1).  out (device, U x d_model) =
+ * per row the sum over its records of raw * expert(row) — the routed experts
+ * only, one row back per (token, rank). */
+int dsmoe_b200_ep_expert(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* rows, long U,
+                         const int32_t* rec_code, const int32_t* rec_row, const float* rec_raw, long S,
+                         const int64_t* src_row_base, const int64_t* src_rec_base, int nranks, void* out);
+/* Sender: out (device, T x d_model) = sum over destinations (ascending) of the
+ * rows returned in send order (ret_rows, same layout as send_rows) + the local
+ * shared experts of the last dispatch. */
+int dsmoe_b200_ep_combine(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* ret_rows, int T,
+                          void* out);
+
 /* dsmoe_b200_forward with flags.  DSMOE_B200_RESIDUAL: out = x + moe(x), the
  * residual step of model_forward_dropped (dropping.hpp:271) fused into the
  * combine kernel (out may not alias x). */

@@ -323,6 +323,9 @@ struct dsmoe_b200_ctx {
   DevBuf logits, sel_code, sel_raw, slot_pos, cnt_chunk, chunk_off, code_base, counters, row_token, row_scale, seg,
       scalars;
   DevBuf tiles1, tiles2, tiles_gate, xperm, H, Y, frac_ws, vseg, vseg_unit;
+  // EP with one row per (token, rank): last ep_pack's layout on this context
+  DevBuf ep_pos_td, ep_send_token, ep_cnt, ep_tot, ep_owner, ep_base;
+  int ep_N = 0, ep_T = -1;
   int gate_tiles_T = -1, gate_tiles_Epad = -1, gate_tiles_d = -1;
   // logits left in `logits` by the last routing on this context (LOGITS_REUSE)
   const void* logits_layer = nullptr;
@@ -612,7 +615,7 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
 
 // K2a: chunk scan + unit segments (+ GEMM work lists) + ordered scatter
 void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool plan, bool gather = false,
-                   int tile_m = kTileM, int tile_m2 = kTileM) {
+                   int tile_m = kTileM, int tile_m2 = kTileM, bool routed_only = false) {
   cudaStream_t s = C->stream;
   const long long Rcap = static_cast<long long>(T) * L->K;
   int* r_total = C->scalars.as<int>();
@@ -622,7 +625,7 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
   pa.seg_unit = nullptr;
   pa.shared_unit0 = L->E;
   pa.num_routed = L->E;
-  pa.num_shared = L->S;
+  pa.num_shared = routed_only ? 0 : L->S;
   pa.T = T;
   pa.d = L->d;
   pa.shared_row0 = static_cast<int>(Rcap);
@@ -723,8 +726,9 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
 }
 
 // ------------------------------------- stage: K2 permute/gather, K3, K4, K5
+// routed_only: the expert side of EP (received rows): no shared experts
 void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T, void* out,
-               const void* resid = nullptr) {
+               const void* resid = nullptr, bool routed_only = false) {
   cudaStream_t s = C->stream;
   const int es = esize(L->dtype);
   const long long Rcap = static_cast<long long>(T) * L->K;
@@ -742,7 +746,7 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   const bool fused_gather = fused_env && L->dtype == DSMOE_B200_BF16;
   const int pair = pair_mask(L);
   C->mark(2);
-  stage_permute(C, L, T, true, fused_gather, (pair & 1) ? 256 : kTileM, (pair & 2) ? 256 : kTileM);
+  stage_permute(C, L, T, true, fused_gather, (pair & 1) ? 256 : kTileM, (pair & 2) ? 256 : kTileM, routed_only);
   C->mark(3);
   if (!fused_gather) {
     launch_check(launch_gather(x, C->xperm.p, C->row_token.as<int32_t>(), r_total, L->d * es, num_sms(), s), "gather");
@@ -754,7 +758,7 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
             C->row_scale.as<float>(), fused_gather ? C->row_token.as<int>() : nullptr, pair);
   C->mark(6);
   launch_check(launch_combine(C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d, L->K,
-                              L->S, static_cast<int>(Rcap), num_sms(), s, resid),
+                              routed_only ? 0 : L->S, static_cast<int>(Rcap), num_sms(), s, resid),
                "combine");
   g_launches += 1;
 }
@@ -1171,6 +1175,97 @@ int dsmoe_b200_combine(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void*
     launch_check(launch_combine2(y_rows, C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d,
                                  L->K, L->S, static_cast<int>(Rcap), num_sms(), C->stream),
                  "combine");
+    ++g_launches;
+  });
+}
+
+int dsmoe_b200_ep_pack(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T, int nranks,
+                       const int32_t* owner, void* send_rows, int32_t* rec_code, int32_t* rec_row, float* rec_raw,
+                       int64_t* counts) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(nranks >= 1 && nranks <= 32, DSMOE_E_INVALID_ARGUMENT, "ep_pack: 1 <= nranks <= 32");
+    require(T >= 1 && x && owner && send_rows && rec_code && rec_row && rec_raw && counts, DSMOE_E_INVALID_ARGUMENT,
+            "null argument");
+    require(C->sel_code.bytes >= static_cast<size_t>(T) * L->K * 4 && C->logits_T == T, DSMOE_E_INVALID_STATE,
+            "ep_pack: no routing recorded on this context for this batch (dispatch first)");
+    for (int e = 0; e < L->E; ++e)
+      require(owner[e] >= 0 && owner[e] < nranks, DSMOE_E_INVALID_ARGUMENT, "ep_pack: owner rank out of range");
+    g_launches = 0;
+    cudaStream_t s = C->stream;
+    const int nchunks = (T + 255) / 256;
+    C->ep_pos_td.ensure(static_cast<size_t>(T) * nranks * 4);
+    C->ep_send_token.ensure(static_cast<size_t>(T) * std::min(nranks, L->K) * 4 + 16);
+    C->ep_cnt.ensure(static_cast<size_t>(2) * nchunks * nranks * 4);
+    C->ep_tot.ensure(static_cast<size_t>(4) * nranks * 4 + 16);
+    C->ep_owner.ensure(static_cast<size_t>(L->E) * 4);
+    cuda_check(cudaMemcpyAsync(C->ep_owner.p, owner, static_cast<size_t>(L->E) * 4, cudaMemcpyHostToDevice, s), "H2D");
+    int* cnt = C->ep_cnt.as<int>();
+    int* r_total = C->ep_tot.as<int>() + 4 * nranks;
+    launch_check(launch_ep_pack(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), C->ep_owner.as<int32_t>(), T, L->K,
+                                nranks, cnt, cnt + nchunks * nranks, C->ep_tot.as<int>(), C->ep_send_token.as<int32_t>(),
+                                C->ep_pos_td.as<int32_t>(), rec_code, rec_row, rec_raw, r_total, num_sms(), s),
+                 "ep_pack");
+    launch_check(launch_gather(x, send_rows, C->ep_send_token.as<int32_t>(), r_total, L->d * esize(L->dtype),
+                               num_sms(), s),
+                 "ep gather");
+    g_launches += 2;
+    std::vector<int> tot(static_cast<size_t>(2 * nranks));
+    cuda_check(cudaMemcpyAsync(tot.data(), C->ep_tot.p, tot.size() * 4, cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    for (int i = 0; i < 2 * nranks; ++i) counts[i] = tot[i];
+    C->ep_N = nranks;
+    C->ep_T = T;
+  });
+}
+
+int dsmoe_b200_ep_expert(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long U,
+                         const int32_t* rec_code, const int32_t* rec_row, const float* rec_raw, long S,
+                         const int64_t* src_row_base, const int64_t* src_rec_base, int nranks, void* out) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(nranks >= 1 && nranks <= 32 && src_row_base && src_rec_base, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(U >= 0 && S >= 0 && U <= (1L << 30), DSMOE_E_INVALID_ARGUMENT, "ep_expert: bad sizes");
+    require(src_row_base[nranks] == U && src_rec_base[nranks] == S, DSMOE_E_INVALID_ARGUMENT,
+            "ep_expert: source bases do not cover the received rows / records");
+    g_launches = 0;
+    if (U == 0) return;
+    require(rows && rec_code && rec_row && rec_raw && out, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    const int Ti = static_cast<int>(U);
+    C->ensure(L, Ti);
+    cudaStream_t s = C->stream;
+    C->ep_base.ensure(static_cast<size_t>(2) * (nranks + 1) * 8);
+    cuda_check(cudaMemcpyAsync(C->ep_base.p, src_rec_base, static_cast<size_t>(nranks + 1) * 8,
+                               cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemcpyAsync(C->ep_base.as<char>() + (nranks + 1) * 8, src_row_base,
+                               static_cast<size_t>(nranks + 1) * 8, cudaMemcpyHostToDevice, s), "H2D");
+    const int nchunks = (Ti + kRouterChunk - 1) / kRouterChunk;
+    cuda_check(cudaMemsetAsync(C->sel_code.p, 0xFF, static_cast<size_t>(Ti) * L->K * 4, s), "memset");
+    cuda_check(cudaMemsetAsync(C->cnt_chunk.p, 0, static_cast<size_t>(nchunks) * 2 * L->E * 4, s), "memset");
+    const long long* b = C->ep_base.as<long long>();
+    launch_check(launch_ep_local_routing(rec_code, rec_row, rec_raw, S, b, b + nranks + 1, nranks, L->K, L->E,
+                                         C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), C->cnt_chunk.as<int>(),
+                                         num_sms(), s),
+                 "ep local routing");
+    ++g_launches;
+    C->logits_T = -1;  // the routing codes on this context are no longer a gate routing
+    stage_ffn(C, L, rows, Ti, out, nullptr, /*routed_only=*/true);
+  });
+}
+
+int dsmoe_b200_ep_combine(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* ret_rows, int T, void* out) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(T >= 1 && ret_rows && out, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(C->ep_T == T && C->ep_N >= 1, DSMOE_E_INVALID_STATE, "ep_combine: no ep_pack recorded for this batch");
+    g_launches = 0;
+    const long long Rcap = static_cast<long long>(T) * L->K;
+    launch_check(launch_ep_final_combine(ret_rows, L->dtype == DSMOE_B200_BF16, C->ep_pos_td.as<int32_t>(), C->ep_N,
+                                         C->Y.p, L->S, static_cast<int>(Rcap), out, T, L->d, num_sms(), C->stream),
+                 "ep combine");
     ++g_launches;
   });
 }

@@ -110,6 +110,11 @@ SYMBOLS = {
     "dsmoe_b200_expert_ffn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_long, C.c_int,
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsmoe_b200_combine": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "dsmoe_b200_ep_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dsmoe_b200_ep_expert": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_long, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_long, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "dsmoe_b200_ep_combine": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "dsmoe_b200_analyze_gating": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                             C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsmoe_b200_drop_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_long, C.c_int, C.c_int, C.c_long, C.c_int,
@@ -536,6 +541,41 @@ def expert_ffn(ctx: Context, layer: MoeLayer, rows, row_scale, segments, y_out=N
                                      rows.shape[0], segs.shape[0], *[c.ctypes.data for c in cols],
                                      C.c_void_p(y_out.data_ptr())))
     return y_out
+
+
+def ep_pack(ctx: Context, layer: MoeLayer, x, nranks: int, owner, send_rows, rec_code, rec_row, rec_raw):
+    """After dispatch() routed x on ctx: one row per (token, owning rank) into
+    send_rows and one record per kept selection; returns (rows per rank,
+    records per rank) as int64 numpy arrays."""
+    own = np.ascontiguousarray(owner, np.int32)
+    counts = np.zeros(2 * nranks, np.int64)
+    _chk(lib().dsmoe_b200_ep_pack(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0], nranks, own.ctypes.data,
+                                  C.c_void_p(send_rows.data_ptr()), C.c_void_p(rec_code.data_ptr()),
+                                  C.c_void_p(rec_row.data_ptr()), C.c_void_p(rec_raw.data_ptr()), counts.ctypes.data))
+    return counts[:nranks].copy(), counts[nranks:].copy()
+
+
+def ep_expert(ctx: Context, layer: MoeLayer, rows, U: int, rec_code, rec_row, rec_raw, S: int, src_row_base,
+              src_rec_base, out=None):
+    """Routed experts over received rows: one output row per received row."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty((max(U, 1), layer.d), dtype=layer.torch_dtype, device=rows.device)
+    rb = np.ascontiguousarray(src_row_base, np.int64)
+    sb = np.ascontiguousarray(src_rec_base, np.int64)
+    _chk(lib().dsmoe_b200_ep_expert(ctx.h, layer.h, C.c_void_p(rows.data_ptr()), U, C.c_void_p(rec_code.data_ptr()),
+                                    C.c_void_p(rec_row.data_ptr()), C.c_void_p(rec_raw.data_ptr()), S, rb.ctypes.data,
+                                    sb.ctypes.data, len(rb) - 1, C.c_void_p(out.data_ptr())))
+    return out
+
+
+def ep_combine(ctx: Context, layer: MoeLayer, ret_rows, T: int, out=None):
+    """out = sum over ranks of the returned rows (send order of the last ep_pack) + shared experts."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty((T, layer.d), dtype=layer.torch_dtype, device=ret_rows.device)
+    _chk(lib().dsmoe_b200_ep_combine(ctx.h, layer.h, C.c_void_p(ret_rows.data_ptr()), T, C.c_void_p(out.data_ptr())))
+    return out
 
 
 def combine(ctx: Context, layer: MoeLayer, y_rows, T, out=None):

@@ -174,8 +174,76 @@ class ExpertParallelMoE:
 
     def forward(self, x, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,
                 timing=False, stats=True):
-        """One EP step; stats=False skips the post-drop load report (one
-        all-reduce + host sync), which the timed bench loop does not need."""
+        """One EP step moving one row per (token, rank) (dsmoe_b200_ep_pack /
+        _ep_expert / _ep_combine): a token goes once to each rank that owns
+        one of its kept selections, with one record per selection; the rank
+        returns one row per token (its experts' weighted sum).  stats=False
+        skips the post-drop load report (an all-reduce + host sync)."""
+        import torch
+        L, W = self.layer, self.world
+        policy = policy or D.DropPolicy()
+        T = x.shape[0]
+        dev = x.device
+        # 1. global pre-drop loads -> thresholds (simulate_step, ep_sim.hpp:110-138)
+        seg0, _, _ = D.dispatch(self.ctx, L, x, D.DropPolicy(), logits_mode=logits_mode)
+        counts = self.coll.all_reduce(torch.from_numpy(seg0[:, 2].astype(np.int64)).to(dev))
+        pre = loads_from_counts(counts.cpu().numpy(), self.owner, W)
+        t_unit, th = None, np.zeros(W)
+        if policy.kind != "none":
+            th = device_thresholds(pre, policy.t_drop, load_aware)
+            t_unit = torch.from_numpy(th[self.owner]).to(dev)
+        # 2. re-route under the owner thresholds (logits of step 1); shared experts run here
+        seg, _, st = D.dispatch(self.ctx, L, x, policy, t_unit=t_unit, logits_mode=D.LOGITS_REUSE, with_stats=stats)
+        # 3. one row per (token, destination) + one record per kept selection
+        cap_rows = T * min(W, L.K) + 1
+        send = torch.empty((cap_rows, L.d), dtype=x.dtype, device=dev)
+        rc = torch.empty(T * L.K + 1, dtype=torch.int32, device=dev)
+        rr = torch.empty_like(rc)
+        rw = torch.empty(T * L.K + 1, dtype=torch.float32, device=dev)
+        nu, ns = D.ep_pack(self.ctx, L, x, W, self.owner, send, rc, rr, rw)
+        # 4. counts, then rows and records
+        cnt = torch.from_numpy(np.stack([nu, ns], axis=1)).to(dev)
+        cnt_recv = torch.empty_like(cnt)
+        self.coll.all_to_all(cnt_recv, cnt, [1] * W, [1] * W)
+        cr = cnt_recv.cpu().numpy()
+        ru, rs = cr[:, 0], cr[:, 1]
+        U, S = int(ru.sum()), int(rs.sum())
+        xr = torch.empty((U + 1, L.d), dtype=x.dtype, device=dev)
+        rcr = torch.empty(S + 1, dtype=torch.int32, device=dev)
+        rrr = torch.empty_like(rcr)
+        rwr = torch.empty(S + 1, dtype=torch.float32, device=dev)
+        self.coll.all_to_all(xr[:U], send[:int(nu.sum())], ru.tolist(), nu.tolist())
+        for dst, src in ((rcr, rc), (rrr, rr), (rwr, rw)):
+            self.coll.all_to_all(dst[:S], src[:int(ns.sum())], rs.tolist(), ns.tolist())
+        # 5. this rank's experts, one output row per received row
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
+        if timing:
+            ev[0].record()
+        yl = D.ep_expert(self.ctx_exp, L, xr, U, rcr, rrr, rwr, S, np.concatenate([[0], np.cumsum(ru)]),
+                         np.concatenate([[0], np.cumsum(rs)]))
+        if timing:
+            ev[1].record()
+        # 6. rows back in send order, summed per token over ranks (+ shared experts)
+        ret = torch.empty((int(nu.sum()) + 1, L.d), dtype=x.dtype, device=dev)
+        self.coll.all_to_all(ret[:int(nu.sum())], yl[:U], nu.tolist(), ru.tolist())
+        out = D.ep_combine(self.ctx, L, ret, T)
+        rep = {"pre_loads": pre, "thresholds": th, "rows_sent": nu, "rows_received": U, "records_sent": ns}
+        if stats:
+            post = torch.from_numpy(np.stack([seg[:, 1], seg[:, 2] - seg[:, 1]]).astype(np.int64)).to(dev)
+            post = self.coll.all_reduce(post).cpu().numpy()
+            rep["post_loads"] = post_loads_from_segments(post[0], post[1], self.owner, W, L.P)
+            rep["speedup"] = modeled_speedup(pre, rep["post_loads"])
+            rep["local_drop_stats"] = st
+        if timing:
+            torch.cuda.synchronize()
+            rep["expert_ms"] = ev[0].elapsed_time(ev[1])
+        return out, rep
+
+    def forward_rows(self, x, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,
+                     timing=False, stats=True):
+        """The first EP data path: one row per kept SELECTION both ways (more
+        bytes; kept for comparison).  stats=False skips the post-drop load
+        report (one all-reduce + host sync)."""
         import torch
         dist, L = self.dist, self.layer
         policy = policy or D.DropPolicy()
