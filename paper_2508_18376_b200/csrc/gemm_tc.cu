@@ -250,10 +250,12 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     }
   }
   tc_fence_before();
-  if constexpr (PAIR)
-    pair_sync();  // the peer's barriers exist before any remote arrive
-  else
+  if constexpr (PAIR) {
+    pair_sync();      // the peer's barriers exist before any remote arrive
+    __syncthreads();  // (and a CTA barrier the race checker models for the TMEM slot)
+  } else {
     __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // "operand ready": own barrier (single CTA) / the leader's (pair)

@@ -59,7 +59,9 @@ __device__ int block_excl_scan(int* v, int n) {
     if (threadIdx.x == 0) s_carry += s_tot;
     __syncthreads();
   }
-  return s_carry;
+  const int total = s_carry;
+  __syncthreads();  // every thread has read s_carry before a next call resets it
+  return total;
 }
 
 // --------------------------------------------------------------------------
