@@ -212,3 +212,21 @@ def test_empty_and_tiny_batches(ctx, c1):
         assert scaled_residual(y.cpu().numpy(), yo) < TOL_F32
     y0 = pkg.forward(ctx, layer, torch.empty((0, 512), device="cuda"), pkg.DropPolicy())
     assert y0.shape == (0, 512)
+
+
+def test_model_forward_dropped_two_layers(ctx):
+    """model_forward_dropped (dropping.hpp:263-274): x_{l+1} = x_l + moe_l(x_l),
+    the residual fused into the combine, per-layer routing and DropStats."""
+    pkg = D()
+    Ls = [O.partial_transform(O.generate_layer(128, 128, 8, 2, seed=s), 2) for s in (81, 82)]
+    layers = [dev_layer(L, "f32") for L in Ls]
+    x = O.generate_tokens(96, 128, seed=83)
+    y, stats = pkg.model_forward_dropped(ctx, layers, torch.from_numpy(x).cuda(), pkg.DropPolicy.two_t_from(0.3),
+                                         logits_mode=pkg.LOGITS_EXACT)
+    cur = x.astype(np.float32)
+    for L, st in zip(Ls, stats):
+        ro = O.route(L, cur, "2t", 0.3)
+        cur = (cur + O.moe_forward(L, cur, ro.idx, ro.raw, ro.frac)).astype(np.float32)
+        so = O.drop_stats(np.ones_like(ro.frac), ro.frac, 2, 0, cur.shape[0], L.d, L.ffn)
+        assert st["drop_rate"] == so["drop_rate"]
+    assert scaled_residual(y.cpu().numpy(), cur) < TOL_F32
