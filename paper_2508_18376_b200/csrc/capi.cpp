@@ -168,13 +168,13 @@ struct dsmoe_b200_layer {
 
 int pair_mask(const dsmoe_b200_layer* L) {
   // Which grouped GEMMs run on CTA pairs (tcgen05 cta_group::2, M = 256
-  // tiles): bit 0 GEMM1, bit 1 GEMM2.  Default: GEMM2 only — measured 15%
-  // fewer cycles than single-CTA tiles, while GEMM1 (long K, fused gather)
-  // gains nothing (profiles/r12_summary.md).  DSMOE_B200_CTA_PAIR: digits
-  // '1' / '2' select GEMM1 / GEMM2, "0" none.
+  // tiles): bit 0 GEMM1, bit 1 GEMM2.  Default: both — GEMM2 15% and GEMM1
+  // (fused gather, CTA-scope stage hand-off) 11% fewer cycles than
+  // single-CTA tiles (profiles/r12_summary.md, r13_summary.md).
+  // DSMOE_B200_CTA_PAIR: digits '1' / '2' select GEMM1 / GEMM2, "0" none.
   static const int mask = [] {
     const char* v = std::getenv("DSMOE_B200_CTA_PAIR");
-    if (!v) return 2;
+    if (!v) return 3;
     const std::string sv(v);
     return (sv.find('1') != std::string::npos ? 1 : 0) | (sv.find('2') != std::string::npos ? 2 : 0);
   }();

@@ -46,6 +46,17 @@ namespace dsb {
 
 // Separate operand rings: A (128 x 64 rows of tokens) is the latency-critical
 // one under the fused gather, so it is deeper than the B (weights) ring.
+// CTA pair + fused gather: how the peer's gathered A stage is handed to the
+// leader's MMA.  1 (default): the gather warp waits for its cp.async group,
+// fences generic -> async proxy at CTA scope and arrives on the leader's
+// barrier with a plain (release.cta) remote arrive, the MMA warp polls it with
+// a plain try_wait — the hand-off CUTLASS's 2-SM UMMA pipelines use
+// (umma_arrive_2x1SM_sm0).  0: release.cluster arrive + acquire.cluster wait +
+// cluster-scope proxy fence, which costs 45% more GEMM1 cycles (1361 vs 832
+// kcyc, profiles/r13_summary.md).
+#ifndef DSB_PAIR_RELAXED
+#define DSB_PAIR_RELAXED 1
+#endif
 #ifndef DSB_A_STAGES
 #define DSB_A_STAGES 5
 #endif
@@ -273,7 +284,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       if (leader)
         mbar_expect_tx(bar, 2 * bytes);
       else if (peer_arrives)
-        pair_arrive_leader(bar);
+        DSB_PAIR_RELAXED ? pair_arrive_leader_cta(bar) : pair_arrive_leader(bar);
       tma_load_2d_to_leader(dst, map, bar, c0, c1);
     } else {
       mbar_expect_tx(bar, bytes);
@@ -366,12 +377,17 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
                            : "memory");
             }
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-            if constexpr (PAIR)  // the leader's MMA reads this CTA's smem
+            if constexpr (PAIR && !DSB_PAIR_RELAXED)  // the leader's MMA reads this CTA's smem
               asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
             else
               fence_proxy_async();  // generic writes -> tcgen05 reads
             __syncwarp();
-            if (lane == 0) ready_arrive(&fullA[gw]);
+            if (lane == 0) {
+              if constexpr (PAIR && DSB_PAIR_RELAXED)
+                pair_arrive_leader_cta(&fullA[gw]);
+              else
+                ready_arrive(&fullA[gw]);
+            }
           } else if (lane == 0) {
             load_op(sa_ptr, ma, &fullA[gw], kb * kTileK, tl.a_row + row_off, kABytes, true);
           }
@@ -404,7 +420,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < tl.nkb; ++kb) {
-        if (PAIR && fused) {  // the peer's gathered rows are released at cluster scope
+        if (PAIR && fused && !DSB_PAIR_RELAXED) {  // the peer's gathered rows are released at cluster scope
           mbar_wait_cluster(&fullA[sa], pa);
           mbar_wait(&fullB[sb], pb);
         } else {
