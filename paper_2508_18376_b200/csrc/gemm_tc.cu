@@ -57,6 +57,12 @@ namespace dsb {
 #ifndef DSB_PAIR_RELAXED
 #define DSB_PAIR_RELAXED 1
 #endif
+#ifndef DSB_PA_STAGES  // CTA pairs: A / B ring depths (16 KB slots each)
+#define DSB_PA_STAGES 6
+#endif
+#ifndef DSB_PB_STAGES
+#define DSB_PB_STAGES 6
+#endif
 #ifndef DSB_A_STAGES
 #define DSB_A_STAGES 5
 #endif
@@ -88,8 +94,8 @@ struct Geo {
   static constexpr bool kGate = MODE == kEpiF32;
   // CTA pair: each CTA stages its 128 A rows and HALF of the B rows (<= 128,
   // 16 KB slots), so both rings can be 6 deep in the same shared memory
-  static constexpr int NA = PAIR ? 6 : kGate ? 8 : DSB_A_STAGES;
-  static constexpr int NB = PAIR ? 6 : kGate ? 8 : DSB_B_STAGES;
+  static constexpr int NA = PAIR ? DSB_PA_STAGES : kGate ? 8 : DSB_A_STAGES;
+  static constexpr int NB = PAIR ? DSB_PB_STAGES : kGate ? 8 : DSB_B_STAGES;
   static constexpr int BSLOT = PAIR ? 128 * kTileK * 2 : kGate ? 64 * kTileK * 2 : kBBytesMax;
   static constexpr int NGW = MODE == kEpiSwiGLU ? NA : 0;  // gather warps, warp 1 + s owns A stage s
   static constexpr int GW0 = 1;
@@ -474,7 +480,12 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       tc_fence_before();
       if constexpr (PAIR) {
         __syncwarp();
-        if (lane == 0) pair_arrive_leader(&tempty[a]);
+        if (lane == 0) {
+          if constexpr (DSB_PAIR_RELAXED)
+            pair_arrive_leader_cta(&tempty[a]);
+          else
+            pair_arrive_leader(&tempty[a]);
+        }
       } else {
         mbar_arrive(&tempty[a]);
       }
@@ -499,7 +510,9 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       (void)sc_cur;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if (args.flags & 8) {  // diagnostics only (wrong results): no epilogue, MMA-only timing
+      // diagnostics only (wrong results): no epilogue, MMA-only timing of the
+      // expert GEMMs (the gate keeps its epilogue so the routing is unchanged)
+      if ((args.flags & 8) && MODE != kEpiF32 && MODE != kEpiF32Wide) {
         release_acc(acc);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
