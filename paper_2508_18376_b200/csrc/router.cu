@@ -209,14 +209,41 @@ __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterA
 // Quad-per-token variant for E <= 4 * EPT (64): lane q of a token's quad
 // holds experts [q*EPT, (q+1)*EPT) in registers.  The softmax denominator is
 // one ascending-e chain of float adds handed from lane to lane (the
-// reference's summation order), the arg-max rounds reduce (value desc, index
-// asc) across the quad, and each lane finishes the slots j = q mod 4.
-// One block = 32 tokens = one scatter chunk (kRouterChunk).
-template <int EPT, int LPT>
+// reference's summation order).  topk_route's K arg-max rounds (strict >,
+// lower index wins) are the descending order of the keys (probability bits
+// << 32) | ~expert (router_kernel): each lane sorts its keys with a register
+// bitonic network, then two bitonic merges with the partner lanes (xor 1,
+// xor 2) leave the quad's top KK keys, sorted, on every lane — a few dozen
+// dependent steps instead of K serial scan + shuffle rounds.  Each lane then
+// finishes the slots j = q mod 4.  One block = 32 tokens = one scatter chunk
+// (kRouterChunk).
+template <int N>
+__device__ __forceinline__ void sort_desc(unsigned long long (&k)[N]) {
+#pragma unroll
+  for (int w = 2; w <= N; w <<= 1) {
+#pragma unroll
+    for (int j = w >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = k[i], b = k[l];
+          const bool sw = ((i & w) == 0) ? (a < b) : (a > b);
+          k[i] = sw ? b : a;
+          k[l] = sw ? a : b;
+        }
+      }
+    }
+  }
+}
+
+template <int EPT, int LPT, int KK>
 __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const RouterArgs a) {
   extern __shared__ int s_hist[];  // 2E
   __shared__ uint64_t tab[32];
   __shared__ unsigned long long s_n1, s_nh;
+  static_assert(KK <= 16 && EPT <= 16, "quad router: at most 16 keys per lane");
+  constexpr int NS = KK > EPT ? KK : EPT;  // keys sorted per lane (padded with 0 = "no expert")
   const int E = a.E, K = a.K, P = a.P;
   const int lane = threadIdx.x & 31, q = lane % LPT, qbase = lane - q;
   for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) s_hist[i] = 0;
@@ -254,43 +281,75 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
   }
 #pragma unroll
   for (int i = 0; i < EPT; ++i) v[i] = __fdiv_rn(v[i], sum);
-  // topk_route (moe.hpp:193-205): K rounds; round winner = max value, lowest index
-  uint32_t taken = 0u;
-  float sraw[16];
-  int sel[16];
-  for (int j = 0; j < K; ++j) {
-    int be = 1 << 30;
-    float bv = 0.0f;
+  // topk_route (moe.hpp:193-205) as a key sort
+  unsigned long long key[NS];
 #pragma unroll
-    for (int i = 0; i < EPT; ++i)
-      if (e0 + i < E && !((taken >> i) & 1u) && (be == (1 << 30) || v[i] > bv)) { be = e0 + i; bv = v[i]; }
+  for (int i = 0; i < NS; ++i) {
+    const int e = e0 + i;
+    key[i] = (i < EPT && e < E) ? (static_cast<unsigned long long>(__float_as_uint(v[i < EPT ? i : 0])) << 32) |
+                                      static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<unsigned>(e))
+                                : 0ull;
+  }
+  sort_desc<NS>(key);
 #pragma unroll
-    for (int o = 1; o < LPT; o <<= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
-      if (oe != (1 << 30) && (be == (1 << 30) || ov > bv || (ov == bv && oe < be))) { bv = ov; be = oe; }
+  for (int m = 1; m < LPT; m <<= 1) {
+    // top KK of (mine U partner's): max(mine[i], theirs[KK-1-i]) is bitonic
+    unsigned long long c[KK];
+#pragma unroll
+    for (int i = 0; i < KK; ++i) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, key[KK - 1 - i], m);
+      c[i] = key[i] > o ? key[i] : o;
     }
-    if (be - e0 >= 0 && be - e0 < EPT) taken |= 1u << (be - e0);
-    sel[j] = be;
-    sraw[j] = bv;
+#pragma unroll
+    for (int j = KK >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < KK; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long x = c[i], y = c[l];
+          c[i] = x > y ? x : y;
+          c[l] = x > y ? y : x;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KK; ++i) key[i] = c[i];
+  }
+  float sraw[KK];
+  int sel[KK];
+#pragma unroll
+  for (int j = 0; j < KK; ++j) {
+    sel[j] = static_cast<int>(0xFFFFFFFFu - static_cast<unsigned>(key[j] & 0xFFFFFFFFull));
+    sraw[j] = __uint_as_float(static_cast<unsigned>(key[j] >> 32));
   }
   // normalize_topk (dropping.hpp:60-72)
   double dsum = 0.0;
   if (a.normalize) {
-    for (int j = 0; j < K; ++j) dsum = __dadd_rn(dsum, static_cast<double>(sraw[j]));
+#pragma unroll
+    for (int j = 0; j < KK; ++j)
+      if (j < K) dsum = __dadd_rn(dsum, static_cast<double>(sraw[j]));
     if (tok_ok && q == 0 && !(dsum > 0.0)) atomicOr(&a.counters[2], 1ull);
   }
   // this lane's slots j = q, q+LPT, ...; top_slot = first maximum of ns (dropping.hpp:99)
-  constexpr int kSl = 16 / LPT;  // K <= 16
+  constexpr int kSl = KK / LPT;
   double nsj[kSl];
+  float rsj[kSl];
+  int esj[kSl];
   double tv = -1.0;
   int ts = 1 << 30;
 #pragma unroll
   for (int m = 0; m < kSl; ++m) {
     const int j = q + LPT * m;
+    float rj = 0.0f;
+    int ej = 0;
+#pragma unroll
+    for (int jj = LPT * m; jj < LPT * (m + 1); ++jj)
+      if (jj == j) { rj = sraw[jj]; ej = sel[jj]; }
+    rsj[m] = rj;
+    esj[m] = ej;
     nsj[m] = 0.0;
     if (j < K) {
-      nsj[m] = a.normalize ? __ddiv_rn(static_cast<double>(sraw[j]), dsum) : static_cast<double>(sraw[j]);
+      nsj[m] = a.normalize ? __ddiv_rn(static_cast<double>(rj), dsum) : static_cast<double>(rj);
       if (ts == (1 << 30) || nsj[m] > tv) { tv = nsj[m]; ts = j; }
     }
   }
@@ -306,7 +365,7 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
     for (int m = 0; m < kSl; ++m) {
       const int j = q + LPT * m;
       if (j >= K) break;
-      const int my_e = sel[j];
+      const int my_e = esj[m];
       const double ns = nsj[m];
       int lv = 2;
       if (a.kind != 0) {
@@ -325,13 +384,13 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
         nh += fc == 1;
         const long long g = static_cast<long long>(t) * K * P + static_cast<long long>(cp) * K + j;
         if (a.idx) a.idx[g] = my_e * P + cp;
-        if (a.raw) a.raw[g] = sraw[j];
+        if (a.raw) a.raw[g] = rsj[m];
         if (a.norm) a.norm[g] = ns;
         if (a.frac) a.frac[g] = fc;
       }
       const long long qi = static_cast<long long>(t) * K + j;
       a.sel_code[qi] = lv > 0 ? my_e * 4 + lv : -1;
-      a.sel_raw[qi] = sraw[j];
+      a.sel_raw[qi] = rsj[m];
       if (lv > 0) atomicAdd(&s_hist[2 * my_e + (lv == 2 ? 0 : 1)], 1);
     }
   }
@@ -358,10 +417,14 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(2 * a.E) * sizeof(int);
   if (blocks <= 0) return 0;
   if (a.E <= 64 && a.K <= 16) {
-    if (a.E <= 32)
-      router_quad_kernel<8, 4><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+    if (a.E <= 32 && a.K <= 8)
+      router_quad_kernel<8, 4, 8><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+    else if (a.E <= 32)
+      router_quad_kernel<8, 4, 16><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+    else if (a.K <= 8)
+      router_quad_kernel<16, 4, 8><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
     else
-      router_quad_kernel<16, 4><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+      router_quad_kernel<16, 4, 16><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : -2;
   }
   const int epl = (a.E + 31) / 32;
