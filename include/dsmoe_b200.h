@@ -157,7 +157,7 @@ int dsmoe_b200_ctx_check(dsmoe_b200_ctx* ctx);
  * 1 router, 2 permute + tile plan, 3 gather, 4 grouped GEMM1 ([W1|W3] +
  * SwiGLU), 5 grouped GEMM2 (W2 + score), 6 combine.  ms receives the summed
  * milliseconds per stage since profiling was (re)enabled. */
-int dsmoe_b200_ctx_set_profiling(dsmoe_b200_ctx* ctx, int on);
+int dsmoe_b200_ctx_set_profiling(dsmoe_b200_ctx* ctx, int on);  /* on = N > 1: every N-th forward */
 int dsmoe_b200_ctx_profile(dsmoe_b200_ctx* ctx, double* ms, int n, long* calls);
 
 /* The token permutation of the last forward on this context (host copies,

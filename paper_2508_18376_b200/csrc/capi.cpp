@@ -344,6 +344,8 @@ struct dsmoe_b200_ctx {
     bool hit[kStages + 1] = {};
   };
   bool profiling = false;
+  int prof_period = 1;    // profile every prof_period-th forward (the others run unmarked)
+  long prof_seen = 0;
   std::vector<EvSet> ring;
   int ring_head = 0, ring_pending = 0;
   EvSet* cur = nullptr;
@@ -355,7 +357,8 @@ struct dsmoe_b200_ctx {
     cur->hit[i] = true;
   }
   void prof_begin() {
-    if (!profiling) return;
+    cur = nullptr;
+    if (!profiling || (prof_seen++ % prof_period) != 0) return;
     if (ring.empty()) {
       ring.resize(kRing);
       for (auto& es : ring)
@@ -878,8 +881,11 @@ int dsmoe_b200_ctx_check(dsmoe_b200_ctx* C) {
 int dsmoe_b200_ctx_set_profiling(dsmoe_b200_ctx* C, int on) {
   return guarded([&] {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require(on >= 0, DSMOE_E_INVALID_ARGUMENT, "profiling period must be >= 0");
     C->resolve();
     C->profiling = on != 0;
+    C->prof_period = on > 1 ? on : 1;
+    C->prof_seen = 0;
     for (double& v : C->prof_ms) v = 0.0;
     C->prof_calls = 0;
   });

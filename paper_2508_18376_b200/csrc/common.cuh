@@ -7,6 +7,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "expf_glibc.h"
 
@@ -312,5 +313,40 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 #endif  // __CUDACC__
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: the forward's kernels are launched with
+// programmaticStreamSerialization, so a kernel's CTAs may start (prologue:
+// barrier init, TMEM alloc, descriptor prefetch) while its predecessor drains;
+// every such kernel calls pdl_wait() before touching global memory the
+// predecessor writes or reads.  No kernel triggers early
+// (griddepcontrol.launch_dependents): successors launch as the predecessor's
+// CTAs exit, so they never co-reside with a running persistent GEMM.
+// DSMOE_B200_PDL=0 launches without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("DSMOE_B200_PDL");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
 
 }  // namespace dsb

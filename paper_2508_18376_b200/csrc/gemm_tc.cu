@@ -226,7 +226,6 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int ntiles = *args.num_tiles;
   // CTA pair: tiles are M = 256; this CTA owns rows [128 rank, 128 rank + 128)
   // and the B rows [rank * N/2, (rank + 1) * N/2); the leader issues the MMAs.
   const int rank = PAIR ? static_cast<int>(pair_rank()) : 0;
@@ -275,6 +274,8 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the predecessor's outputs (tile lists, A rows) are complete from here on
+  const int ntiles = *args.num_tiles;
   // "operand ready": own barrier (single CTA) / the leader's (pair)
   auto ready_arrive = [&](uint64_t* bar) {
     if constexpr (PAIR)
@@ -648,13 +649,15 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * clusters);
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
 #define DSB_LAUNCH_PAIR(M)                                                                         \
   {                                                                                                \
     static bool attr = false;                                                                      \
@@ -685,7 +688,9 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                            Geo<M>::SMEM);                                                     \
       attr = true;                                                                            \
     }                                                                                         \
-    gemm_tc_kernel<M, false><<<grid, Geo<M>::THREADS, Geo<M>::SMEM, stream>>>(*mapA, *mapA2, *mapB, *mo, a); \
+    err = launch_pdl(gemm_tc_kernel<M, false>, dim3(grid), dim3(Geo<M>::THREADS), Geo<M>::SMEM, stream, *mapA, \
+                     *mapA2, *mapB, *mo, a);                                                  \
+    if (err != cudaSuccess) return static_cast<int>(err);                                      \
     break;                                                                                    \
   }
     DSB_LAUNCH(kEpiF32)

@@ -373,6 +373,7 @@ __global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a
   __shared__ int s_carry;
   const int ncode = 2 * a.E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  pdl_wait();
   // ---- phase A: per-code exclusive scans over chunks (scan_codes_kernel)
   for (int c = blockIdx.x; c < ncode; c += gridDim.x) {
     if (threadIdx.x == 0) s_carry = 0;
@@ -494,9 +495,19 @@ int launch_permute_fused(const int* cnt_chunk, int nchunks, int E, int* chunk_of
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, permute_fused_kernel, threads, smem);
   if (per_sm < 1) return -3;
   const int grid = num_sms;  // one CTA per SM: every CTA is co-resident (cooperative launch checks it)
-  void* args[] = {&a};
-  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(permute_fused_kernel), dim3(grid),
-                                                    dim3(threads), args, smem, stream);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, permute_fused_kernel, a);
   return e == cudaSuccess ? 0 : -2;
 }
 
@@ -547,6 +558,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y, 
                                                       int S, int shared_row0, const TY* __restrict__ resid) {
   constexpr int V = 16 / sizeof(TY);  // elements per 16-byte vector
   const int nvec = d / V;
+  pdl_wait();
   for (int t = blockIdx.x; t < T; t += gridDim.x) {
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
       float acc[V];
@@ -614,14 +626,13 @@ int launch_combine2(const void* y, const void* ysh, int y_bf16, const int32_t* s
                     int K, int S, int shared_row0, int num_sms, cudaStream_t stream, const void* resid) {
   const int grid = T < num_sms * 16 ? (T > 0 ? T : 1) : num_sms * 16;
   if (y_bf16)
-    combine_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16*>(y), static_cast<const __nv_bfloat16*>(ysh), slot_pos,
-        static_cast<__nv_bfloat16*>(out), T, d, K, S, shared_row0, static_cast<const __nv_bfloat16*>(resid));
+    launch_pdl(combine_kernel<__nv_bfloat16, __nv_bfloat16>, dim3(grid), dim3(256), 0, stream,
+               static_cast<const __nv_bfloat16*>(y), static_cast<const __nv_bfloat16*>(ysh), slot_pos,
+               static_cast<__nv_bfloat16*>(out), T, d, K, S, shared_row0, static_cast<const __nv_bfloat16*>(resid));
   else
-    combine_kernel<float, float><<<grid, 256, 0, stream>>>(static_cast<const float*>(y),
-                                                           static_cast<const float*>(ysh), slot_pos,
-                                                           static_cast<float*>(out), T, d, K, S, shared_row0,
-                                                           static_cast<const float*>(resid));
+    launch_pdl(combine_kernel<float, float>, dim3(grid), dim3(256), 0, stream, static_cast<const float*>(y),
+               static_cast<const float*>(ysh), slot_pos, static_cast<float*>(out), T, d, K, S, shared_row0,
+               static_cast<const float*>(resid));
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterA
   if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
   if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }
   __syncthreads();
+  pdl_wait();
   constexpr int epl = EPL;
   unsigned long long n1 = 0, nh = 0;
   const int t = blockIdx.x * kRouterChunk + warp;  // one token per warp
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
   if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
   if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }
   __syncthreads();
+  pdl_wait();
   unsigned long long n1 = 0, nh = 0;
   const int t = blockIdx.x * kRouterChunk + threadIdx.x / LPT;
   const bool tok_ok = t < a.T;  // uniform across the quad
@@ -418,24 +420,24 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
   if (blocks <= 0) return 0;
   if (a.E <= 64 && a.K <= 16) {
     if (a.E <= 32 && a.K <= 8)
-      router_quad_kernel<8, 4, 8><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+      launch_pdl(router_quad_kernel<8, 4, 8>, dim3(blocks), dim3(kRouterChunk * 4), smem, stream, a);
     else if (a.E <= 32)
-      router_quad_kernel<8, 4, 16><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+      launch_pdl(router_quad_kernel<8, 4, 16>, dim3(blocks), dim3(kRouterChunk * 4), smem, stream, a);
     else if (a.K <= 8)
-      router_quad_kernel<16, 4, 8><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+      launch_pdl(router_quad_kernel<16, 4, 8>, dim3(blocks), dim3(kRouterChunk * 4), smem, stream, a);
     else
-      router_quad_kernel<16, 4, 16><<<blocks, kRouterChunk * 4, smem, stream>>>(a);
+      launch_pdl(router_quad_kernel<16, 4, 16>, dim3(blocks), dim3(kRouterChunk * 4), smem, stream, a);
     return cudaGetLastError() == cudaSuccess ? 0 : -2;
   }
   const int epl = (a.E + 31) / 32;
   if (epl <= 1)
-    router_kernel<1><<<blocks, kRouterChunk * 32, smem, stream>>>(a);
+    launch_pdl(router_kernel<1>, dim3(blocks), dim3(kRouterChunk * 32), smem, stream, a);
   else if (epl <= 2)
-    router_kernel<2><<<blocks, kRouterChunk * 32, smem, stream>>>(a);
+    launch_pdl(router_kernel<2>, dim3(blocks), dim3(kRouterChunk * 32), smem, stream, a);
   else if (epl <= 4)
-    router_kernel<4><<<blocks, kRouterChunk * 32, smem, stream>>>(a);
+    launch_pdl(router_kernel<4>, dim3(blocks), dim3(kRouterChunk * 32), smem, stream, a);
   else
-    router_kernel<8><<<blocks, kRouterChunk * 32, smem, stream>>>(a);
+    launch_pdl(router_kernel<8>, dim3(blocks), dim3(kRouterChunk * 32), smem, stream, a);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

@@ -285,8 +285,10 @@ class Context:
 
     STAGES = ("gate", "router", "permute_plan", "gather", "gemm1", "gemm2", "combine")
 
-    def set_profiling(self, on: bool):
-        _chk(lib().dsmoe_b200_ctx_set_profiling(self.h, int(on)))
+    def set_profiling(self, on: bool, every: int = 1):
+        """Per-stage CUDA events on every `every`-th forward (the others run
+        without events, so their kernels keep their launch overlap)."""
+        _chk(lib().dsmoe_b200_ctx_set_profiling(self.h, (max(1, int(every)) if on else 0)))
 
     def profile(self) -> dict:
         """Summed per-stage device milliseconds (CUDA events) since profiling
