@@ -537,7 +537,7 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
                  const PolicyResolved& pol, int logits_mode, const float* logits_in, float* logits_out,
                  const dsmoe_b200_routing* out, uint8_t* frac_ws) {
   cudaStream_t s = C->stream;
-  cuda_check(cudaMemsetAsync(C->counters.p, 0, 4 * sizeof(unsigned long long), s), "memset");
+  bool counters_zeroed = false;  // the tensor-core gate kernel zeroes them in its prologue
   const float* lg = logits_in;
   int ld = L->E;
   C->mark(0);
@@ -567,8 +567,10 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
       const CUtensorMap mx = make_map(x, T, L->d, L->d, kTileM);
       launch_check(launch_gemm_tc(0, &mx, &mx, &L->map_gate, C->tiles_gate.as<GemmTile>(),
                                   C->scalars.as<int>() + 3, (T + kTileM - 1) / kTileM, C->logits.p, L->Epad,
-                                  nullptr, L->Epad, num_sms(), s),
+                                  nullptr, L->Epad, num_sms(), s, nullptr, nullptr, 0, nullptr, 0,
+                                  C->counters.as<unsigned long long>()),
                    "gate gemm");
+      counters_zeroed = true;
       ld = L->Epad;
     } else {
       launch_check(launch_gate_logits_exact(x, L->dtype == DSMOE_B200_BF16, L->gate_exact.as<float>(),
@@ -585,6 +587,8 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
     cuda_check(cudaMemcpy2DAsync(logits_out, L->E * 4, lg, ld * 4, L->E * 4, T, cudaMemcpyDeviceToDevice, s),
                "logits copy");
   }
+  if (!counters_zeroed)
+    cuda_check(cudaMemsetAsync(C->counters.p, 0, 4 * sizeof(unsigned long long), s), "memset");
   C->mark(1);
   RouterArgs a{};
   a.logits = lg;

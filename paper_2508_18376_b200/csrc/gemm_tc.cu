@@ -120,6 +120,7 @@ struct GemmArgs {
   long long gather_ld;
   int flags;               // DSMOE_B200_GEMM_FLAGS: bit 0 B loads evict-first (fused gather), bit 1 no TMA stores
   int tma_store;           // bf16 outputs leave through mapO
+  unsigned long long* zero4;  // gate: the router's 4 counters, zeroed here (saves a memset between launches)
 };
 
 // swish(g) = g * sigmoid(g) = 0.5 g (1 + tanh(g / 2)): one MUFU op (tanh.approx,
@@ -276,6 +277,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // the predecessor's outputs (tile lists, A rows) are complete from here on
   const int ntiles = *args.num_tiles;
+  if ((MODE == kEpiF32 || MODE == kEpiF32Wide) && args.zero4 && blockIdx.x == 0 && threadIdx.x < 4) args.zero4[threadIdx.x] = 0ull;
   // "operand ready": own barrier (single CTA) / the leader's (pair)
   auto ready_arrive = [&](uint64_t* bar) {
     if constexpr (PAIR)
@@ -630,13 +632,15 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    const CUtensorMap* mapB, const GemmTile* tiles, const int* num_tiles,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
                    int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token,
-                   const void* gather_src, long long gather_ld, const CUtensorMap* mapO, int pair) {
+                   const void* gather_src, long long gather_ld, const CUtensorMap* mapO, int pair,
+                   unsigned long long* zero4) {
   static const int flags = [] {
     const char* v = std::getenv("DSMOE_B200_GEMM_FLAGS");
     return v ? std::atoi(v) : 0;
   }();
   GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128), row_token,
-             gather_src, gather_ld, flags, mapO != nullptr && mode != kEpiF32 && mode != kEpiF32Wide && !(flags & 2) ? 1 : 0};
+             gather_src, gather_ld, flags, mapO != nullptr && mode != kEpiF32 && mode != kEpiF32Wide && !(flags & 2) ? 1 : 0,
+             zero4};
   // gate logits with more than 64 output columns need the wide B slots
   if (mode == kEpiF32 && b_box_rows > 64) mode = kEpiF32Wide;
   const CUtensorMap* mo = mapO ? mapO : mapB;
