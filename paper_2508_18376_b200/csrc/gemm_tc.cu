@@ -376,14 +376,19 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
           mbar_wait(&emptyA[gw], phase ^ 1);
           if (gather) {
             const char* src = X + kb * 128 + ch * 16;
+            // rows past the segment end are not loaded: their accumulator rows
+            // are never stored, and fetching a placeholder token for each of
+            // them would hammer one L2 line (small segments: most of the tile)
+            const int nrow = tl.m_valid - row_off;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int row = 4 * i + rr;
               const long long tk = __shfl_sync(0xffffffffu, tok[i >> 3], 4 * (i & 7) + rr);
               const uint32_t dst = sa + row * 128 + ((ch ^ (row & 7)) << 4);
-              asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst),
-                           "l"(src + tk * args.gather_ld), "l"(pol)
-                           : "memory");
+              if (row < nrow)
+                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst),
+                             "l"(src + tk * args.gather_ld), "l"(pol)
+                             : "memory");
             }
             asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
             if constexpr (PAIR && !DSB_PAIR_RELAXED)  // the leader's MMA reads this CTA's smem
