@@ -32,13 +32,12 @@ constexpr int kMaxEPL = 8;    // experts per lane (E <= 256)
 // glibc expf (expf_glibc.h) with the 2^(i/32) table staged in shared memory:
 // lanes index it divergently, which serialises in the constant cache.
 __device__ __forceinline__ float expf_tab(float x, const uint64_t* tab) {
-  const uint32_t abstop = (__float_as_uint(x) >> 20) & 0x7ff;
-  if (abstop >= 0x42b) {
-    if (__float_as_uint(x) == 0xff800000u) return 0.0f;
-    if (abstop >= 0x7f8) return x + x;
-    if (x > 0x1.62e42ep6f) return __uint_as_float(0x7f800000u);
-    if (x < -0x1.9fe368p6f) return 0.0f;
-  }
+  // glibc's main path, computed unconditionally; its special-case exits
+  // (|x| >= 88, inf, nan) become selects, so independent calls carry no
+  // branches and the compiler can interleave them (one call alone is ~200
+  // cycles of dependent FP64 latency)
+  const uint32_t ux = __float_as_uint(x);
+  const uint32_t abstop = (ux >> 20) & 0x7ff;
   const double InvLn2N = 0x1.71547652b82fep+5, SHIFT = 0x1.8p+52;
   const double C0 = 0x1.c6af84b912394p-20, C1 = 0x1.ebfce50fac4f3p-13, C2 = 0x1.62e42ff0c52d6p-6;
   const double xd = static_cast<double>(x);
@@ -48,7 +47,14 @@ __device__ __forceinline__ float expf_tab(float x, const uint64_t* tab) {
   const double r = __fma_rn(InvLn2N, xd, -kd);
   const double s = __longlong_as_double(static_cast<long long>(tab[ki % 32] + (ki << 47)));
   const double y = __fma_rn(__fma_rn(C0, r, C1), __dmul_rn(r, r), __fma_rn(C2, r, 1.0));
-  return static_cast<float>(__dmul_rn(y, s));
+  float res = static_cast<float>(__dmul_rn(y, s));
+  // glibc's exits for abstop >= top12(88): none of these conditions holds
+  // below that, so they apply unconditionally (selects, no branch)
+  res = x < -0x1.9fe368p6f ? 0.0f : res;
+  res = x > 0x1.62e42ep6f ? __uint_as_float(0x7f800000u) : res;
+  res = abstop >= 0x7f8 ? x + x : res;
+  res = ux == 0xff800000u ? 0.0f : res;
+  return res;
 }
 
 template <int EPL>  // experts per lane, E <= 32 * EPL
