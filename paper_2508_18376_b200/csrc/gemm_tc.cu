@@ -141,6 +141,11 @@ __device__ __forceinline__ float silu_fast(float g) {
 // and owns the bulk group), so the epilogue has no CTA-wide barriers; rows cut
 // by the segment end are copied out masked.
 constexpr int kBoxCols = DSB_STAGE_OUT == 2 ? 32 : 64;
+// half-M pair tiles for segment tails (<= 128 rows); needs the 32-column boxes
+#ifndef DSB_HALF_M
+#define DSB_HALF_M 1
+#endif
+constexpr bool kHalfM = DSB_HALF_M != 0 && kBoxCols == 32;
 constexpr int kRowBytes = kBoxCols * 2;
 constexpr int kWarpSlot = 32 * kRowBytes;
 
@@ -233,7 +238,14 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   const bool leader = rank == 0;
   const int t0 = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
   const int gs = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
-  const int row_off = 128 * rank;
+  // CTA pair, tiles of <= 128 rows (segment tails): tcgen05.mma M = 128
+  // (cta_group::2), each CTA contributes 64 A rows; D lands in each CTA's TMEM
+  // as 64 rows x N with N columns [0, N/2) in lanes 0-63 and [N/2, N) in lanes
+  // 64-127, both at columns [0, N/2) (probed: tools/micro/pair_m128_probe.cu).
+  // Half the MMA time of an M = 256 tile that carries the same rows.
+  // (N a multiple of 128, so each lane half holds whole 64-column groups)
+  auto half_m = [&](const GemmTile& t) { return PAIR && kHalfM && t.m_valid <= 128 && (t.n_mma & 127) == 0; };
+  auto row_off_of = [&](const GemmTile& t) { return half_m(t) ? 64 * rank : 128 * rank; };
 
   const bool fused = MODE == kEpiSwiGLU && kGatherWarps > 0 && args.gather_src != nullptr;
   if (threadIdx.x == 0) {
@@ -318,7 +330,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
         for (int kb = 0; kb < tl.nkb; ++kb) {
           if (!fused) {
             mbar_wait(&emptyA[sa], pa ^ 1);
-            load_op(ringA + sa * kABytes, ma, &fullA[sa], kb * kTileK, tl.a_row + row_off, kABytes);
+            load_op(ringA + sa * kABytes, ma, &fullA[sa], kb * kTileK, tl.a_row + row_off_of(tl), kABytes);
             if (++sa == kAStages) { sa = 0; pa ^= 1; }
           }
           mbar_wait(&emptyB[sb], pb ^ 1);
@@ -352,10 +364,11 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       // i+1 are in flight while tile i's k-blocks are gathered
       auto load_tok = [&](const GemmTile& tl, int* tok) {
         if ((tl.m_live & kTileGatherA) == 0) return;
-        const int* rt = args.row_token + tl.a_row;  // this CTA's rows start at row_off
+        const int* rt = args.row_token + tl.a_row;  // this CTA's rows start at row_off_of(tl)
+        const int ro = row_off_of(tl);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int i = row_off + lane + 32 * j;
+          const int i = ro + lane + 32 * j;
           tok[j] = rt[i < tl.m_valid ? i : 0];
         }
       };
@@ -379,7 +392,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
             // rows past the segment end are not loaded: their accumulator rows
             // are never stored, and fetching a placeholder token for each of
             // them would hammer one L2 line (small segments: most of the tile)
-            const int nrow = tl.m_valid - row_off;
+            const int nrow = min(tl.m_valid - row_off_of(tl), half_m(tl) ? 64 : 128);
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int row = 4 * i + rr;
@@ -403,7 +416,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
                 ready_arrive(&fullA[gw]);
             }
           } else if (lane == 0) {
-            load_op(sa_ptr, ma, &fullA[gw], kb * kTileK, tl.a_row + row_off, kABytes, true);
+            load_op(sa_ptr, ma, &fullA[gw], kb * kTileK, tl.a_row + row_off_of(tl), kABytes, true);
           }
           __syncwarp();
           phase ^= 1;
@@ -429,7 +442,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     for (int t = t0; t < ntiles && leader; t += gs) {
       const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
       if (t + gs < ntiles) nxt = args.tiles[t + gs];
-      const uint32_t idesc = idesc_bf16(PAIR ? 2 * kTileM : kTileM, tl.n_mma);
+      const uint32_t idesc = idesc_bf16(PAIR ? (half_m(tl) ? kTileM : 2 * kTileM) : kTileM, tl.n_mma);
       const uint32_t dtmem = tmem_base + acc * kAccCols;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -478,7 +491,10 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     // chunks interleaved between them
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = (warp - kEpiWarp0) >> 2;
-    const int r = q * 32 + lane;
+    // rows of this warp within its CTA's rows of a tile: M = 256 pair / single
+    // tiles: lane quarter q holds rows [32q, 32q + 32); half-M pair tiles: 64
+    // rows per CTA, quarters q and q + 2 hold the same rows (other N half)
+    auto row_base = [&](const GemmTile& t) { return half_m(t) ? 32 * (q & 1) : 32 * q; };
     uint8_t* wslot = stage_buf + (warp - kEpiWarp0) * kWarpSlot;  // this warp's staging slot
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -500,19 +516,26 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     };
     GemmTile nxt = t0 < ntiles ? args.tiles[t0] : GemmTile{};
     float sc_nxt = 0.f;  // kEpiScale: this thread's row score, loaded a tile ahead
-    if (MODE == kEpiScale && t0 < ntiles && row_off + r < nxt.m_valid)
-      sc_nxt = args.row_scale[nxt.out_row + row_off + r];
+    auto load_score = [&](const GemmTile& t) {
+      const int rr = row_off_of(t) + row_base(t) + lane;
+      return rr < t.m_valid ? args.row_scale[t.out_row + rr] : 0.f;
+    };
+    if (MODE == kEpiScale && t0 < ntiles) sc_nxt = load_score(nxt);
     for (int t = t0; t < ntiles; t += gs) {
       GemmTile tl = nxt;  // descriptor prefetched one tile ahead
       const float sc_cur = sc_nxt;
       if (t + gs < ntiles) {
         nxt = args.tiles[t + gs];
-        if (MODE == kEpiScale && row_off + r < nxt.m_valid) sc_nxt = args.row_scale[nxt.out_row + row_off + r];
+        if (MODE == kEpiScale) sc_nxt = load_score(nxt);
       }
-      if constexpr (PAIR) {  // this CTA's half of the 256-row tile
-        tl.out_row += row_off;
-        tl.m_valid -= row_off;
-        const int live = (tl.m_live & 0xFFFFF) - row_off;
+      const bool hm = half_m(tl);
+      const int rb = row_base(tl);
+      const int r = rb + lane;
+      if constexpr (PAIR) {  // this CTA's rows of the pair tile
+        const int ro = row_off_of(tl);
+        tl.out_row += ro;
+        tl.m_valid -= ro;
+        const int live = (tl.m_live & 0xFFFFF) - ro;
         tl.m_live = (tl.m_live & ~0xFFFFF) | (live > 0 ? live : 0);
       }
       (void)sc_cur;
@@ -528,80 +551,90 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       const uint32_t taddr = tmem_base + acc * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
       const bool valid = r < tl.m_valid;
       const long long orow = static_cast<long long>(tl.out_row + r);
-      // this warp's rows [32q, 32q + 32) of the tile: all inside the segment ->
-      // one TMA store per 64-column box; cut by the segment end -> masked copy
-      const bool rows_full = 32 * q + 32 <= tl.m_valid;
+      // this warp's 32 rows: all inside the segment -> TMA stores; cut by the
+      // segment end -> masked copy
+      const bool rows_full = rb + 32 <= tl.m_valid;
       if constexpr (MODE == kEpiSwiGLU) {
-        // h = swish(g) * u over columns [64 half, 64 half + 64) of the nc-wide output
+        // h = swish(g) * u; a 32-neuron group = 64 accumulator columns [g | u].
+        // M = 256 / single: groups 2 half, 2 half + 1 at TMEM columns 128 half
+        // + 64 gi.  Half-M: lane half q >> 1 holds groups [(q >> 1) G, +G),
+        // G = N / 128, at TMEM columns 64 j; this warp takes j = half.
         const int nc = tl.n_mma >> 1;
         const bool live = r < (tl.m_live & 0xFFFFF);
-        const int c0 = 64 * half;  // output columns of this warp: groups 2 half, 2 half + 1
-        if (c0 < nc) {
-          if (kStageOut && kBoxCols == 64) warp_slot_acquire(lane);
+        const int c0 = 64 * half;
+        if (kStageOut && kBoxCols == 64 && c0 < nc) warp_slot_acquire(lane);
 #pragma unroll
-          for (int gi = 0; gi < 2; ++gi) {
-            if (kStageOut && kBoxCols == 32) warp_slot_acquire(lane);
-            uint32_t v[64];  // [g of 32 neurons | u of the same 32]
-            tmem_ld64(taddr + 2 * c0 + 64 * gi, v);
-            tmem_ld_wait();
-            uint32_t pk[16];
+        for (int gi = 0; gi < 2; ++gi) {
+          if (hm && gi == 1) break;
+          const int tcol = hm ? 64 * half : 2 * c0 + 64 * gi;
+          const int ocol = hm ? (64 * half < (tl.n_mma >> 1) ? 32 * ((q >> 1) * (tl.n_mma >> 7) + half) : nc)
+                              : c0 + 32 * gi;
+          if (ocol >= nc) continue;
+          if (kStageOut && kBoxCols == 32) warp_slot_acquire(lane);
+          uint32_t v[64];  // [g of 32 neurons | u of the same 32]
+          tmem_ld64(taddr + tcol, v);
+          tmem_ld_wait();
+          uint32_t pk[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float h0 = 0.f, h1 = 0.f;
-              if (live) {
-                h0 = silu_fast(__uint_as_float(v[2 * i])) * __uint_as_float(v[32 + 2 * i]);
-                h1 = silu_fast(__uint_as_float(v[2 * i + 1])) * __uint_as_float(v[32 + 2 * i + 1]);
-              }
-              pk[i] = pack_bf16x2(h0, h1);
+          for (int i = 0; i < 16; ++i) {
+            float h0 = 0.f, h1 = 0.f;
+            if (live) {
+              h0 = silu_fast(__uint_as_float(v[2 * i])) * __uint_as_float(v[32 + 2 * i]);
+              h1 = silu_fast(__uint_as_float(v[2 * i + 1])) * __uint_as_float(v[32 + 2 * i + 1]);
             }
-            if (kStageOut && kBoxCols == 32) {
-              warp_put(wslot, lane, 0, pk);
-              warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c0 + 32 * gi, tl.m_valid - 32 * q,
-                         rows_full, lane);
-            } else if (kStageOut)
-              warp_put(wslot, lane, 32 * gi, pk);
-            else if (valid)
-              row_put(args, orow, tl.out_col + c0 + 32 * gi, pk);
+            pk[i] = pack_bf16x2(h0, h1);
           }
+          if (kStageOut && kBoxCols == 32) {
+            warp_put(wslot, lane, 0, pk);
+            warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + ocol, tl.m_valid - rb, rows_full, lane);
+          } else if (kStageOut)
+            warp_put(wslot, lane, 32 * gi, pk);
+          else if (valid)
+            row_put(args, orow, tl.out_col + ocol, pk);
         }
         release_acc(acc);
         if (kStageOut && kBoxCols == 64 && c0 < nc)
-          warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c0, tl.m_valid - 32 * q, rows_full, lane);
+          warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + c0, tl.m_valid - rb, rows_full, lane);
       } else if constexpr (MODE == kEpiScale) {
-        // y = acc * raw score -> bf16; pass p = columns [128p + 64 half, +64),
-        // one x64 TMEM load each.  The row's score was loaded a tile ahead.
+        // y = acc * raw score -> bf16, 64 output columns per x64 TMEM load.
+        // M = 256 / single: columns 128 p + 64 half (p = 0, 1) at the same
+        // TMEM column.  Half-M: column (q >> 1) N/2 + 64 half at TMEM column
+        // 64 half (when 64 half < N/2).  The row's score was loaded a tile ahead.
         const float sc = valid ? sc_cur : 0.f;
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-          const int c = 128 * p + 64 * half;
-          const bool have = c < tl.n_mma;
+          const bool last = hm || p == 1;
+          const int c = hm ? (q >> 1) * (tl.n_mma >> 1) + 64 * half : 128 * p + 64 * half;
+          const int tcol = hm ? 64 * half : c;
+          const bool have = hm ? 64 * half < (tl.n_mma >> 1) : c < tl.n_mma;
           uint32_t pk[32];
           if (have) {
             uint32_t v[64];
-            tmem_ld64(taddr + c, v);
+            tmem_ld64(taddr + tcol, v);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]) * sc, __uint_as_float(v[2 * i + 1]) * sc);
           }
-          if (p == 1) release_acc(acc);
+          if (last) release_acc(acc);
           if (have && kStageOut && kBoxCols == 64) {
             warp_slot_acquire(lane);
             warp_put(wslot, lane, 0, pk);
             warp_put(wslot, lane, 32, pk + 16);
-            warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c, tl.m_valid - 32 * q, rows_full, lane);
+            warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + c, tl.m_valid - rb, rows_full, lane);
           } else if (have && kStageOut) {
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               warp_slot_acquire(lane);
               warp_put(wslot, lane, 0, pk + 16 * hh);
-              warp_store(wslot, &mapO, args, tl.out_row + 32 * q, tl.out_col + c + 32 * hh, tl.m_valid - 32 * q,
-                         rows_full, lane);
+              warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + c + 32 * hh, tl.m_valid - rb, rows_full,
+                         lane);
             }
           } else if (have && valid) {
             row_put(args, orow, tl.out_col + c, pk);
             row_put(args, orow, tl.out_col + c + 32, pk + 16);
           }
+          if (last) break;
         }
       } else {
         float* O = static_cast<float*>(args.out) + orow * args.ldo + tl.out_col;

@@ -16,12 +16,16 @@ for tg in (0.0, 0.25, 0.5):
     pol, rate = bench.calibrate(ctx, layer, x, tg)
     seg, R, _ = D.dispatch(ctx, layer, x, pol)
     nf, nt = seg[:, 1].astype(np.int64), seg[:, 2].astype(np.int64)
-    c = lambda n: (n + 127) // 128
-    # GEMM1: 4 chunks of major (all rows) + 4 of minor (full rows); GEMM2: K major or full per m-tile
-    g1_issued = (c(nt) * 4 + c(nf) * 4) * 128
-    g1_useful = nt * 4 + nf * 4
-    g2_issued = sum((c(nt[u]) * 512 + min(c(nf[u]), c(nt[u])) * 512) * 128 for u in range(len(nt)))
-    g2_useful = int((nt * 512 + nf * 512).sum())
-    print(json.dumps({"target": tg, "drop": rate, "rows": int(R), "full_rows": int(nf.sum()),
-                      "g1_waste": 1 - g1_useful.sum() / g1_issued.sum(), "g2_waste": 1 - g2_useful / g2_issued,
-                      "min_tot": int(nt.min()), "max_tot": int(nt.max()), "min_full": int(nf.min()), "max_full": int(nf.max())}))
+    nm = nt - nf  # major-only rows
+    out = {"target": tg, "drop": rate, "rows": int(R), "full_rows": int(nf.sum())}
+    for M in (128, 256):  # single-CTA tiles / CTA-pair tiles
+        c = lambda n: (n + M - 1) // M
+        # GEMM1: 4 chunks over all rows (major half) + 4 over the full rows (minor half)
+        g1_issued = ((c(nt) + c(nf)) * 4 * M).sum()
+        g1_useful = ((nt + nf) * 4).sum()
+        # GEMM2: full-row tiles run K = 1024, major-only tiles K = 512 (separate tiles)
+        g2_issued = ((c(nf) * 1024 + c(nm) * 512) * M).sum()
+        g2_useful = (nf * 1024 + nm * 512).sum()
+        out[f"g1_waste_m{M}"] = float(1 - g1_useful / g1_issued)
+        out[f"g2_waste_m{M}"] = float(1 - g2_useful / g2_issued)
+    print(json.dumps(out))
