@@ -78,6 +78,7 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
   const int tm = a.tile_m ? a.tile_m : kTileM;     // GEMM1 rows per tile: 128 (single CTA) or 256 (CTA pair)
   const int tm2 = a.tile_m2 ? a.tile_m2 : tm;      // GEMM2 rows per tile
   const int ntd = cdiv(a.d, kTileN2);
+  const bool unified = tm2 <= tm && tm % tm2 == 0;
   auto unit_of = [&](int u) { return u < a.num_routed ? (a.seg_unit ? a.seg_unit[u] : u) : a.shared_unit0 + (u - a.num_routed); };
   auto seg_of = [&](int u) {
     if (u < a.num_routed) return seg[u];
@@ -92,9 +93,13 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     int c1 = 0;
     for (int p = 0; p < ui.nsub; ++p) c1 += cdiv(ui.sub_wpad[p], kChunk) * (p == 0 ? mt_all : mt_full);
     off1[u] = c1;
-    // GEMM2: the full rows and the major-only rows tile separately, so a tile
-    // never mixes K = full width with K = major width
-    off2[u] = (cdiv(sg.n_full, tm2) + cdiv(sg.n_tot - sg.n_full, tm2)) * ntd;
+    // GEMM2 (unified, tm2 <= tm): tiles over all rows; a tile holding any
+    // full row runs K = full width — its major-only rows read minor-sub-block H
+    // that GEMM1's straddling minor tile wrote as zeros (rows in [live,
+    // m_valid) of a GEMM1 tile store 0, and GEMM1 tiles of tm rows contain the
+    // GEMM2 tile).  Otherwise the full rows and the major-only rows tile
+    // separately (two tails per unit instead of one).
+    off2[u] = (unified ? cdiv(sg.n_tot, tm2) : cdiv(sg.n_full, tm2) + cdiv(sg.n_tot - sg.n_full, tm2)) * ntd;
   }
   __syncthreads();
   const int tot1 = block_excl_scan(off1, nu);
@@ -163,8 +168,8 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     const int mt = li / ntd, nt = li - mt * ntd;
     const int mt_f = cdiv(sg.n_full, tm2);
     const bool full = mt < mt_f;
-    const int row0 = full ? mt * tm2 : sg.n_full + (mt - mt_f) * tm2;
-    const int m_valid = min(tm2, (full ? sg.n_full : sg.n_tot) - row0);
+    const int row0 = (full || unified) ? mt * tm2 : sg.n_full + (mt - mt_f) * tm2;
+    const int m_valid = min(tm2, ((full && !unified) ? sg.n_full : sg.n_tot) - row0);
     GemmTile tl;
     tl.a_row = sg.start + row0;
     tl.b_row = ui.w2t_row + nt * kTileN2;
