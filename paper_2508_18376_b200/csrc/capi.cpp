@@ -326,7 +326,7 @@ struct dsmoe_b200_ctx {
   // EP with one row per (token, rank): last ep_pack's layout on this context
   DevBuf ep_pos_td, ep_send_token, ep_cnt, ep_tot, ep_owner, ep_base;
   int ep_N = 0, ep_T = -1;
-  int gate_tiles_T = -1, gate_tiles_Epad = -1, gate_tiles_d = -1;
+  int gate_tiles_T = -1, gate_tiles_Epad = -1, gate_tiles_d = -1, gate_tiles_S = -1;
   // logits left in `logits` by the last routing on this context (LOGITS_REUSE)
   const void* logits_layer = nullptr;
   int logits_T = -1, logits_ld = 0;
@@ -540,6 +540,8 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   bool counters_zeroed = false;  // the tensor-core gate kernel zeroes them in its prologue
   const float* lg = logits_in;
   int ld = L->E;
+  int nsplit = 1;               // split-K gate: partial logit planes the router sums
+  long long split_stride = 0;
   C->mark(0);
   if (!lg && logits_mode == DSMOE_B200_LOGITS_REUSE) {
     require(C->logits_layer == L && C->logits_T == T, DSMOE_E_INVALID_STATE,
@@ -550,23 +552,48 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   if (!lg) {
     const bool tc = logits_mode == DSMOE_B200_LOGITS_TENSOR && L->dtype == DSMOE_B200_BF16;
     if (tc) {
-      if (C->gate_tiles_T != T || C->gate_tiles_Epad != L->Epad || C->gate_tiles_d != L->d) {
-        const int nt = (T + kTileM - 1) / kTileM;
-        std::vector<GemmTile> tl(static_cast<size_t>(nt));
-        for (int m = 0; m < nt; ++m)
-          tl[m] = GemmTile{m * kTileM, 0, m * kTileM, 0, L->d / kTileK, L->Epad, std::min(kTileM, T - m * kTileM), 0};
-        C->tiles_gate.ensure(sizeof(GemmTile) * (nt + 1) + 16);
-        cuda_check(cudaMemcpyAsync(C->tiles_gate.p, tl.data(), sizeof(GemmTile) * nt, cudaMemcpyHostToDevice, s), "H2D");
+      // Few 128-token tiles (small batches) leave most SMs idle and each tile
+      // streams its K serially: split K over up to 8 CTAs per tile; the
+      // router sums the partial planes in ascending order and writes the
+      // logits back (DSMOE_B200_GATE_SPLIT=1 disables).
+      const int nt = (T + kTileM - 1) / kTileM;
+      const int nkb = L->d / kTileK;
+      static const int split_max = [] {
+        const char* v = std::getenv("DSMOE_B200_GATE_SPLIT");
+        return v ? std::max(1, std::atoi(v)) : 8;
+      }();
+      int S = (L->E <= 64 && L->K <= 16) ? std::min({split_max, num_sms() / nt, nkb / 2}) : 1;
+      if (S < 2) S = 1;
+      const long long Tp = static_cast<long long>(nt) * kTileM;
+      if (C->gate_tiles_T != T || C->gate_tiles_Epad != L->Epad || C->gate_tiles_d != L->d ||
+          C->gate_tiles_S != S) {
+        std::vector<GemmTile> tl;
+        for (int sp = 0; sp < S; ++sp) {
+          const int kb0 = sp * nkb / S, kb1 = (sp + 1) * nkb / S;
+          for (int m = 0; m < nt; ++m)
+            tl.push_back(GemmTile{m * kTileM, 0, static_cast<int>(sp * Tp) + m * kTileM, 0, kb1 - kb0, L->Epad,
+                                  std::min(kTileM, T - m * kTileM), kb0});
+        }
+        const int ntiles = static_cast<int>(tl.size());
+        C->tiles_gate.ensure(sizeof(GemmTile) * (ntiles + 1) + 16);
+        cuda_check(cudaMemcpyAsync(C->tiles_gate.p, tl.data(), sizeof(GemmTile) * ntiles, cudaMemcpyHostToDevice, s),
+                   "H2D");
         int* ng = C->scalars.as<int>() + 3;
-        cuda_check(cudaMemcpyAsync(ng, &nt, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+        cuda_check(cudaMemcpyAsync(ng, &ntiles, sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
         cuda_check(cudaStreamSynchronize(s), "sync");
         C->gate_tiles_T = T;
         C->gate_tiles_Epad = L->Epad;
         C->gate_tiles_d = L->d;
+        C->gate_tiles_S = S;
+      }
+      C->logits.ensure(static_cast<size_t>(S * Tp) * L->Epad * 4 + 16);
+      if (S > 1) {
+        nsplit = S;
+        split_stride = Tp * L->Epad;
       }
       const CUtensorMap mx = make_map(x, T, L->d, L->d, kTileM);
       launch_check(launch_gemm_tc(0, &mx, &mx, &L->map_gate, C->tiles_gate.as<GemmTile>(),
-                                  C->scalars.as<int>() + 3, (T + kTileM - 1) / kTileM, C->logits.p, L->Epad,
+                                  C->scalars.as<int>() + 3, S * nt, C->logits.p, L->Epad,
                                   nullptr, L->Epad, num_sms(), s, nullptr, nullptr, 0, nullptr, 0,
                                   C->counters.as<unsigned long long>()),
                    "gate gemm");
@@ -582,10 +609,6 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
     C->logits_layer = L;
     C->logits_T = T;
     C->logits_ld = ld;
-  }
-  if (logits_out && logits_out != lg) {
-    cuda_check(cudaMemcpy2DAsync(logits_out, L->E * 4, lg, ld * 4, L->E * 4, T, cudaMemcpyDeviceToDevice, s),
-               "logits copy");
   }
   if (!counters_zeroed)
     cuda_check(cudaMemsetAsync(C->counters.p, 0, 4 * sizeof(unsigned long long), s), "memset");
@@ -616,8 +639,16 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   a.sel_raw = C->sel_raw.as<float>();
   a.cnt_chunk = C->cnt_chunk.as<int>();
   a.counters = C->counters.as<unsigned long long>();
+  a.nsplit = nsplit;
+  a.split_stride = split_stride;
+  a.logits_sum = nsplit > 1 ? C->logits.as<float>() : nullptr;
   launch_check(launch_router(a, s), "router");
   ++g_launches;
+  // after the router: with a split-K gate the summed logits exist only now
+  if (logits_out && logits_out != lg) {
+    cuda_check(cudaMemcpy2DAsync(logits_out, L->E * 4, lg, ld * 4, L->E * 4, T, cudaMemcpyDeviceToDevice, s),
+               "logits copy");
+  }
 }
 
 // K2a: chunk scan + unit segments (+ GEMM work lists) + ordered scatter

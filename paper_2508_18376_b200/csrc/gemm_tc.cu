@@ -327,10 +327,12 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
         const bool alt = (tl.m_live & kTileAltA) != 0;
         const void* ma = alt ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
         const int brow = tl.b_row + (PAIR ? rank * (tl.n_mma >> 1) : 0);
+        // gate tiles of a split-K launch: K blocks [kb0, kb0 + nkb) (m_live low bits)
+        const int kb0 = (MODE == kEpiF32 || MODE == kEpiF32Wide) ? (tl.m_live & 0xFFFFF) : 0;
         for (int kb = 0; kb < tl.nkb; ++kb) {
           if (!fused) {
             mbar_wait(&emptyA[sa], pa ^ 1);
-            load_op(ringA + sa * kABytes, ma, &fullA[sa], kb * kTileK, tl.a_row + row_off_of(tl), kABytes);
+            load_op(ringA + sa * kABytes, ma, &fullA[sa], (kb0 + kb) * kTileK, tl.a_row + row_off_of(tl), kABytes);
             if (++sa == kAStages) { sa = 0; pa ^= 1; }
           }
           mbar_wait(&emptyB[sb], pb ^ 1);
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
             mbar_expect_tx(&fullB[sb], args.b_bytes);
             tma_load_2d_hint(ringB + sb * kBSlot, &mapB, &fullB[sb], kb * kTileK, brow, pol_b);
           } else {
-            load_op(ringB + sb * kBSlot, &mapB, &fullB[sb], kb * kTileK, brow, args.b_bytes);
+            load_op(ringB + sb * kBSlot, &mapB, &fullB[sb], (kb0 + kb) * kTileK, brow, args.b_bytes);
           }
           if (++sb == kBStages) { sb = 0; pb ^= 1; }
         }

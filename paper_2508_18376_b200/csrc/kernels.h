@@ -12,6 +12,9 @@ namespace dsb {
 struct RouterArgs {
   const float* logits;
   int ld_logits;
+  int nsplit;               // > 1: logits = sum of nsplit partial planes (split-K gate), ascending
+  long long split_stride;   // elements between planes
+  float* logits_sum;        // nsplit > 1: the summed logits are written back here (plane 0)
   int T, E, K, P;
   int kind;
   double t_major, t_minor;

@@ -266,6 +266,30 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
   float v[EPT];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) v[i] = (tok_ok && e0 + i < E) ? row[e0 + i] : -INFINITY;
+  if (a.nsplit > 1) {  // split-K gate: partial planes summed in ascending order, written back
+    for (int sp0 = 1; sp0 < a.nsplit; sp0 += 4) {  // 4 planes' loads in flight, then the ordered adds
+      float w[4][EPT];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float* rs = row + (sp0 + j) * a.split_stride;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) w[j][i] = (sp0 + j < a.nsplit && tok_ok && e0 + i < E) ? rs[e0 + i] : 0.0f;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (sp0 + j < a.nsplit) {
+#pragma unroll
+          for (int i = 0; i < EPT; ++i)
+            if (e0 + i < E) v[i] = __fadd_rn(v[i], w[j][i]);
+        }
+    }
+    if (tok_ok) {
+      float* w = a.logits_sum + static_cast<long long>(t) * a.ld_logits;
+#pragma unroll
+      for (int i = 0; i < EPT; ++i)
+        if (e0 + i < E) w[e0 + i] = v[i];
+    }
+  }
   // softmax_inplace (matrix.hpp:68-78): max (order-free), expf, ascending-e sum, divide
   float mx = v[0];
 #pragma unroll
@@ -424,6 +448,7 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
   const int blocks = (a.T + kRouterChunk - 1) / kRouterChunk;
   const size_t smem = static_cast<size_t>(2 * a.E) * sizeof(int);
   if (blocks <= 0) return 0;
+  if (a.nsplit > 1 && !(a.E <= 64 && a.K <= 16)) return -1;  // split planes: quad router only
   if (a.E <= 64 && a.K <= 16) {
     if (a.E <= 32 && a.K <= 8)
       launch_pdl(router_quad_kernel<8, 4, 8>, dim3(blocks), dim3(kRouterChunk * 4), smem, stream, a);
