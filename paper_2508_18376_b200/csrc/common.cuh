@@ -324,6 +324,20 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // CTAs exit, so they never co-reside with a running persistent GEMM.
 // DSMOE_B200_PDL=0 launches without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Early trigger for the small kernels whose successors can co-reside (gate ->
+// router -> permutation): the successor's launch overlaps this kernel's run.
+#ifndef DSB_PDL_TRIGGER
+#define DSB_PDL_TRIGGER 1
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+  if (DSB_PDL_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#ifndef DSB_PDL_TRIGGER_TAIL  // experiment: also trigger in GEMM2 (-> combine) and combine (-> next gate)
+#define DSB_PDL_TRIGGER_TAIL 0
+#endif
+__device__ __forceinline__ void pdl_trigger_tail() {
+  if (DSB_PDL_TRIGGER_TAIL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 inline bool pdl_enabled() {
   static const bool on = [] {

@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a
   const int ncode = 2 * a.E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   pdl_wait();
+  pdl_trigger();
   // ---- phase A: per-code exclusive scans over chunks (scan_codes_kernel)
   for (int c = blockIdx.x; c < ncode; c += gridDim.x) {
     if (threadIdx.x == 0) s_carry = 0;
@@ -564,6 +565,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const TY* __restrict__ y, 
   constexpr int V = 16 / sizeof(TY);  // elements per 16-byte vector
   const int nvec = d / V;
   pdl_wait();
+  pdl_trigger_tail();
   for (int t = blockIdx.x; t < T; t += gridDim.x) {
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
       float acc[V];

@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
   if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }
   __syncthreads();
   pdl_wait();
+  pdl_trigger();
   unsigned long long n1 = 0, nh = 0;
   const int t = blockIdx.x * kRouterChunk + threadIdx.x / LPT;
   const bool tok_ok = t < a.T;  // uniform across the quad
