@@ -290,6 +290,9 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   pdl_wait();  // the predecessor's outputs (tile lists, A rows) are complete from here on
   if (MODE == kEpiF32 || MODE == kEpiF32Wide) pdl_trigger();  // gate: the router may launch
   if (MODE == kEpiScale) pdl_trigger_tail();
+#ifdef DSB_PDL_TRIGGER_G1  // experiment: GEMM1 -> GEMM2 (GEMM2 CTAs take SMs as GEMM1 CTAs exit)
+  if (MODE == kEpiSwiGLU) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   const int ntiles = *args.num_tiles;
   if ((MODE == kEpiF32 || MODE == kEpiF32Wide) && args.zero4 && blockIdx.x == 0 && threadIdx.x < 4) args.zero4[threadIdx.x] = 0ull;
   // "operand ready": own barrier (single CTA) / the leader's (pair)
