@@ -604,6 +604,11 @@ def main():
             cpu = {"value": rate, "unit": "tokens/s", "cores": ncores, "kind": "reference",
                    "sample": f"{sample} tokens of the same layer shape (route_and_drop + moe_forward of "
                              f"/root/reference/proj compiled into oracle/_ref), {dt:.1f} s"}
+            # the reference is single-threaded: its own 1-core rate beside the sharded one
+            s1 = max(4, sample // 32)
+            rate1, dt1 = cpu_reference_rate(host, s1, 1)
+            cpu["single_core"] = {"value": rate1, "unit": "tokens/s", "cores": 1,
+                                  "sample": f"{s1} tokens, {dt1:.1f} s"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "tokens/s", "cores": ncores, "kind": "reference",
                    "sample": f"unavailable: {e}"}
