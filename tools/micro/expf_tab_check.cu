@@ -1,0 +1,32 @@
+// Exhaustive: the router's branch-free expf_tab (router.cu) vs dsb::glibc_expf
+// (expf_glibc.h, itself checked bit-exact against libm over every float by
+// tools/check_expf.sh) over all 2^32 float bit patterns, on the device.
+#include <cstdio>
+#include "../../paper_2508_18376_b200/csrc/router.cu"
+using namespace dsb;
+__global__ void check(unsigned long long* bad, unsigned* first) {
+  __shared__ uint64_t tab[32];
+  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+  __syncthreads();
+  unsigned long long nb = 0;
+  for (unsigned long long u = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; u <= 0xffffffffull;
+       u += (unsigned long long)gridDim.x * blockDim.x) {
+    const float x = __uint_as_float(static_cast<unsigned>(u));
+    const float a = expf_tab(x, tab), b = glibc_expf(x);
+    if (__float_as_uint(a) != __float_as_uint(b) && !(a != a && b != b)) {
+      ++nb;
+      atomicMin(first, static_cast<unsigned>(u));
+    }
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+int main() {
+  unsigned long long* bad; unsigned* first;
+  cudaMallocManaged(&bad, 8); cudaMallocManaged(&first, 4);
+  *bad = 0; *first = 0xffffffffu;
+  check<<<148 * 8, 256>>>(bad, first);
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("expf_tab vs glibc_expf over 2^32 floats: mismatches %llu first 0x%08x (%s)\n", *bad, *first,
+         cudaGetErrorString(e));
+  return *bad != 0;
+}
