@@ -15,7 +15,8 @@ namespace dsb {
 // FMA-contracted form the x86-64 IFUNC selects on FMA hosts.  Table entry i is
 // asuint64(2^(i/32)) - (i << 47), generated to correct rounding by
 // tools/gen_exp2f_table.py; verified bit-exact against libm expf over every
-// float by tests/test_expf.py (CPU, host build of this same function).
+// float by tools/check_expf.sh (CPU, host build of this same function; sampled in
+// tests/test_capi_cpu.py).
 // ----------------------------------------------------------------------------
 #ifdef __CUDACC__
 #define DSB_HD __host__ __device__ __forceinline__

@@ -1,7 +1,7 @@
 """The router's branch-free glibc expf (router.cu expf_tab) equals
 dsb::glibc_expf on every one of the 2^32 float inputs, on the device
 (glibc_expf itself is checked against this host's libm over every float by
-tests/test_expf.py / tools/check_expf.sh)."""
+tests/test_capi_cpu.py::test_host_expf_matches_libm_sampled, exhaustively by tools/check_expf.sh)."""
 import os
 import subprocess
 
