@@ -145,7 +145,7 @@ constexpr int kBoxCols = DSB_STAGE_OUT == 2 ? 32 : 64;
 #ifndef DSB_HALF_M
 #define DSB_HALF_M 1
 #endif
-constexpr bool kHalfM = DSB_HALF_M != 0 && kBoxCols == 32;
+constexpr bool kHalfM = DSB_HALF_M != 0 && (kBoxCols == 32 || DSB_STAGE_OUT == 0);
 constexpr int kRowBytes = kBoxCols * 2;
 constexpr int kWarpSlot = 32 * kRowBytes;
 
