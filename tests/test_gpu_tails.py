@@ -55,9 +55,11 @@ def test_tail_sizes(ffn):
     assert _case(ffn, 71 + ffn) < 1e-2
 
 
-@pytest.mark.parametrize("pair", ["0", "12"])
+@pytest.mark.parametrize("pair", ["0", "1", "2", "12"])
 def test_tail_sizes_cta_variants(pair):
-    """Same cases with single-CTA tiles ("0") and pairs on both GEMMs."""
+    """Same cases with single-CTA tiles ("0"), pairs on one GEMM ("1": GEMM2
+    tiles nest in GEMM1 tiles -> unified GEMM2 tiles; "2": they do not ->
+    full / major-only GEMM2 tiles) and pairs on both."""
     code = (f"import sys; sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r}); "
             "sys.path.insert(0, %r); import torch; torch.cuda.set_device(0); import test_gpu_tails as t; "
             "print('RES', max(t._case(f, 71 + f) for f in (256, 128)))" % os.path.dirname(os.path.abspath(__file__)))
