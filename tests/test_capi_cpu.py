@@ -47,6 +47,10 @@ def test_library_is_sm100a_code():
     assert "UTCHMMA" in sass, "no tcgen05.mma in the grouped GEMM"
     assert "UTMALDG" in sass, "no TMA loads"
     assert "LDTM" in sass, "no tcgen05.ld epilogue"
+    assert "UTCHMMA.2CTA" in sass and "UTMALDG.2D.2CTA" in sass, "no CTA-pair (cta_group::2) MMA / TMA"
+    assert "UTCBAR.2CTA.MULTICAST" in sass, "no multicast MMA commit to both CTAs of a pair"
+    assert "UTMASTG" in sass, "no TMA stores in the epilogue"
+    assert "PREEXIT" in sass, "no griddepcontrol.launch_dependents (PDL early trigger)"
 
 
 def test_version_and_errors():
