@@ -467,8 +467,22 @@ def main():
         for name, p_, aware in (("no_drop", D.DropPolicy(), False), ("uniform", pol, False), ("load_aware", pol, True)):
             ms = time_steps(lambda: m.forward(x, p_, load_aware=aware, stats=False), args.steps, args.warmup, dist)
             res[name] = ms / args.steps
+        l0 = D.total_launch_count()
         _, rep = m.forward(x, pol, load_aware=True)
+        launches_per_step = D.total_launch_count() - l0
         ms_step = res["load_aware"]
+        # e2e through the public API with host buffers: per step the rank's
+        # tokens come H2D from pinned memory and its output goes back D2H
+        xh = x.cpu().pin_memory()
+        oh = torch.empty_like(xh).pin_memory()
+        xd = torch.empty_like(x)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            y, _ = m.forward(xd, pol, load_aware=True, stats=False)
+            oh.copy_(y, non_blocking=True)
+        n_e2e = max(5, args.steps // 2)
+        ms_e2e = time_steps(e2e_step, n_e2e, 2, dist) / n_e2e
         # skewed routing (acceptance.cpp:381-387: every token biased toward one
         # hot expert): where load-aware thresholds matter; t_max for load-aware
         # is the uniform t (the reference's comparison at equal t_max)
@@ -512,9 +526,11 @@ def main():
                               "modeled_speedup": rep_sk["speedup"]},
                 "comm_etp_vs_setp": comm_res,
                 "roofline": None, "cpu_baseline": None,
-                "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                        "note": "device-resident inputs under EP"},
-                "gpu_launches": None}))
+                "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+                        "h2d_bytes_per_step": xh.numel() * xh.element_size() * world,
+                        "d2h_bytes_per_step": oh.numel() * oh.element_size() * world,
+                        "mode": "per rank: H2D of its tokens, EP step (load-aware), D2H of its output"},
+                "gpu_launches": launches_per_step * args.steps, "gpu_launches_per_step": launches_per_step}))
         dist.destroy_process_group()
         return
 

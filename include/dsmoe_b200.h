@@ -128,6 +128,8 @@ const char* dsmoe_b200_version(void);
 const char* dsmoe_b200_last_error(void);
 /* number of kernels the last dsmoe_b200_forward / _moe_forward launched */
 int dsmoe_b200_last_launch_count(void);
+/* every kernel this library has launched in this process (all entry points) */
+long long dsmoe_b200_total_launch_count(void);
 
 /* ---- layers ------------------------------------------------------------ */
 int dsmoe_b200_layer_create(const dsmoe_b200_layer_config* cfg, dsmoe_b200_layer** out);

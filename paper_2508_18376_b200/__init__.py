@@ -7,6 +7,7 @@ torch.distributed (NCCL).
 """
 from .dsmoe import (  # noqa: F401
     DropPolicy, DsmoeError, MoeLayer, Context, RoutingDecision, route_and_drop, moe_forward, forward,
-    drop_stats, load_aware_thresholds, place_experts, lib, last_launch_count, LOGITS_TENSOR, LOGITS_EXACT,
+    drop_stats, load_aware_thresholds, place_experts, lib, last_launch_count, total_launch_count, LOGITS_TENSOR,
+    LOGITS_EXACT,
     profile_importance, reconstruct_experts, model_forward_dropped, dispatch, expert_ffn, combine,
 )

@@ -5,6 +5,7 @@
 // thread-local message, nothing thrown across the boundary.
 #include "../../include/dsmoe_b200.h"
 
+#include <atomic>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -44,6 +45,11 @@ void launch_check(int rc, const char* what) {
 
 thread_local std::string g_last_error;
 thread_local int g_launches = 0;
+std::atomic<long long> g_launches_total{0};  // every kernel this library launched, process-wide
+inline void count_launch(int n) {
+  g_launches += n;
+  g_launches_total.fetch_add(n, std::memory_order_relaxed);
+}
 
 template <class F>
 int guarded(F&& f) {
@@ -434,7 +440,7 @@ struct dsmoe_b200_ctx {
     if (L->S > 0 && scale_fill_key != key) {
       launch_check(launch_fill_f32(row_scale.as<float>() + Rcap, 1.0f, static_cast<long long>(L->S) * T, stream),
                    "fill");
-      ++g_launches;
+      count_launch(1);
       scale_fill_key = key;
     }
   }
@@ -604,7 +610,7 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
                                             C->logits.as<float>(), T, L->d, L->E, s),
                    "gate logits");
     }
-    ++g_launches;
+    count_launch(1);
     lg = C->logits.as<float>();
     C->logits_layer = L;
     C->logits_T = T;
@@ -643,7 +649,7 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   a.split_stride = split_stride;
   a.logits_sum = nsplit > 1 ? C->logits.as<float>() : nullptr;
   launch_check(launch_router(a, s), "router");
-  ++g_launches;
+  count_launch(1);
   // after the router: with a split-K gate the summed logits exist only now
   if (logits_out && logits_out != lg) {
     cuda_check(cudaMemcpy2DAsync(logits_out, L->E * 4, lg, ld * 4, L->E * 4, T, cudaMemcpyDeviceToDevice, s),
@@ -689,7 +695,7 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
                                       C->row_scale.as<float>(), C->slot_pos.as<int32_t>(), plan ? &pa : nullptr,
                                       num_sms(), s),
                  "permute");
-    g_launches += 1;
+    count_launch(1);
     return;
   }
   launch_check(launch_scan_plan(C->cnt_chunk.as<int>(), nchunks, L->E, C->chunk_off.as<int>(), C->code_base.as<int>(),
@@ -699,7 +705,7 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
                               C->code_base.as<int>(), C->row_token.as<int32_t>(), C->row_scale.as<float>(),
                               C->slot_pos.as<int32_t>(), s),
                "scatter");
-  g_launches += 3;
+  count_launch(3);
 }
 
 // K3 + K4 over the work lists at n1/n2: A = `rows` (permuted tokens, a_rows
@@ -760,7 +766,7 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
     C->mark(5);
     launch_check(launch_gemm_simt(2, g2, mt2, num_sms(), s), "gemm2 simt");
   }
-  g_launches += 2;
+  count_launch(2);
 }
 
 // ------------------------------------- stage: K2 permute/gather, K3, K4, K5
@@ -788,7 +794,7 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   C->mark(3);
   if (!fused_gather) {
     launch_check(launch_gather(x, C->xperm.p, C->row_token.as<int32_t>(), r_total, L->d * es, num_sms(), s), "gather");
-    g_launches += 1;
+    count_launch(1);
   }
   const long long rows = Rcap + static_cast<long long>(L->S) * T + kRowSlack;
   run_gemms(C, L, fused_gather ? x : C->xperm.p, fused_gather ? T : Rcap + kRowSlack, x, T, n1, n2, C->max_tiles1(L, T),
@@ -798,7 +804,7 @@ void stage_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int 
   launch_check(launch_combine(C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d, L->K,
                               routed_only ? 0 : L->S, static_cast<int>(Rcap), num_sms(), s, resid),
                "combine");
-  g_launches += 1;
+  count_launch(1);
 }
 
 void require_layer(const dsmoe_b200_layer* L) {
@@ -814,6 +820,7 @@ extern "C" {
 const char* dsmoe_b200_version(void) { return "dsmoe_b200 0.1 (sm_100a)"; }
 const char* dsmoe_b200_last_error(void) { return g_last_error.c_str(); }
 int dsmoe_b200_last_launch_count(void) { return g_launches; }
+long long dsmoe_b200_total_launch_count(void) { return g_launches_total.load(std::memory_order_relaxed); }
 
 int dsmoe_b200_layer_create(const dsmoe_b200_layer_config* cfg, dsmoe_b200_layer** out) {
   return guarded([&] {
@@ -1021,7 +1028,7 @@ int dsmoe_b200_moe_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
     a.cnt_chunk = C->cnt_chunk.as<int>();
     a.counters = C->counters.as<unsigned long long>();
     launch_check(launch_import_routing(a, s), "import routing");
-    ++g_launches;
+    count_launch(1);
     stage_ffn(C, L, x, T, out);
     check_flags(C);
   });
@@ -1088,7 +1095,7 @@ int dsmoe_b200_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void
     if (rows_out) {
       launch_check(launch_gather(x, rows_out, C->row_token.as<int32_t>(), r_total, L->d * esize(L->dtype), num_sms(), s),
                    "gather");
-      ++g_launches;
+      count_launch(1);
     }
     if (scale_out)
       cuda_check(cudaMemcpyAsync(scale_out, C->row_scale.p, sizeof(float) * static_cast<size_t>(T) * L->K,
@@ -1111,7 +1118,7 @@ int dsmoe_b200_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void
       pa.tiles2 = C->tiles2.as<GemmTile>();
       pa.n2 = r_total + 2;
       launch_check(launch_plan(pa, num_sms(), s), "plan shared");
-      ++g_launches;
+      count_launch(1);
       const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
       run_gemms(C, L, x, T, x, T, r_total + 1, r_total + 2, C->max_tiles1(L, T), C->max_tiles2(L, T), rows, C->Y.p,
                 C->row_scale.as<float>());
@@ -1193,7 +1200,7 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
     pa.tile_m = (pair & 1) ? 256 : kTileM;
     pa.tile_m2 = (pair & 2) ? 256 : kTileM;
     launch_check(launch_plan(pa, num_sms(), s), "plan");
-    ++g_launches;
+    count_launch(1);
     run_gemms(C, L, rows, nrows, nullptr, 0, nn + 1, nn + 2, max1, max2, h_rows, y_out, row_scale, nullptr, pair, nrows);
     // no host sync: the segment tables were staged by cudaMemcpyAsync from
     // pageable memory (copied before the call returns); rows / y_out are the
@@ -1216,7 +1223,7 @@ int dsmoe_b200_combine(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void*
     launch_check(launch_combine2(y_rows, C->Y.p, L->dtype == DSMOE_B200_BF16, C->slot_pos.as<int32_t>(), out, T, L->d,
                                  L->K, L->S, static_cast<int>(Rcap), num_sms(), C->stream),
                  "combine");
-    ++g_launches;
+    count_launch(1);
   });
 }
 
@@ -1248,10 +1255,11 @@ int dsmoe_b200_ep_pack(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void*
                                 nranks, cnt, cnt + nchunks * nranks, C->ep_tot.as<int>(), C->ep_send_token.as<int32_t>(),
                                 C->ep_pos_td.as<int32_t>(), rec_code, rec_row, rec_raw, r_total, num_sms(), s),
                  "ep_pack");
+    count_launch(1);
     launch_check(launch_gather(x, send_rows, C->ep_send_token.as<int32_t>(), r_total, L->d * esize(L->dtype),
                                num_sms(), s),
                  "ep gather");
-    g_launches += 2;
+    count_launch(2);
     std::vector<int> tot(static_cast<size_t>(2 * nranks));
     cuda_check(cudaMemcpyAsync(tot.data(), C->ep_tot.p, tot.size() * 4, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaStreamSynchronize(s), "sync");
@@ -1290,7 +1298,8 @@ int dsmoe_b200_ep_expert(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const voi
                                          C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), C->cnt_chunk.as<int>(),
                                          num_sms(), s),
                  "ep local routing");
-    ++g_launches;
+    count_launch(1);
+    count_launch(1);
     C->logits_T = -1;  // the routing codes on this context are no longer a gate routing
     stage_ffn(C, L, rows, Ti, out, nullptr, /*routed_only=*/true);
   });
@@ -1307,7 +1316,7 @@ int dsmoe_b200_ep_combine(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
     launch_check(launch_ep_final_combine(ret_rows, L->dtype == DSMOE_B200_BF16, C->ep_pos_td.as<int32_t>(), C->ep_N,
                                          C->Y.p, L->S, static_cast<int>(Rcap), out, T, L->d, num_sms(), C->stream),
                  "ep combine");
-    ++g_launches;
+    count_launch(1);
   });
 }
 
@@ -1338,7 +1347,7 @@ int dsmoe_b200_analyze_gating(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, cons
     launch_check(launch_gating_hist(di.as<int32_t>(), dr.as<float>(), dn.as<double>(), T, L->K, L->P, L->E, bins, a,
                                     a + L->E, a + L->E + bins, num_sms(), s),
                  "gating histogram");
-    ++g_launches;
+    count_launch(1);
     std::vector<unsigned long long> h(static_cast<size_t>(L->E + 2 * bins));
     cuda_check(cudaMemcpyAsync(h.data(), acc.p, acc.bytes, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaStreamSynchronize(s), "sync");
@@ -1447,7 +1456,9 @@ int dsmoe_b200_profile_importance(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, 
                                            seg[e].n_tot, L->w13.p, imp_unit(L, e), L->d, L->ffn, metric, v.as<double>(),
                                            s),
                    "importance");
+      count_launch(1);
     launch_check(launch_importance_reduce(v.as<double>(), C->seg.as<UnitSeg>(), L->E, L->ffn, values, s), "reduce");
+    count_launch(1);
     cuda_check(cudaStreamSynchronize(s), "sync");
   });
 }

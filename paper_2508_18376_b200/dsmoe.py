@@ -81,6 +81,7 @@ SYMBOLS = {
     "dsmoe_b200_version": (C.c_char_p, []),
     "dsmoe_b200_last_error": (C.c_char_p, []),
     "dsmoe_b200_last_launch_count": (C.c_int, []),
+    "dsmoe_b200_total_launch_count": (C.c_longlong, []),
     "dsmoe_b200_layer_create": (C.c_int, [C.POINTER(LayerConfig), C.POINTER(C.c_void_p)]),
     "dsmoe_b200_layer_free": (None, [C.c_void_p]),
     "dsmoe_b200_layer_set_gate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
@@ -154,6 +155,11 @@ def _chk(rc: int):
 
 def last_launch_count() -> int:
     return int(lib().dsmoe_b200_last_launch_count())
+
+
+def total_launch_count() -> int:
+    """Every kernel the library launched in this process (all entry points)."""
+    return int(lib().dsmoe_b200_total_launch_count())
 
 
 # ----------------------------------------------------------------- torch glue
