@@ -1,7 +1,8 @@
 """Every grouped-GEMM variant the library can select stays at parity with the
 oracle: CTA pairs for GEMM1 / GEMM2 / both / neither (DSMOE_B200_CTA_PAIR),
 the explicit X_perm gather instead of the fused one (DSMOE_B200_GATHER) and
-the split permutation (DSMOE_B200_PERMUTE).  The switches are read once per
+the split permutation (DSMOE_B200_PERMUTE), plain stream-ordered launches
+(DSMOE_B200_PDL=0) and the unsplit gate (DSMOE_B200_GATE_SPLIT=1).  The switches are read once per
 process, so each case runs in a fresh interpreter."""
 import json
 import os
@@ -44,6 +45,7 @@ print("RESULT", json.dumps(res))
     {"DSMOE_B200_CTA_PAIR": "2"},
     {"DSMOE_B200_CTA_PAIR": "12", "DSMOE_B200_GATHER": "explicit"},
     {"DSMOE_B200_CTA_PAIR": "0", "DSMOE_B200_GATHER": "explicit", "DSMOE_B200_PERMUTE": "split"},
+    {"DSMOE_B200_PDL": "0", "DSMOE_B200_GATE_SPLIT": "1"},
 ], ids=lambda e: ",".join(f"{k[11:]}={v}" for k, v in e.items()))
 def test_gemm_variant_parity(env):
     r = subprocess.run([sys.executable, "-c", CASE % {"root": ROOT}], env={**os.environ, **env},
