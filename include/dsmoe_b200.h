@@ -27,6 +27,8 @@
  *   dsmoe_b200_reconstruct      build_reconstruction_map + reconstruct_experts
  *                               (reconstruct.hpp:151, :196)
  *   dsmoe_b200_load_aware_thresholds  load_aware_thresholds (ep_sim.hpp:76)
+ *   dsmoe_b200_transform        complete_transform / partial_transform /
+ *                               reverse_partial (transform.hpp:66, :100, :136)
  */
 #ifndef DSMOE_B200_H
 #define DSMOE_B200_H
@@ -180,7 +182,11 @@ int dsmoe_b200_route(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const v
                      float* logits_out, const dsmoe_b200_routing* out,
                      dsmoe_b200_drop_stats_t* stats);
 /* moe_forward with a caller routing (device arrays, T x K*P): out (device,
- * T x d_model, layer dtype) = sum over kept slots of raw * block(x) + shared. */
+ * T x d_model, layer dtype) = sum over kept slots of raw * block(x) + shared.
+ * Any valid RoutingDecision (moe.hpp:142-167) is accepted: the canonical
+ * replayed layout runs on the fused path, anything else (any physical block
+ * and fraction per slot) on the layer's block view.  Index out of range or a
+ * fraction outside {0, 0.5, 1}: DSMOE_E_INVALID_STATE (moe.hpp:258-262). */
 int dsmoe_b200_moe_forward(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x,
                            int T, const int32_t* indices, const double* raw,
                            const double* fraction, void* out);
@@ -273,6 +279,29 @@ int dsmoe_b200_profile_importance(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* l
  * (major = first ceil(d_ffn/2) neurons of the order). */
 int dsmoe_b200_reconstruct(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const double* values,
                            int32_t* order, dsmoe_b200_layer** out);
+
+/* ---- partition API on the device (transform.hpp) ----------------------- */
+#define DSMOE_B200_TRANSFORM_COMPLETE 0 /* complete_transform (transform.hpp:66-95) */
+#define DSMOE_B200_TRANSFORM_PARTIAL 1  /* partial_transform (transform.hpp:100-131) */
+#define DSMOE_B200_TRANSFORM_REVERSE 2  /* reverse_partial (transform.hpp:136-170) */
+/* A new device layer re-grouped from `layer` without leaving the device:
+ * complete -> E*p experts of width d_ffn/p, gate columns repeated (copies of
+ * e at e*p..e*p+p-1), W2 scaled by p, top-K*p; partial -> replay_factor p,
+ * unscaled chunks, gate unchanged; reverse -> the sub-blocks concatenated
+ * back into P = 1 experts.  Errors as the reference (p >= 2, p | d_ffn,
+ * layer not already partitioned). */
+int dsmoe_b200_transform(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, int mode, int p,
+                         dsmoe_b200_layer** out);
+/* block widths (E*P entries) and shared-expert widths (S entries), host */
+int dsmoe_b200_layer_widths(const dsmoe_b200_layer* layer, int32_t* block_widths, int32_t* shared_widths);
+/* Read-back in the reference layout (moe.hpp:39-45, :75), layer dtype:
+ * gate d x E; block b: w1, w3 d x width, w2 width x d.  dst_on_device says
+ * whether the destinations are device or host pointers. */
+int dsmoe_b200_layer_get_gate(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, void* gate, int dst_on_device);
+int dsmoe_b200_layer_get_block(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, int block, void* w1, void* w3,
+                               void* w2, int dst_on_device);
+int dsmoe_b200_layer_get_shared(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, int s, void* w1, void* w3,
+                                void* w2, int dst_on_device);
 
 /* ---- expert parallelism policy (ep_sim.hpp) ----------------------------- */
 /* host arrays; same arithmetic as load_aware_thresholds (ep_sim.hpp:76-89) */

@@ -22,6 +22,7 @@
 
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "dsmoe/dropping.hpp"
@@ -64,6 +65,13 @@ class Context {
 // compute type: fp32 (bit-faithful weights) or bf16 (round to nearest even).
 template <std::floating_point T>
 class DeviceLayer {
+  // The device path computes in fp32 (or bf16).  A 64-bit layer — the
+  // reference's verification mode, whose gate matmul and softmax run in
+  // double — would be narrowed silently and could route differently on
+  // near-ties, so it is rejected at compile time.
+  static_assert(std::is_same_v<T, float>, "dsmoe::b200::DeviceLayer: the device path computes fp32/bf16; "
+                                          "64-bit (scalar_width 8) layers are not supported");
+
  public:
   DeviceLayer(const MoeLayer<T>& layer, bool bf16 = false, cudaStream_t s = nullptr)
       : config(layer.config), replay_factor(layer.replay_factor), bf16_(bf16) {

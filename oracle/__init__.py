@@ -310,9 +310,22 @@ def drop_stats(pre_frac, post_frac, P, S, T, d, ffn) -> dict:
     return dict(zip(keys, out.tolist()))
 
 
-def moe_forward(layer: Layer, x, idx, raw, frac) -> np.ndarray:
+def moe_forward(layer: Layer, x, idx, raw, frac, threads: int = 1) -> np.ndarray:
+    """moe_forward (moe.hpp:239-271).  threads > 1 shards the tokens into
+    contiguous blocks run concurrently (ctypes drops the GIL): the forward is
+    per-token separable (moe.hpp:253-269), so the result is bit-identical to
+    one call."""
     x = np.ascontiguousarray(x, np.float32)
     T, d = x.shape
+    if threads > 1 and T > 1:
+        import concurrent.futures as cf
+        idx2 = np.asarray(idx).reshape(T, -1)
+        raw2 = np.asarray(raw).reshape(T, -1)
+        frac2 = np.asarray(frac).reshape(T, -1)
+        parts = [p for p in np.array_split(np.arange(T), min(threads, T)) if p.size]
+        with cf.ThreadPoolExecutor(len(parts)) as ex:
+            outs = list(ex.map(lambda p: moe_forward(layer, x[p], idx2[p], raw2[p], frac2[p]), parts))
+        return np.concatenate(outs, axis=0)
     idx = np.ascontiguousarray(idx, np.int32)
     raw = np.ascontiguousarray(raw, np.float64)
     frac = np.ascontiguousarray(frac, np.float64)

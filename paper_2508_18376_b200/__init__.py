@@ -10,4 +10,5 @@ from .dsmoe import (  # noqa: F401
     drop_stats, load_aware_thresholds, place_experts, lib, last_launch_count, total_launch_count, LOGITS_TENSOR,
     LOGITS_EXACT,
     profile_importance, reconstruct_experts, model_forward_dropped, dispatch, expert_ffn, combine,
+    LOGITS_REUSE, transform, complete_transform, partial_transform, layer_weights,
 )

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -160,6 +161,12 @@ struct dsmoe_b200_layer {
   CUtensorMap map_w13_h{}, map_w2t_h{};  // 128-row boxes: half-N B tiles of the CTA-pair GEMM
   std::vector<char> block_set, shared_set;
   bool gate_set = false;
+  // lazily built "block view" of a P > 1 layer: every physical block its own
+  // unit, so a RoutingDecision outside the canonical replayed layout (any
+  // block, any fraction per slot, moe.hpp:239-271) runs on the same kernels
+  mutable dsmoe_b200_layer* bview = nullptr;
+  mutable std::mutex bview_mu;
+  ~dsmoe_b200_layer();
 
   int nunits() const { return E + S; }
   // sub-block p of routed unit e <- block (e, p) columns [col0, col0 + n)
@@ -171,6 +178,8 @@ struct dsmoe_b200_layer {
       require(shared_set[s], DSMOE_E_INVALID_STATE, "layer: shared expert " + std::to_string(s) + " not set");
   }
 };
+
+dsmoe_b200_layer::~dsmoe_b200_layer() { delete bview; }
 
 int pair_mask(const dsmoe_b200_layer* L) {
   // Which grouped GEMMs run on CTA pairs (tcgen05 cta_group::2, M = 256
@@ -189,7 +198,7 @@ int pair_mask(const dsmoe_b200_layer* L) {
 
 namespace {
 
-void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c) {
+void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool ragged = false) {
   require(c.d_model >= 1, DSMOE_E_INVALID_ARGUMENT, "config: d_model must be >= 1");
   require(c.d_ffn >= 2, DSMOE_E_INVALID_ARGUMENT, "config: d_ffn must be >= 2");
   require(c.num_experts >= 1, DSMOE_E_INVALID_ARGUMENT, "config: num_experts must be >= 1");
@@ -220,7 +229,7 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c) {
       require(L->widths[e * P + p] >= 1, DSMOE_E_SHAPE_MISMATCH, "layer: block widths must be >= 1");
       tot += L->widths[e * P + p];
     }
-    require(tot == L->ffn, DSMOE_E_INVALID_STATE,
+    require(ragged || tot == L->ffn, DSMOE_E_INVALID_STATE,
             "layer: block widths of expert " + std::to_string(e) + " sum to " + std::to_string(tot) +
                 ", expected " + std::to_string(L->ffn));
   }
@@ -321,6 +330,195 @@ void pack_sub(dsmoe_b200_layer* L, int u, int p, const void* w1, const void* w3,
                "pack_w2t");
 }
 
+// ------------------------------------------------ re-grouping (transform.cu)
+// Neuron n of a unit, counted over the concatenated true widths of its
+// sub-blocks -> (sub-block, index inside it).
+struct NeuronLoc {
+  int sub, i;
+};
+NeuronLoc neuron_loc(const UnitInfo& u, int n) {
+  for (int p = 0; p < u.nsub; ++p) {
+    if (n < u.sub_w[p]) return {p, n};
+    n -= u.sub_w[p];
+  }
+  fail(DSMOE_E_INTERNAL, "neuron_loc: neuron outside the unit");
+}
+long long sub_w13_base(const UnitInfo& u, int p) {
+  long long b = u.w13_row;
+  for (int q = 0; q < p; ++q) b += 2LL * u.sub_wpad[q];
+  return b;
+}
+int sub_hcol(const UnitInfo& u, int p) {
+  int h = 0;
+  for (int q = 0; q < p; ++q) h += u.sub_wpad[q];
+  return h;
+}
+
+template <class T>
+struct Staging {  // host vector -> device copy (freed after the stream syncs)
+  DevBuf buf;
+  T* put(const std::vector<T>& v, cudaStream_t s) {
+    buf.ensure(sizeof(T) * std::max<size_t>(1, v.size()));
+    if (!v.empty()) cuda_check(cudaMemcpyAsync(buf.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s), "H2D");
+    return buf.as<T>();
+  }
+};
+
+// Fill the packed weights of R from L: dst unit u' takes its neurons from src
+// unit src_unit[u'] through nmap(u', n') -> n (concatenated true-width
+// indices), W2 scaled by scale[u'].  gmap[e'] = src gate column of dst gate
+// column e' (the gate is re-grouped too: complete_transform repeats columns).
+template <class NMap>
+void regroup(const dsmoe_b200_layer* L, dsmoe_b200_layer* R, const std::vector<int>& src_unit,
+             const std::vector<float>& scale, NMap nmap, const std::vector<int>& gmap, cudaStream_t s) {
+  const int es = esize(L->dtype);
+  std::vector<long long> drow, srow;
+  std::vector<int> colmap(static_cast<size_t>(R->nunits()) * R->hstride, -1);
+  std::vector<ColUnit> cu;
+  for (int v = 0; v < R->nunits(); ++v) {
+    const UnitInfo& du = R->units[v];
+    const UnitInfo& su = L->units[src_unit[v]];
+    int off = 0;
+    for (int p = 0; p < du.nsub; ++p) {
+      const long long db = sub_w13_base(du, p);
+      const int dh = sub_hcol(du, p);
+      for (int i = 0; i < du.sub_wpad[p]; ++i) {
+        long long s1 = -1, s3 = -1;
+        if (i < du.sub_w[p]) {
+          const NeuronLoc sl = neuron_loc(su, nmap(v, off + i));
+          const long long sb = sub_w13_base(su, sl.sub);
+          s1 = w13_row_of(sb, sl.i, 0);
+          s3 = w13_row_of(sb, sl.i, 1);
+          colmap[static_cast<size_t>(v) * R->hstride + dh + i] = sub_hcol(su, sl.sub) + sl.i;
+        }
+        drow.push_back(w13_row_of(db, i, 0));
+        srow.push_back(s1);
+        drow.push_back(w13_row_of(db, i, 1));
+        srow.push_back(s3);
+      }
+      off += du.sub_w[p];
+    }
+    cu.push_back(ColUnit{du.w2t_row, su.w2t_row, v * R->hstride, R->hstride, scale[v], 0});
+  }
+  Staging<long long> sd, ss;
+  Staging<int> sc, sg;
+  Staging<ColUnit> su;
+  launch_check(launch_row_gather(L->w13.p, R->w13.p, sd.put(drow, s), ss.put(srow, s), static_cast<long long>(drow.size()),
+                                 static_cast<long long>(L->d) * es, num_sms(), s),
+               "regroup W13");
+  launch_check(launch_col_gather(L->dtype == DSMOE_B200_BF16, L->w2t.p, R->w2t.p, su.put(cu, s),
+                                 static_cast<int>(cu.size()), sc.put(colmap, s), L->d, L->hstride, R->hstride, s),
+               "regroup W2T");
+  // gate: gateT rows (Epad x d, layer dtype) and the exact-mode d x E fp32 copy
+  std::vector<long long> gd, gs;
+  for (int e = 0; e < R->Epad; ++e) {
+    gd.push_back(e);
+    gs.push_back(e < R->E ? gmap[e] : -1);
+  }
+  Staging<long long> sgd, sgs;
+  launch_check(launch_row_gather(L->gateT.p, R->gateT.p, sgd.put(gd, s), sgs.put(gs, s), R->Epad,
+                                 static_cast<long long>(L->d) * es, num_sms(), s),
+               "regroup gate");
+  std::vector<ColUnit> gu{ColUnit{0, 0, 0, R->E, 1.0f, 0}};
+  Staging<ColUnit> sgu;
+  launch_check(launch_col_gather(0, L->gate_exact.p, R->gate_exact.p, sgu.put(gu, s), 1, sg.put(gmap, s), L->d, L->E,
+                                 R->E, s),
+               "regroup exact gate");
+  count_launch(4);
+  cuda_check(cudaStreamSynchronize(s), "sync");
+  R->gate_set = L->gate_set;
+  std::fill(R->block_set.begin(), R->block_set.end(), 1);
+  std::fill(R->shared_set.begin(), R->shared_set.end(), 1);
+}
+
+constexpr int kModeComplete = 0, kModePartial = 1, kModeReverse = 2, kModeBlocks = 3;
+
+// complete_transform / partial_transform / reverse_partial (transform.hpp:66-170)
+// or the block view of a device layer, as a new device layer.
+dsmoe_b200_layer* transform_layer(const dsmoe_b200_layer* L, int mode, int p, cudaStream_t s) {
+  std::vector<int32_t> widths, swidths(L->swidths.begin(), L->swidths.end());
+  dsmoe_b200_layer_config cfg{L->d, L->ffn, L->E, L->K, L->S, L->prenorm, 1, L->dtype, nullptr, nullptr};
+  std::vector<int> src_unit, gmap;
+  std::vector<float> scale;
+  std::function<int(int, int)> nmap;
+  if (mode == kModeComplete || mode == kModePartial) {
+    const char* who = mode == kModeComplete ? "complete_transform" : "partial_transform";
+    require(L->P == 1, DSMOE_E_INVALID_STATE, std::string(who) + ": layer already carries a partial transformation");
+    require(p >= 2, DSMOE_E_INVALID_ARGUMENT, std::string(who) + ": p must be >= 2");
+    require(L->ffn % p == 0, DSMOE_E_INVALID_ARGUMENT,
+            std::string(who) + ": d_ffn " + std::to_string(L->ffn) + " not divisible by p " + std::to_string(p));
+  }
+  const int c = (mode == kModeComplete || mode == kModePartial) ? L->ffn / p : 0;
+  if (mode == kModeComplete) {
+    cfg.d_ffn = c;
+    cfg.num_experts = L->E * p;
+    cfg.top_k = L->K * p;
+    for (int e = 0; e < L->E * p; ++e) widths.push_back(c);
+    for (int e = 0; e < L->E; ++e)
+      for (int q = 0; q < p; ++q) {
+        src_unit.push_back(e);
+        scale.push_back(static_cast<float>(p));
+        gmap.push_back(e);
+      }
+    nmap = [c, p](int v, int n) { return (v % p) * c + n; };
+  } else if (mode == kModePartial) {
+    cfg.replay_factor = p;
+    for (int e = 0; e < L->E * p; ++e) widths.push_back(c);
+    for (int e = 0; e < L->E; ++e) {
+      src_unit.push_back(e);
+      scale.push_back(1.0f);
+      gmap.push_back(e);
+    }
+    nmap = [](int, int n) { return n; };
+  } else if (mode == kModeReverse) {
+    require(L->P > 1, DSMOE_E_INVALID_STATE, "reverse: layer does not carry a partial transformation");
+    for (int e = 0; e < L->E; ++e) {
+      widths.push_back(L->ffn);
+      src_unit.push_back(e);
+      scale.push_back(1.0f);
+      gmap.push_back(e);
+    }
+    nmap = [](int, int n) { return n; };
+  } else {  // block view: unit b = e*P + q <- sub-block q of unit e
+    const int P = L->P;
+    cfg.num_experts = L->E * P;
+    cfg.top_k = L->K * P;
+    cfg.d_ffn = *std::max_element(L->widths.begin(), L->widths.end());
+    for (int b = 0; b < L->E * P; ++b) {
+      widths.push_back(L->widths[b]);
+      src_unit.push_back(b / P);
+      scale.push_back(1.0f);
+      gmap.push_back(std::min(b / P, L->E - 1));
+    }
+    nmap = [L, P](int v, int n) {
+      const UnitInfo& u = L->units[v / P];
+      int off = 0;
+      for (int q = 0; q < v % P; ++q) off += u.sub_w[q];
+      return off + n;
+    };
+  }
+  for (int si = 0; si < L->S; ++si) {
+    src_unit.push_back(L->E + si);
+    scale.push_back(1.0f);
+  }
+  require(cfg.num_experts <= 256 && cfg.top_k <= 16, DSMOE_E_INVALID_ARGUMENT,
+          "transform: the result exceeds the device limits (256 experts, top_k 16)");
+  cfg.block_widths = widths.data();
+  cfg.shared_widths = swidths.empty() ? nullptr : swidths.data();
+  auto* R = new dsmoe_b200_layer;
+  try {
+    // block view: block widths need not sum to a common d_ffn (major / minor halves)
+    layer_build(R, cfg, /*ragged=*/mode == kModeBlocks);
+    const int nE = R->E;
+    auto full = [&](int v, int n) { return v < nE ? nmap(v, n) : n; };
+    regroup(L, R, src_unit, scale, full, gmap, s);
+  } catch (...) {
+    delete R;
+    throw;
+  }
+  return R;
+}
+
 }  // namespace
 
 // ====================================================================== ctx
@@ -417,7 +615,10 @@ struct dsmoe_b200_ctx {
     cnt_chunk.ensure(nchunks * 2 * L->E * 4 + 16);
     chunk_off.ensure(nchunks * 2 * L->E * 4 + 16);
     code_base.ensure(static_cast<size_t>(4 * L->E) * 4);  // [2E bases | 2E totals]
-    counters.ensure(4 * sizeof(unsigned long long));
+    if (!counters.p) {  // [0..3] per call (zeroed by each routing), [4] sticky error flags
+      counters.ensure(8 * sizeof(unsigned long long));
+      cuda_check(cudaMemsetAsync(counters.p, 0, counters.bytes, stream), "memset");
+    }
     row_token.ensure(static_cast<size_t>(Rcap + kRowSlack) * 4);
     seg.ensure(sizeof(UnitSeg) * L->E);
     scalars.ensure(4 * sizeof(int));  // r_total, n1, n2, ngate
@@ -526,16 +727,32 @@ void stats_from_counts(const dsmoe_b200_layer* L, int T, unsigned long long n1, 
   st->retained_flops = st->total_flops - st->saved_flops;
 }
 
-void check_flags(dsmoe_b200_ctx* C) {
-  unsigned long long h[4];
-  cuda_check(cudaMemcpyAsync(h, C->counters.p, sizeof(h), cudaMemcpyDeviceToHost, C->stream), "D2H");
-  cuda_check(cudaStreamSynchronize(C->stream), "sync");
-  const unsigned long long f = h[2] | C->last_err_flags;
-  C->last_err_flags = 0;
+// Error flags raised on the device.  counters[2] belongs to the last call;
+// counters[4] is sticky: a forward launched without stats (no host sync)
+// still reports its degenerate-normalisation error (normalize_topk throws,
+// dropping.hpp:67) at the next synchronising call on the context.
+void raise_flags(unsigned long long f) {
   if (f & 1ull) fail(DSMOE_E_INVALID_ARGUMENT, "normalize_topk: degenerate zero-sum scores");
   if (f & 4ull)
     fail(DSMOE_E_INVALID_STATE,
-         "moe_forward: routing is not in the canonical replayed layout the device path supports");
+         "moe_forward: routing has an expert index out of range or a compute fraction outside {0, 0.5, 1}");
+}
+
+// read counters[0..4] after the work queued so far (synchronises the stream);
+// sticky flags are cleared once reported
+void read_counters(dsmoe_b200_ctx* C, unsigned long long* h5) {
+  cuda_check(cudaMemcpyAsync(h5, C->counters.p, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, C->stream),
+             "D2H counters");
+  cuda_check(cudaStreamSynchronize(C->stream), "sync");
+  const unsigned long long f = h5[2] | h5[4] | C->last_err_flags;
+  C->last_err_flags = 0;
+  if (h5[4]) cuda_check(cudaMemsetAsync(C->counters.as<unsigned long long>() + 4, 0, 8, C->stream), "memset");
+  raise_flags(f);
+}
+
+void check_flags(dsmoe_b200_ctx* C) {
+  unsigned long long h[5];
+  read_counters(C, h);
 }
 
 // -------------------------------------------------- stage: gate logits + K1
@@ -558,17 +775,21 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   if (!lg) {
     const bool tc = logits_mode == DSMOE_B200_LOGITS_TENSOR && L->dtype == DSMOE_B200_BF16;
     if (tc) {
-      // Few 128-token tiles (small batches) leave most SMs idle and each tile
-      // streams its K serially: split K over up to 8 CTAs per tile; the
-      // router sums the partial planes in ascending order and writes the
-      // logits back (DSMOE_B200_GATE_SPLIT=1 disables).
+      // K may be split into S pieces over S CTAs per 128-token tile (partial
+      // fp32 logit planes the router sums in ascending order and writes
+      // back).  S depends on the layer only, never on T, so a token's logits
+      // — and its top-K / drop band on near-ties — do not change with the
+      // batch it rides in (EP ranks with different shard sizes route
+      // identical tokens identically).  Default S = 1: a second
+      // plane cost +10 us of gate + router at T = 16384 (r2 bench).
+      // DSMOE_B200_GATE_SPLIT=S selects a split (small-batch latency).
       const int nt = (T + kTileM - 1) / kTileM;
       const int nkb = L->d / kTileK;
-      static const int split_max = [] {
+      static const int split_env = [] {
         const char* v = std::getenv("DSMOE_B200_GATE_SPLIT");
-        return v ? std::max(1, std::atoi(v)) : 8;
+        return v ? std::max(1, std::atoi(v)) : 1;
       }();
-      int S = (L->E <= 64 && L->K <= 16) ? std::min({split_max, num_sms() / nt, nkb / 2}) : 1;
+      int S = (L->E <= 64 && L->K <= 16) ? std::min(split_env, std::max(1, nkb / 2)) : 1;
       if (S < 2) S = 1;
       const long long Tp = static_cast<long long>(nt) * kTileM;
       if (C->gate_tiles_T != T || C->gate_tiles_Epad != L->Epad || C->gate_tiles_d != L->d ||
@@ -987,10 +1208,8 @@ int dsmoe_b200_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x
     if (need_frac) C->frac_ws.ensure(static_cast<size_t>(T) * L->K * L->P);
     stage_route(C, L, x, T, pol, logits_mode, logits_in, logits_out, out, need_frac ? C->frac_ws.as<uint8_t>() : nullptr);
     if (stats) {
-      unsigned long long h[4];
-      cuda_check(cudaMemcpyAsync(h, C->counters.p, sizeof(h), cudaMemcpyDeviceToHost, C->stream), "D2H");
-      cuda_check(cudaStreamSynchronize(C->stream), "sync");
-      if (h[2] & 1ull) fail(DSMOE_E_INVALID_ARGUMENT, "normalize_topk: degenerate zero-sum scores");
+      unsigned long long h[5];
+      read_counters(C, h);
       std::vector<uint8_t> fh;
       if (!is_pow2(L->P)) {
         fh.resize(static_cast<size_t>(T) * L->K * L->P);
@@ -1029,7 +1248,39 @@ int dsmoe_b200_moe_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
     a.counters = C->counters.as<unsigned long long>();
     launch_check(launch_import_routing(a, s), "import routing");
     count_launch(1);
-    stage_ffn(C, L, x, T, out);
+    unsigned long long h[5];
+    cuda_check(cudaMemcpyAsync(h, C->counters.p, sizeof(h), cudaMemcpyDeviceToHost, s), "D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+    if (!(h[2] & 4ull) || L->P == 1) {
+      stage_ffn(C, L, x, T, out);
+      check_flags(C);
+      return;
+    }
+    // Not the canonical replayed layout (e.g. copies of one selection with
+    // different raw scores, a kept copy 1 without copy 0, fraction 0.5 on a
+    // split layer, duplicate blocks): evaluate every slot on its own physical
+    // block through the layer's block view — moe_forward's per-slot semantics
+    // (moe.hpp:253-266): block indices[f], its first ceil(w/2) neurons when
+    // fraction 0.5, weighted by raw.
+    const dsmoe_b200_layer* B = nullptr;
+    {
+      std::lock_guard<std::mutex> lock(L->bview_mu);
+      if (!L->bview) L->bview = transform_layer(L, kModeBlocks, 0, s);
+      B = L->bview;
+    }
+    C->ensure(B, T);
+    cuda_check(cudaMemsetAsync(C->counters.p, 0, 5 * sizeof(unsigned long long), s), "memset");
+    ImportArgs b = a;
+    b.K = B->K;
+    b.P = 1;
+    b.nphys = B->E;
+    b.nunits = B->E;
+    b.sel_code = C->sel_code.as<int32_t>();
+    b.sel_raw = C->sel_raw.as<float>();
+    b.cnt_chunk = C->cnt_chunk.as<int>();
+    launch_check(launch_import_routing(b, s), "import routing (block view)");
+    count_launch(1);
+    stage_ffn(C, B, x, T, out);
     check_flags(C);
   });
 }
@@ -1062,10 +1313,8 @@ int dsmoe_b200_forward_ex(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
     stage_ffn(C, L, x, T, out, (flags & DSMOE_B200_RESIDUAL) ? x : nullptr);
     C->prof_end();
     if (stats) {
-      unsigned long long h[4];
-      cuda_check(cudaMemcpyAsync(h, C->counters.p, sizeof(h), cudaMemcpyDeviceToHost, C->stream), "D2H");
-      cuda_check(cudaStreamSynchronize(C->stream), "sync");
-      if (h[2] & 1ull) fail(DSMOE_E_INVALID_ARGUMENT, "normalize_topk: degenerate zero-sum scores");
+      unsigned long long h[5];
+      read_counters(C, h);
       std::vector<uint8_t> fh;
       if (need_frac) {
         fh.resize(static_cast<size_t>(T) * L->K * L->P);
@@ -1124,11 +1373,9 @@ int dsmoe_b200_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void
                 C->row_scale.as<float>());
     }
     std::vector<UnitSeg> h(static_cast<size_t>(L->E));
-    unsigned long long cnt[4];
+    unsigned long long cnt[5];
     cuda_check(cudaMemcpyAsync(h.data(), C->seg.p, sizeof(UnitSeg) * L->E, cudaMemcpyDeviceToHost, s), "D2H");
-    cuda_check(cudaMemcpyAsync(cnt, C->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, s), "D2H");
-    cuda_check(cudaStreamSynchronize(s), "sync");
-    if (cnt[2] & 1ull) fail(DSMOE_E_INVALID_ARGUMENT, "normalize_topk: degenerate zero-sum scores");
+    read_counters(C, cnt);
     int R = 0;
     for (int e = 0; e < L->E; ++e) {
       if (seg_out) {
@@ -1350,7 +1597,8 @@ int dsmoe_b200_analyze_gating(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, cons
     count_launch(1);
     std::vector<unsigned long long> h(static_cast<size_t>(L->E + 2 * bins));
     cuda_check(cudaMemcpyAsync(h.data(), acc.p, acc.bytes, cudaMemcpyDeviceToHost, s), "D2H");
-    cuda_check(cudaStreamSynchronize(s), "sync");
+    unsigned long long cnt[5];
+    read_counters(C, cnt);  // normalize_topk on a zero-sum row throws (dropping.hpp:67)
     for (int e = 0; e < L->E; ++e) selection_counts[e] = static_cast<long long>(h[e]);
     for (int b = 0; b < bins; ++b) {
       raw_hist[b] = static_cast<long long>(h[L->E + b]);
@@ -1379,6 +1627,114 @@ int dsmoe_b200_drop_stats(const double* pre, const double* post, long n, int P, 
     st->total_flops = denom * unit;
     st->saved_flops = st->dropped_units * unit;
     st->retained_flops = st->total_flops - st->saved_flops;
+  });
+}
+
+int dsmoe_b200_transform(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int mode, int p, dsmoe_b200_layer** out) {
+  return guarded([&] {
+    require(C != nullptr && out != nullptr, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require_layer(L);
+    require(mode == kModeComplete || mode == kModePartial || mode == kModeReverse, DSMOE_E_INVALID_ARGUMENT,
+            "transform: mode must be complete, partial or reverse");
+    g_launches = 0;
+    *out = transform_layer(L, mode, p, C->stream);
+  });
+}
+
+int dsmoe_b200_layer_widths(const dsmoe_b200_layer* L, int32_t* block_widths, int32_t* shared_widths) {
+  return guarded([&] {
+    require(L != nullptr, DSMOE_E_INVALID_ARGUMENT, "null layer");
+    if (block_widths) std::copy(L->widths.begin(), L->widths.end(), block_widths);
+    if (shared_widths) std::copy(L->swidths.begin(), L->swidths.end(), shared_widths);
+  });
+}
+
+namespace {
+// host or device destination of a read-back
+struct Sink {
+  void* dst;
+  int on_device;
+  DevBuf tmp;
+  void* dev(size_t bytes) {
+    if (on_device) return dst;
+    tmp.ensure(bytes);
+    return tmp.p;
+  }
+  void finish(size_t bytes, cudaStream_t s) {
+    if (!on_device) cuda_check(cudaMemcpyAsync(dst, tmp.p, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+  }
+};
+
+// unit u (sub-blocks [p0, p1)) -> reference-layout w1, w3 (d x w), w2 (w x d)
+void read_unit(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int u, int p0, int p1, void* w1, void* w3, void* w2,
+               int on_device) {
+  cudaStream_t s = C->stream;
+  const UnitInfo& ui = L->units[u];
+  const int es = esize(L->dtype), bf = L->dtype == DSMOE_B200_BF16;
+  std::vector<long long> r1, r3;
+  for (int p = p0; p < p1; ++p) {
+    const long long b = sub_w13_base(ui, p);
+    for (int i = 0; i < ui.sub_w[p]; ++i) {
+      r1.push_back(w13_row_of(b, i, 0));
+      r3.push_back(w13_row_of(b, i, 1));
+    }
+  }
+  const int w = static_cast<int>(r1.size());
+  const size_t nb = static_cast<size_t>(w) * L->d * es;
+  Sink k1{w1, on_device}, k3{w3, on_device}, k2{w2, on_device};
+  Staging<long long> s1, s3;
+  launch_check(launch_transpose(bf, L->w13.p, L->d, s1.put(r1, s), 0, 0, w, L->d, k1.dev(nb), s), "read w1");
+  launch_check(launch_transpose(bf, L->w13.p, L->d, s3.put(r3, s), 0, 0, w, L->d, k3.dev(nb), s), "read w3");
+  char* o2 = static_cast<char*>(k2.dev(nb));
+  for (int p = p0; p < p1; ++p) {  // W2T columns of each sub-block -> w2 rows
+    launch_check(launch_transpose(bf, L->w2t.p, L->hstride, nullptr, ui.w2t_row, sub_hcol(ui, p), L->d, ui.sub_w[p],
+                                  o2, s),
+                 "read w2");
+    o2 += static_cast<size_t>(ui.sub_w[p]) * L->d * es;
+  }
+  count_launch(2 + (p1 - p0));
+  k1.finish(nb, s);
+  k3.finish(nb, s);
+  k2.finish(nb, s);
+  cuda_check(cudaStreamSynchronize(s), "sync");
+}
+}  // namespace
+
+int dsmoe_b200_layer_get_gate(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, void* gate, int dst_on_device) {
+  return guarded([&] {
+    require(C && L && gate, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(L->gate_set, DSMOE_E_INVALID_STATE, "layer: gate weights not set");
+    const size_t nb = static_cast<size_t>(L->d) * L->E * esize(L->dtype);
+    Sink k{gate, dst_on_device};
+    launch_check(launch_transpose(L->dtype == DSMOE_B200_BF16, L->gateT.p, L->d, nullptr, 0, 0, L->E, L->d,
+                                  k.dev(nb), C->stream),
+                 "read gate");
+    count_launch(1);
+    k.finish(nb, C->stream);
+    cuda_check(cudaStreamSynchronize(C->stream), "sync");
+  });
+}
+
+int dsmoe_b200_layer_get_block(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int b, void* w1, void* w3, void* w2,
+                               int dst_on_device) {
+  return guarded([&] {
+    require(C && L && w1 && w3 && w2, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(b >= 0 && b < L->E * L->P, DSMOE_E_INVALID_ARGUMENT, "block index out of range");
+    require(L->block_set[b], DSMOE_E_INVALID_STATE, "layer: expert block not set");
+    const int e = b / L->P;
+    if (L->P == 1)
+      read_unit(C, L, e, 0, L->units[e].nsub, w1, w3, w2, dst_on_device);  // both virtual halves
+    else
+      read_unit(C, L, e, b % L->P, b % L->P + 1, w1, w3, w2, dst_on_device);
+  });
+}
+
+int dsmoe_b200_layer_get_shared(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int si, void* w1, void* w3, void* w2,
+                                int dst_on_device) {
+  return guarded([&] {
+    require(C && L && w1 && w3 && w2, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(si >= 0 && si < L->S, DSMOE_E_INVALID_ARGUMENT, "shared expert index out of range");
+    read_unit(C, L, L->E + si, 0, 1, w1, w3, w2, dst_on_device);
   });
 }
 
@@ -1443,11 +1799,12 @@ int dsmoe_b200_profile_importance(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, 
     a.counters = C->counters.as<unsigned long long>();
     launch_check(launch_import_routing(a, s), "import routing");
     stage_permute(C, L, T, false);
-    unsigned long long flags[4];
+    unsigned long long flags[5];
     cuda_check(cudaMemcpyAsync(flags, C->counters.p, sizeof(flags), cudaMemcpyDeviceToHost, s), "D2H");
     std::vector<UnitSeg> seg(static_cast<size_t>(L->E));
     cuda_check(cudaMemcpyAsync(seg.data(), C->seg.p, sizeof(UnitSeg) * L->E, cudaMemcpyDeviceToHost, s), "D2H");
     cuda_check(cudaStreamSynchronize(s), "sync");
+    if (flags[4] & 4ull) cuda_check(cudaMemsetAsync(C->counters.as<unsigned long long>() + 4, 0, 8, s), "memset");
     require(!(flags[2] & 4ull), DSMOE_E_INVALID_STATE, "profile_importance: expert index out of range");
     DevBuf v;
     v.ensure(sizeof(double) * static_cast<size_t>(n) * L->ffn + 8);

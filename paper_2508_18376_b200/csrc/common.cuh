@@ -347,6 +347,17 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// Opt `func` into `bytes` of dynamic shared memory on the current device.
+// The attribute is per (function, device), so the largest size set so far is
+// tracked per device; callers pass the DYNAMIC size and the check against
+// the 48 KB default is left to the runtime (static + dynamic is what counts,
+// a permute kernel with 22.8 KB static smem).  Defined in pack.cu.
+cudaError_t set_max_dyn_smem(const void* func, size_t bytes);
+template <typename F>
+inline cudaError_t set_max_dyn_smem(F* func, size_t bytes) {
+  return set_max_dyn_smem(reinterpret_cast<const void*>(func), bytes);
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                               Args&&... args) {

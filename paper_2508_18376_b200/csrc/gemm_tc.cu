@@ -709,12 +709,7 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
     cfg.numAttrs = 2;
 #define DSB_LAUNCH_PAIR(M)                                                                         \
   {                                                                                                \
-    static bool attr = false;                                                                      \
-    if (!attr) {                                                                                   \
-      cudaFuncSetAttribute(gemm_tc_kernel<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                           Geo<M, true>::SMEM);                                                    \
-      attr = true;                                                                                 \
-    }                                                                                              \
+    set_max_dyn_smem(gemm_tc_kernel<M, true>, Geo<M, true>::SMEM);                                 \
     cfg.blockDim = dim3(Geo<M, true>::THREADS);                                                    \
     cfg.dynamicSmemBytes = Geo<M, true>::SMEM;                                                     \
     err = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<M, true>, *mapA, *mapA2, *mapB, *mo, a);         \
@@ -731,12 +726,7 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
   switch (mode) {
 #define DSB_LAUNCH(M)                                                                         \
   case M: {                                                                                   \
-    static bool attr = false;                                                                 \
-    if (!attr) {                                                                              \
-      cudaFuncSetAttribute(gemm_tc_kernel<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           Geo<M>::SMEM);                                                     \
-      attr = true;                                                                            \
-    }                                                                                         \
+    set_max_dyn_smem(gemm_tc_kernel<M, false>, Geo<M>::SMEM);                                 \
     err = launch_pdl(gemm_tc_kernel<M, false>, dim3(grid), dim3(Geo<M>::THREADS), Geo<M>::SMEM, stream, *mapA, \
                      *mapA2, *mapB, *mo, a);                                                  \
     if (err != cudaSuccess) return static_cast<int>(err);                                      \

@@ -28,7 +28,8 @@ struct RouterArgs {
   int32_t* sel_code;   // T x K : unit * 4 + level, -1 when dropped
   float* sel_raw;      // T x K
   int* cnt_chunk;      // ceil(T/128) x 2E histograms of (unit, level)
-  unsigned long long* counters;  // [0] copies with fraction 1, [1] fraction 0.5, [2] error flags
+  unsigned long long* counters;  // [0] copies with fraction 1, [1] fraction 0.5, [2] error flags of this call,
+                                 // [4] sticky error flags (cleared only when reported, dsmoe_b200_ctx_check)
 };
 struct ImportArgs {
   const int32_t* idx;
@@ -138,6 +139,20 @@ int launch_pack_w2t(int src_dt, int dst_dt, const void* w2, int d, const int* or
                     void* dst, long long drow, int hcol0, long long hstride, cudaStream_t s);
 int launch_pack_gate(int src_dt, int dst_dt, const void* gate, int d, int E, void* gateT, float* gate_exact,
                      cudaStream_t s);
+
+// transform.cu (re-grouping of the packed layout, read-back)
+struct ColUnit {
+  long long dst_row0, src_row0;
+  int map_off, ncols;
+  float scale;
+  int pad;
+};
+int launch_row_gather(const void* src, void* dst, const long long* dst_row, const long long* src_row, long long n,
+                      long long row_bytes, int num_sms, cudaStream_t s);
+int launch_col_gather(int bf16, const void* src, void* dst, const ColUnit* units, int nunits, const int* colmap,
+                      int rows, long long src_ld, long long dst_ld, cudaStream_t s);
+int launch_transpose(int bf16, const void* src, long long src_ld, const long long* rows, long long row0,
+                     long long col0, int R, int Ccount, void* out, cudaStream_t s);
 
 }  // namespace dsb
 

@@ -329,8 +329,7 @@ int launch_scatter(const int32_t* sel_code, const float* sel_raw, int T, int K, 
   const int nchunks = (T + kRouterChunk - 1) / kRouterChunk;
   const int threads = 1024;
   const size_t smem = static_cast<size_t>(2 * E) * (1 + threads / 32) * sizeof(int);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (set_max_dyn_smem(scatter_kernel, smem) != cudaSuccess) return -2;
   if (nchunks > 0)
     scatter_kernel<<<nchunks, threads, smem, stream>>>(sel_code, sel_raw, T, K, E, chunk_off, code_base, row_token,
                                                        row_scale, slot_pos);
@@ -492,11 +491,7 @@ int launch_permute_fused(const int* cnt_chunk, int nchunks, int E, int* chunk_of
                 row_token, row_scale, slot_pos, plan ? *plan : PlanArgs{}, plan != nullptr};
   const int threads = 1024;
   const size_t smem = static_cast<size_t>(2 * E) * (1 + 4 * (1 + 8)) * sizeof(int);
-  static size_t attr_set = 0;
-  if (smem > 32 * 1024 && smem > attr_set) {
-    cudaFuncSetAttribute(permute_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr_set = smem;
-  }
+  if (set_max_dyn_smem(permute_fused_kernel, smem) != cudaSuccess) return -2;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, permute_fused_kernel, threads, smem);
   if (per_sm < 1) return -3;

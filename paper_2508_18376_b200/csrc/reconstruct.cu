@@ -214,7 +214,7 @@ int launch_order_sort(const double* values, int E, int ffn, int32_t* order, cuda
   while (n < ffn) n <<= 1;
   const size_t smem = static_cast<size_t>(n) * (sizeof(double) + sizeof(int));
   if (smem > 200 * 1024) return -1;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(order_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (set_max_dyn_smem(order_sort_kernel, smem) != cudaSuccess) return -2;
   order_sort_kernel<<<E, 1024, smem, s>>>(values, ffn, n, order);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

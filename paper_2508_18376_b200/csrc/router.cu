@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kRouterChunk * 32) router_kernel(const RouterA
     double dsum = 0.0;
     if (a.normalize) {
       for (int s = 0; s < K; ++s) dsum = __dadd_rn(dsum, static_cast<double>(__shfl_sync(0xffffffffu, my_raw, s)));
-      if (!(dsum > 0.0) && lane == 0) atomicOr(&a.counters[2], 1ull);
+      if (!(dsum > 0.0) && lane == 0) { atomicOr(&a.counters[2], 1ull); atomicOr(&a.counters[4], 1ull); }
     }
     const double ns = active ? (a.normalize ? __ddiv_rn(static_cast<double>(my_raw), dsum) : static_cast<double>(my_raw))
                              : -1.0;
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
 #pragma unroll
     for (int j = 0; j < KK; ++j)
       if (j < K) dsum = __dadd_rn(dsum, static_cast<double>(sraw[j]));
-    if (tok_ok && q == 0 && !(dsum > 0.0)) atomicOr(&a.counters[2], 1ull);
+    if (tok_ok && q == 0 && !(dsum > 0.0)) { atomicOr(&a.counters[2], 1ull); atomicOr(&a.counters[4], 1ull); }
   }
   // this lane's slots j = q, q+LPT, ...; top_slot = first maximum of ns (dropping.hpp:99)
   constexpr int kSl = KK / LPT;
@@ -510,6 +510,7 @@ __global__ void __launch_bounds__(kRouterChunk) import_routing_kernel(const Impo
       }
       if (!ok) {
         atomicOr(&a.counters[2], 4ull);
+        atomicOr(&a.counters[4], 4ull);
         lv = 0;
       }
       const int unit = ok ? e0 / a.P : 0;

@@ -125,6 +125,13 @@ SYMBOLS = {
     "dsmoe_b200_reconstruct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.POINTER(C.c_void_p)]),
     "dsmoe_b200_load_aware_thresholds": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_void_p]),
+    "dsmoe_b200_transform": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "dsmoe_b200_layer_widths": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dsmoe_b200_layer_get_gate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
+    "dsmoe_b200_layer_get_block": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_int]),
+    "dsmoe_b200_layer_get_shared": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_int]),
 }
 
 
@@ -259,12 +266,23 @@ class MoeLayer:
                                                    C.c_void_p(a2[0]), a1[1], a1[2], st))
 
     @classmethod
-    def _wrap(cls, handle, like: "MoeLayer", P):
+    def _wrap(cls, handle, like: "MoeLayer", P=None):
+        """A Python handle for a layer the library created (transform,
+        reconstruct): the shape is read back from the library."""
         obj = cls.__new__(cls)
         obj.__dict__.update(like.__dict__)
         obj.h = handle
-        obj.P = P
+        info = (C.c_int32 * 8)()
+        _chk(lib().dsmoe_b200_layer_info(handle, info))
+        obj.d, obj.ffn, obj.E, obj.K, obj.S, obj.P = (int(v) for v in info[:6])
         return obj
+
+    def widths(self):
+        """(block widths E*P, shared widths S) as int lists."""
+        bw = (C.c_int32 * max(1, self.E * self.P))()
+        sw = (C.c_int32 * max(1, self.S))()
+        _chk(lib().dsmoe_b200_layer_widths(self.h, bw, sw))
+        return list(bw)[:self.E * self.P], list(sw)[:self.S]
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -517,7 +535,57 @@ def reconstruct_experts(ctx: Context, layer: MoeLayer, values):
     h = C.c_void_p()
     _chk(lib().dsmoe_b200_reconstruct(ctx.h, layer.h, C.c_void_p(values.data_ptr()), C.c_void_p(order.data_ptr()),
                                       C.byref(h)))
-    return MoeLayer._wrap(h, layer, 2), order
+    return MoeLayer._wrap(h, layer), order
+
+
+# ------------------------------------------------- partition API (K8b)
+TRANSFORM = {"complete": 0, "partial": 1, "reverse": 2}
+
+
+def transform(ctx: Context, layer: MoeLayer, mode: str, p: int = 0) -> MoeLayer:
+    """complete_transform / partial_transform (transform.hpp:66-131) or
+    reverse_partial (:136-170) of a device layer, re-grouped on the device;
+    returns the new MoeLayer (the source is unchanged)."""
+    if mode not in TRANSFORM:
+        raise DsmoeError(1, "mode must be complete, partial or reverse")
+    h = C.c_void_p()
+    _chk(lib().dsmoe_b200_transform(ctx.h, layer.h, TRANSFORM[mode], int(p), C.byref(h)))
+    return MoeLayer._wrap(h, layer)
+
+
+def complete_transform(ctx: Context, layer: MoeLayer, p: int) -> MoeLayer:
+    """complete_transform (transform.hpp:66-95)."""
+    return transform(ctx, layer, "complete", p)
+
+
+def partial_transform(ctx: Context, layer: MoeLayer, p: int) -> MoeLayer:
+    """partial_transform (transform.hpp:100-131); the PartitionSpec is
+    (factor p, partial, E, d_ffn, chunk d_ffn/p) and is implied by the layer."""
+    return transform(ctx, layer, "partial", p)
+
+
+def layer_weights(ctx: Context, layer: MoeLayer, device=True, blocks=None):
+    """The layer's weights in the reference layout (moe.hpp:39-45, :75), layer
+    dtype: (gate d x E, [(w1 d x w, w3 d x w, w2 w x d) per block], [shared]).
+    `blocks` (optional index list) reads only those blocks (None elsewhere)."""
+    torch = _torch()
+    dev = "cuda" if device else "cpu"
+    dt = layer.torch_dtype
+    bw, sw = layer.widths()
+    gate = torch.empty((layer.d, layer.E), dtype=dt, device=dev)
+    _chk(lib().dsmoe_b200_layer_get_gate(ctx.h, layer.h, C.c_void_p(gate.data_ptr()), int(device)))
+
+    def get(fn, i, w):
+        w1 = torch.empty((layer.d, w), dtype=dt, device=dev)
+        w3 = torch.empty_like(w1)
+        w2 = torch.empty((w, layer.d), dtype=dt, device=dev)
+        _chk(fn(ctx.h, layer.h, i, C.c_void_p(w1.data_ptr()), C.c_void_p(w3.data_ptr()), C.c_void_p(w2.data_ptr()),
+                int(device)))
+        return w1, w3, w2
+    want = set(range(len(bw))) if blocks is None else set(blocks)
+    out = [get(lib().dsmoe_b200_layer_get_block, b, w) if b in want else None for b, w in enumerate(bw)]
+    shared = [get(lib().dsmoe_b200_layer_get_shared, i, w) for i, w in enumerate(sw)]
+    return gate, out, shared
 
 
 # ------------------------------------------------ expert-parallel data path

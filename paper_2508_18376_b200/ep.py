@@ -37,30 +37,58 @@ from . import dsmoe as D
 
 
 # --------------------------------------------------------------- host policy
+def block_devices(num_experts: int, replay_factor: int, devices: int, strategy: str = "contiguous"):
+    """Placement::device_of (ep_sim.hpp:38-54): the device of every physical
+    block e*P + p."""
+    return D.place_experts(num_experts * replay_factor, devices, strategy)
+
+
 def owner_of_experts(num_experts: int, replay_factor: int, devices: int, strategy: str = "contiguous"):
-    """Device of each original expert = device of its copy-0 block, the owner
-    simulate_step thresholds by (ep_sim.hpp:139-141)."""
-    blocks = D.place_experts(num_experts * replay_factor, devices, strategy)
-    return blocks[np.arange(num_experts) * replay_factor]
+    """Device whose threshold an original expert's selections use = the device
+    of its copy-0 (whole or major) block (ep_sim.hpp:139-141)."""
+    return block_devices(num_experts, replay_factor, devices, strategy)[np.arange(num_experts) * replay_factor]
 
 
-def loads_from_counts(counts, owner, devices):
-    """device_loads (ep_sim.hpp:59-72) of a no-drop routing: every selection
-    contributes P copies x 1/P = exactly 1 unit, so the double sums are exact
-    integers and independent of summation order."""
+def expert_aligned(device_of, replay_factor: int) -> bool:
+    """True when every expert's P blocks sit on one device (the data path
+    then moves whole selections; contiguous placement with E*P/D a multiple
+    of P, ep_sim.hpp:48-52)."""
+    dv = np.asarray(device_of).reshape(-1, replay_factor)
+    return bool((dv == dv[:, :1]).all())
+
+
+def loads_from_counts(counts, device_of, devices, replay_factor: int = 1):
+    """device_loads (ep_sim.hpp:59-72) of a no-drop routing from per-expert
+    selection counts: each selection adds fraction/P = 1/P to the device of
+    each of its P blocks.  P is a power of two in every caller, so each
+    partial sum is an exact multiple of 1/P and the double sums do not
+    depend on their order.  `device_of` has E*P entries (block devices)."""
+    P = int(replay_factor)
+    dv = np.asarray(device_of).reshape(-1, P)
+    c = np.asarray(counts, np.float64)
     loads = np.zeros(devices, np.float64)
-    np.add.at(loads, np.asarray(owner), np.asarray(counts, np.float64))
+    for p in range(P):
+        np.add.at(loads, dv[:, p], c * (1.0 / P))
     return loads
 
 
-def post_loads_from_segments(seg_full, seg_major, owner, devices, replay_factor):
-    """device_loads of the dropped routing: a full selection keeps P copies
-    (1 unit), a major-only one copy 0 only (1/P unit) — exact for P a power
-    of two."""
-    w = 1.0 / replay_factor
-    per = np.asarray(seg_full, np.float64) + np.asarray(seg_major, np.float64) * w
+def post_loads_from_segments(seg_full, seg_major, device_of, devices, replay_factor):
+    """device_loads of the dropped routing from per-expert (full, major-only)
+    kept-selection counts: a full selection keeps every copy (1/P each), a
+    major-only one copy 0 only — fraction 1.0 at weight 1/P for P > 1, or
+    fraction 0.5 for P = 1 (dropping.hpp:105-116).  Exact for P a power of two."""
+    P = int(replay_factor)
+    dv = np.asarray(device_of).reshape(-1, P)
+    full = np.asarray(seg_full, np.float64)
+    maj = np.asarray(seg_major, np.float64)
     loads = np.zeros(devices, np.float64)
-    np.add.at(loads, np.asarray(owner), per)
+    if P == 1:
+        np.add.at(loads, dv[:, 0], full + 0.5 * maj)
+        return loads
+    w = 1.0 / P
+    np.add.at(loads, dv[:, 0], (full + maj) * w)
+    for p in range(1, P):
+        np.add.at(loads, dv[:, p], full * w)
     return loads
 
 
@@ -166,6 +194,10 @@ class ExpertParallelMoE:
         self.rank = dist.get_rank(group)
         if strategy != "contiguous":
             raise D.DsmoeError(1, "expert-parallel data path needs contiguous placement")
+        self.device_of = block_devices(layer.E, layer.P, self.world, strategy)
+        if not expert_aligned(self.device_of, layer.P):
+            raise D.DsmoeError(1, "expert-parallel data path: an expert's sub-blocks straddle two ranks "
+                                  "(contiguous placement needs E*P/world to be a multiple of P)")
         self.owner = owner_of_experts(layer.E, layer.P, self.world, strategy)
         self.local = np.nonzero(self.owner == self.rank)[0]
         self.ctx = D.Context()
@@ -187,7 +219,7 @@ class ExpertParallelMoE:
         # 1. global pre-drop loads -> thresholds (simulate_step, ep_sim.hpp:110-138)
         seg0, _, _ = D.dispatch(self.ctx, L, x, D.DropPolicy(), logits_mode=logits_mode)
         counts = self.coll.all_reduce(torch.from_numpy(seg0[:, 2].astype(np.int64)).to(dev))
-        pre = loads_from_counts(counts.cpu().numpy(), self.owner, W)
+        pre = loads_from_counts(counts.cpu().numpy(), self.device_of, W, L.P)
         t_unit, th = None, np.zeros(W)
         if policy.kind != "none":
             th = device_thresholds(pre, policy.t_drop, load_aware)
@@ -231,7 +263,7 @@ class ExpertParallelMoE:
         if stats:
             post = torch.from_numpy(np.stack([seg[:, 1], seg[:, 2] - seg[:, 1]]).astype(np.int64)).to(dev)
             post = self.coll.all_reduce(post).cpu().numpy()
-            rep["post_loads"] = post_loads_from_segments(post[0], post[1], self.owner, W, L.P)
+            rep["post_loads"] = post_loads_from_segments(post[0], post[1], self.device_of, W, L.P)
             rep["speedup"] = modeled_speedup(pre, rep["post_loads"])
             rep["local_drop_stats"] = st
         if timing:
@@ -253,7 +285,7 @@ class ExpertParallelMoE:
         seg0, _, _ = D.dispatch(self.ctx, L, x, D.DropPolicy(), logits_mode=logits_mode)
         counts = torch.from_numpy(seg0[:, 2].astype(np.int64)).to(dev)
         counts = self.coll.all_reduce(counts)
-        pre = loads_from_counts(counts.cpu().numpy(), self.owner, self.world)
+        pre = loads_from_counts(counts.cpu().numpy(), self.device_of, self.world, L.P)
         t_unit, th = None, np.zeros(self.world)
         if policy.kind != "none":
             th = device_thresholds(pre, policy.t_drop, load_aware)
@@ -298,7 +330,7 @@ class ExpertParallelMoE:
         post = torch.from_numpy(np.stack([seg[:, 1], seg[:, 2] - seg[:, 1]]).astype(np.int64)).to(dev)
         post = self.coll.all_reduce(post)
         post = post.cpu().numpy()
-        post_loads = post_loads_from_segments(post[0], post[1], self.owner, self.world, L.P)
+        post_loads = post_loads_from_segments(post[0], post[1], self.device_of, self.world, L.P)
         rep = {"pre_loads": pre, "post_loads": post_loads, "thresholds": th, "speedup": modeled_speedup(pre, post_loads),
                "local_drop_stats": st, "rows_sent": send, "rows_received": int(nrecv)}
         if timing:
@@ -317,6 +349,9 @@ class EpEmulator:
     def __init__(self, layer: D.MoeLayer, devices: int):
         self.layer = layer
         self.D = devices
+        self.device_of = block_devices(layer.E, layer.P, devices)
+        if not expert_aligned(self.device_of, layer.P):
+            raise D.DsmoeError(1, "EpEmulator: an expert's sub-blocks straddle two devices")
         self.owner = owner_of_experts(layer.E, layer.P, devices)
         self.ctx = [D.Context() for _ in range(devices)]
         self.ctx_exp = [D.Context() for _ in range(devices)]
@@ -330,7 +365,7 @@ class EpEmulator:
         for r in range(Dv):
             seg0, _, _ = D.dispatch(self.ctx[r], L, xs[r], D.DropPolicy(), logits_mode=logits_mode)
             counts += seg0[:, 2]
-        pre = loads_from_counts(counts, self.owner, Dv)
+        pre = loads_from_counts(counts, self.device_of, Dv, L.P)
         t_unit, th = None, np.zeros(Dv)
         if policy.kind != "none":
             th = device_thresholds(pre, policy.t_drop, load_aware)
@@ -381,7 +416,7 @@ class EpEmulator:
         for r in range(Dv):
             full += seg[r][:, 1]
             maj += seg[r][:, 2] - seg[r][:, 1]
-        post = post_loads_from_segments(full, maj, self.owner, Dv, L.P)
+        post = post_loads_from_segments(full, maj, self.device_of, Dv, L.P)
         rep = {"pre_loads": pre, "post_loads": post, "thresholds": th, "speedup": modeled_speedup(pre, post)}
         if timing:
             rep["expert_ms"] = expert_ms

@@ -45,7 +45,7 @@ def _worker(rank, world, port, results):
     counts = np.bincount(r.idx[:, :rec.K].ravel() // rec.P, minlength=rec.E)
     t = torch.from_numpy(counts.astype(np.int64))
     dist.all_reduce(t)
-    pre = ep.loads_from_counts(t.numpy(), owner, 4)
+    pre = ep.loads_from_counts(t.numpy(), ep.block_devices(rec.E, rec.P, 4), 4, rec.P)
     th = ep.device_thresholds(pre, 0.3, True)
     # dispatch bookkeeping: seg from the oracle permutation of the dropped routing
     tmaj = th[owner][r.idx[:, :rec.K] // rec.P] - 0.01
@@ -93,6 +93,9 @@ def test_ep_host_helpers():
     owner = ep.owner_of_experts(8, 2, 4)
     assert owner.tolist() == [0, 0, 1, 1, 2, 2, 3, 3]
     assert ep.loads_from_counts([3, 1, 0, 0, 2, 2, 5, 0], owner, 4).tolist() == [4, 0, 4, 5]
+    dv = ep.block_devices(8, 2, 4)
+    assert ep.expert_aligned(dv, 2)
+    assert ep.loads_from_counts([3, 1, 0, 0, 2, 2, 5, 0], dv, 4, 2).tolist() == [4, 0, 4, 5]
     assert ep.modeled_speedup([4, 0, 4, 5], [4, 0, 4, 4]) == 1.25
     seg = np.array([[0, 2, 3], [3, 1, 1], [4, 0, 0], [4, 0, 0], [4, 2, 2], [6, 0, 1], [7, 1, 1], [8, 0, 0]])
     assert ep.send_counts(seg, owner, 4).tolist() == [4, 0, 3, 1]
@@ -100,4 +103,30 @@ def test_ep_host_helpers():
     assert c[0].tolist() == [[2, 1], [1, 0]]
     segs, n = ep.receive_segments(np.stack([c[0], c[0]]), [0, 1])
     assert segs == [(0, 0, 2, 3), (1, 3, 1, 1), (0, 4, 2, 3), (1, 7, 1, 1)] and n == 8
-    assert ep.post_loads_from_segments([2, 1], [1, 0], [0, 0], 1, 2).tolist() == [3.5]
+    assert ep.post_loads_from_segments([2, 1], [1, 0], [0, 0, 0, 0], 1, 2).tolist() == [3.5]
+
+
+def test_ep_loads_straddling_blocks():
+    """E*P/D odd (E=6, P=2, D=4 -> 3 blocks per device) puts an
+    expert's halves on two devices; loads must follow the physical blocks as
+    device_loads does (ep_sim.hpp:59-72), not the copy-0 owner."""
+    from paper_2508_18376_b200 import ep
+    E, P, Dv = 6, 2, 4
+    dv = ep.block_devices(E, P, Dv)  # 12 blocks, 3 per device
+    assert not ep.expert_aligned(dv, P)
+    rng = np.random.default_rng(3)
+    T, K = 50, 2
+    idx0 = np.stack([rng.permutation(E)[:K] for _ in range(T)])
+    # replayed no-drop routing: copy-major indices e*P+p, fraction 1
+    idx = np.concatenate([idx0 * P + p for p in range(P)], axis=1)
+    frac = np.ones_like(idx, dtype=np.float64)
+    ref = O.device_loads(idx, frac, P, dv, Dv)
+    counts = np.bincount(idx0.ravel(), minlength=E)
+    assert np.array_equal(ep.loads_from_counts(counts, dv, Dv, P), ref)
+    # dropped routing: some selections major-only (copy 1 dropped), some dropped entirely
+    f1 = rng.integers(0, 3, size=idx0.shape)  # 0 dropped, 1 major-only, 2 full
+    frac = np.concatenate([(f1 > 0).astype(np.float64), (f1 == 2).astype(np.float64)], axis=1)
+    ref = O.device_loads(idx, frac, P, dv, Dv)
+    full = np.bincount(idx0[f1 == 2], minlength=E)
+    maj = np.bincount(idx0[f1 == 1], minlength=E)
+    assert np.array_equal(ep.post_loads_from_segments(full, maj, dv, Dv, P), ref)

@@ -17,7 +17,7 @@ T = int(os.environ.get("T", "16384"))
 torch.cuda.set_device(0)
 ctx = D.Context()
 layer, _ = bench.build_layer(cfg, ctx)
-x = torch.randn(T, bench.CONFIGS[cfg][0], device="cuda").to(torch.bfloat16)
+x = bench.bench_tokens(bench.base_cfg(cfg), T).cuda()
 pol, rate = bench.calibrate(ctx, layer, x, drop)
 for _ in range(3):
     D.forward(ctx, layer, x, pol)
