@@ -16,7 +16,6 @@
  *                               i.e. gate_scores moe.hpp:170, topk_route :181,
  *                               replay_routing :277, ensure_normalized
  *                               dropping.hpp:75, drop_1t :133 / drop_2t :141
- *   dsmoe_b200_route_logits     the same on caller-supplied fp32 logits
  *   dsmoe_b200_moe_forward      moe_forward (include/dsmoe/moe.hpp:239)
  *   dsmoe_b200_forward          route_and_drop + drop_stats + moe_forward, the
  *                               per-layer body of model_forward_dropped
@@ -306,6 +305,23 @@ int dsmoe_b200_layer_get_shared(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* lay
 /* ---- expert parallelism policy (ep_sim.hpp) ----------------------------- */
 /* host arrays; same arithmetic as load_aware_thresholds (ep_sim.hpp:76-89) */
 int dsmoe_b200_load_aware_thresholds(const double* loads, int devices, double t_max, double* out);
+/* simulate_step (ep_sim.hpp:110-160) for one layer on the device: the batch x
+ * (device, T x d) routed without drop, device_loads of the placement
+ * device_of (host, E*P block devices over `devices`), uniform or load-aware
+ * thresholds, the batch re-routed under each selection's owner-device
+ * threshold (2T keeping the policy's band offsets).  Host outputs:
+ * pre_loads / post_loads / thresholds (`devices` each), scalars3 = {ideal
+ * load, drop rate, speed-up max(pre)/max(post)}, stats (optional).  Optional
+ * device outputs: post (the dropped RoutingDecision) and y = moe_forward(x,
+ * post) (+ x with DSMOE_B200_RESIDUAL in flags) — simulate_step followed by
+ * the forward of dsmoe_sim_ep (capi.cpp:421-429).  The loads are exact: each
+ * device's load is its number of kept copies times 1/P, summed as the
+ * reference's slot loop sums them. */
+int dsmoe_b200_simulate_step(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T, int devices,
+                             const int32_t* device_of, const dsmoe_b200_policy* policy, int load_aware,
+                             int logits_mode, double* pre_loads, double* post_loads, double* thresholds,
+                             double* scalars3, dsmoe_b200_drop_stats_t* stats, const dsmoe_b200_routing* post,
+                             void* y, int flags);
 
 #ifdef __cplusplus
 }

@@ -746,7 +746,10 @@ void read_counters(dsmoe_b200_ctx* C, unsigned long long* h5) {
   cuda_check(cudaStreamSynchronize(C->stream), "sync");
   const unsigned long long f = h5[2] | h5[4] | C->last_err_flags;
   C->last_err_flags = 0;
-  if (h5[4]) cuda_check(cudaMemsetAsync(C->counters.as<unsigned long long>() + 4, 0, 8, C->stream), "memset");
+  if (h5[2] | h5[4]) {  // report once: the next check on this context starts clean
+    cuda_check(cudaMemsetAsync(C->counters.as<unsigned long long>() + 2, 0, 8, C->stream), "memset");
+    cuda_check(cudaMemsetAsync(C->counters.as<unsigned long long>() + 4, 0, 8, C->stream), "memset");
+  }
   raise_flags(f);
 }
 

@@ -153,6 +153,7 @@ int launch_col_gather(int bf16, const void* src, void* dst, const ColUnit* units
                       int rows, long long src_ld, long long dst_ld, cudaStream_t s);
 int launch_transpose(int bf16, const void* src, long long src_ld, const long long* rows, long long row0,
                      long long col0, int R, int Ccount, void* out, cudaStream_t s);
+int launch_compare_rows(int bf16, const void* a, const void* b, int T, int d, double* out, cudaStream_t s);
 
 }  // namespace dsb
 

@@ -128,4 +128,57 @@ int launch_transpose(int bf16, const void* src, long long src_ld, const long lon
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
+// Row comparison of two T x d outputs (report metrics of the reference C
+// ABI: mean_relative_error, dropping.hpp:278-293, and the scaled residual of
+// verify_equivalence, transform.hpp:190-198): per token t, out[5t + ...] =
+// { sum (a-b)^2, sum b^2, max |a-b|, max |a|, max |b| } in double.  One warp
+// per token.
+template <typename TE>
+__global__ void __launch_bounds__(256) compare_rows_kernel(const TE* __restrict__ a, const TE* __restrict__ b,
+                                                           int T, int d, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= T) return;
+  const TE* ra = a + static_cast<long long>(t) * d;
+  const TE* rb = b + static_cast<long long>(t) * d;
+  double s_d = 0.0, s_b = 0.0, m_d = 0.0, m_a = 0.0, m_b = 0.0;
+  for (int j = lane; j < d; j += 32) {
+    const double va = static_cast<double>(static_cast<float>(ra[j]));
+    const double vb = static_cast<double>(static_cast<float>(rb[j]));
+    const double df = va - vb;
+    s_d += df * df;
+    s_b += vb * vb;
+    m_d = fmax(m_d, fabs(df));
+    m_a = fmax(m_a, fabs(va));
+    m_b = fmax(m_b, fabs(vb));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s_d += __shfl_xor_sync(0xffffffffu, s_d, o);
+    s_b += __shfl_xor_sync(0xffffffffu, s_b, o);
+    m_d = fmax(m_d, __shfl_xor_sync(0xffffffffu, m_d, o));
+    m_a = fmax(m_a, __shfl_xor_sync(0xffffffffu, m_a, o));
+    m_b = fmax(m_b, __shfl_xor_sync(0xffffffffu, m_b, o));
+  }
+  if (lane == 0) {
+    double* o5 = out + 5LL * t;
+    o5[0] = s_d;
+    o5[1] = s_b;
+    o5[2] = m_d;
+    o5[3] = m_a;
+    o5[4] = m_b;
+  }
+}
+
+int launch_compare_rows(int bf16, const void* a, const void* b, int T, int d, double* out, cudaStream_t s) {
+  if (T <= 0) return 0;
+  const int blocks = (T + 7) / 8;
+  if (bf16)
+    compare_rows_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(a),
+                                                              static_cast<const __nv_bfloat16*>(b), T, d, out);
+  else
+    compare_rows_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(a), static_cast<const float*>(b), T,
+                                                      d, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
 }  // namespace dsb

@@ -125,6 +125,10 @@ SYMBOLS = {
     "dsmoe_b200_reconstruct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.POINTER(C.c_void_p)]),
     "dsmoe_b200_load_aware_thresholds": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_void_p]),
+    "dsmoe_b200_simulate_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                           C.POINTER(Policy), C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.POINTER(DropStatsC), C.POINTER(RoutingOut), C.c_void_p,
+                                           C.c_int]),
     "dsmoe_b200_transform": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "dsmoe_b200_layer_widths": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsmoe_b200_layer_get_gate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
