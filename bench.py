@@ -516,6 +516,7 @@ def main():
 
 def run_ep(args, dist, rank, world, local):
     """N > 1: expert parallelism over NCCL (ep.py)."""
+    import numpy as np
     import torch
     import paper_2508_18376_b200 as D
     from paper_2508_18376_b200 import ep
@@ -559,8 +560,8 @@ def run_ep(args, dist, rank, world, local):
     n_e2e = max(5, args.steps // 2)
     ms_e2e = time_steps(e2e_step, n_e2e, 2, dist) / n_e2e
     # roofline of the expert side: the slowest rank's grouped-GEMM FLOPs / its expert time
-    t = torch.tensor([rep.get("expert_ms") or 0.0, rep.get("expert_flops") or 0.0], device="cuda",
-                     dtype=torch.float64)
+    t = torch.tensor([rep.get("expert_ms") or 0.0, rep.get("expert_flops") or 0.0, rep.get("exchange_ms") or 0.0,
+                      rep.get("exchange_bytes") or 0.0], device="cuda", dtype=torch.float64)
     tall = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(tall, t)
     tall = torch.stack(tall).cpu().numpy()
@@ -587,7 +588,12 @@ def run_ep(args, dist, rank, world, local):
             "roofline": {"bound": "tensor", "kernel": "expert grouped GEMMs of the slowest rank",
                          "achieved": r4(tf), "peak": peak_burst, "unit": "TFLOP/s",
                          "frac": r4(tf / peak_burst) if tf else None, "traffic": None,
-                         "peak_kind": f"bf16 burst ({peak_src})"},
+                         "peak_kind": f"bf16 burst ({peak_src})",
+                         "exchange": {"what": "all-to-all rows + records, both directions, per rank",
+                                      "bytes_max_rank": int(tall[:, 3].max()),
+                                      "ms_max_rank": r4(float(tall[:, 2].max())),
+                                      "GBps_per_rank": r4(float((tall[:, 3] / np.maximum(tall[:, 2], 1e-9)).min()
+                                                                / 1e6))}},
             "cpu_baseline": cpu,
             "e2e": {"value": T * world / (ms_e2e * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": xh.numel() * xh.element_size() * world,

@@ -248,6 +248,47 @@ int dsmoe_b200_ep_expert(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, con
 int dsmoe_b200_ep_combine(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* ret_rows, int T,
                           void* out);
 
+/* EP with one host synchronisation per step (ep.py, ExpertParallelMoE):
+ *   ep_route_counts   route the batch without drop (normalisation per the
+ *                     policy) and write the per-expert selection counts
+ *                     (device, E x {full, major-only} int64) — the integers
+ *                     all-reduced across ranks;
+ *   ep_last_counts    the same counts of the last routing on the context
+ *                     (after ep_dispatch: the kept selections, for post loads);
+ *   ep_thresholds     from the all-reduced counts (device): device_loads of the
+ *                     placement device_of (device, E*P int32) over `devices`,
+ *                     load-aware or uniform thresholds, and the owner table
+ *                     t_unit (device, E doubles) simulate_step applies
+ *                     (ep_sim.hpp:59-89, :139-141); loads (device, optional);
+ *   ep_dispatch       re-route under policy->t_unit (pass logits_mode
+ *                     DSMOE_B200_LOGITS_REUSE to reuse the logits of
+ *                     ep_route_counts), pack one row per (token, destination)
+ *                     into send_rows and one 3 x int32 record {expert*4+level,
+ *                     row, raw-score bits} per kept selection into records,
+ *                     counts (device, nranks x {rows, records} int64), and
+ *                     evaluate the local shared experts; owner (device, E);
+ *   ep_expert_packed  dsmoe_b200_ep_expert with the interleaved records.
+ * None of them synchronises the host. */
+int dsmoe_b200_ep_route_counts(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
+                               const dsmoe_b200_policy* policy, int logits_mode, int64_t* counts);
+int dsmoe_b200_ep_last_counts(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, int T, int64_t* counts);
+int dsmoe_b200_ep_thresholds(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const int64_t* counts, int devices,
+                             const int32_t* device_of, double t_max, int load_aware, double* t_unit, double* loads);
+int dsmoe_b200_ep_dispatch(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
+                           const dsmoe_b200_policy* policy, int logits_mode, int nranks, const int32_t* owner,
+                           void* send_rows, int32_t* records, int64_t* counts);
+int dsmoe_b200_ep_expert_packed(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* rows, long U,
+                                const int32_t* records, long S, const int64_t* src_row_base,
+                                const int64_t* src_rec_base, int nranks, void* out);
+/* An expert shard of `layer` for expert parallelism: the same gate, shared
+ * experts and shapes, but only routed experts [unit_lo, unit_hi) hold
+ * weights (contiguous placement puts each rank's experts in one range,
+ * ep_sim.hpp:48-52).  A shard routes, dispatches and runs ep_expert for its
+ * own experts; whole-layer entry points (forward, moe_forward, profile,
+ * reconstruct, transform) reject it with DSMOE_E_INVALID_STATE. */
+int dsmoe_b200_layer_shard(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, int unit_lo, int unit_hi,
+                           dsmoe_b200_layer** out);
+
 /* dsmoe_b200_forward with flags.  DSMOE_B200_RESIDUAL: out = x + moe(x), the
  * residual step of model_forward_dropped (dropping.hpp:271) fused into the
  * combine kernel (out may not alias x). */

@@ -86,3 +86,24 @@ def calibrate_rate(ctx: Context, layer, x, target: float, kind="2t", keep_top1=T
         else:
             hi = t
     return best
+
+
+def calibrate_per_layer(ctx: Context, layers, x, target: float, kind="2t", keep_top1=True, tol=0.005,
+                        logits_mode=LOGITS_EXACT):
+    """Per-layer thresholds for model_forward_dropped: the
+    threshold that reaches `target` differs by layer, so layer
+    l's t is calibrated on the activations that reach it under the policies
+    already chosen for layers 0..l-1.  Returns ([DropPolicy per layer],
+    [achieved rate per layer])."""
+    import torch
+    from .dsmoe import forward
+    cur = x
+    pols, rates = [], []
+    for layer in layers:
+        pol, rate = calibrate_rate(ctx, layer, cur, target, kind, keep_top1, tol, logits_mode=logits_mode)
+        pols.append(pol)
+        rates.append(rate)
+        nxt = torch.empty_like(cur)
+        forward(ctx, layer, cur, pol, out=nxt, logits_mode=logits_mode, residual=True)
+        cur = nxt
+    return pols, rates

@@ -166,9 +166,14 @@ struct dsmoe_b200_layer {
   // block, any fraction per slot, moe.hpp:239-271) runs on the same kernels
   mutable dsmoe_b200_layer* bview = nullptr;
   mutable std::mutex bview_mu;
+  // expert shard (expert parallelism): only routed units [shard_lo, shard_hi)
+  // (and the shared experts) hold weights; the gate is whole
+  int shard_lo = 0, shard_hi = 0;
   ~dsmoe_b200_layer();
 
   int nunits() const { return E + S; }
+  bool sharded() const { return shard_lo > 0 || shard_hi < E; }
+  bool holds(int unit) const { return unit >= E || (unit >= shard_lo && unit < shard_hi); }
   // sub-block p of routed unit e <- block (e, p) columns [col0, col0 + n)
   void check_ready() const {
     require(gate_set, DSMOE_E_INVALID_STATE, "layer: gate weights not set");
@@ -198,7 +203,8 @@ int pair_mask(const dsmoe_b200_layer* L) {
 
 namespace {
 
-void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool ragged = false) {
+void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool ragged = false, int shard_lo = 0,
+                 int shard_hi = -1) {
   require(c.d_model >= 1, DSMOE_E_INVALID_ARGUMENT, "config: d_model must be >= 1");
   require(c.d_ffn >= 2, DSMOE_E_INVALID_ARGUMENT, "config: d_ffn must be >= 2");
   require(c.num_experts >= 1, DSMOE_E_INVALID_ARGUMENT, "config: num_experts must be >= 1");
@@ -220,6 +226,10 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool rag
   L->P = c.replay_factor;
   L->prenorm = c.gate_prenormalized != 0;
   L->dtype = c.dtype;
+  L->shard_lo = shard_lo;
+  L->shard_hi = shard_hi < 0 ? c.num_experts : shard_hi;
+  require(L->shard_lo >= 0 && L->shard_lo < L->shard_hi && L->shard_hi <= c.num_experts, DSMOE_E_INVALID_ARGUMENT,
+          "layer: shard range must satisfy 0 <= lo < hi <= num_experts");
   const int P = L->P;
   for (int b = 0; b < L->E * P; ++b) L->widths.push_back(c.block_widths ? c.block_widths[b] : c.d_ffn / P);
   for (int s = 0; s < L->S; ++s) L->swidths.push_back(c.shared_widths ? c.shared_widths[s] : c.d_ffn);
@@ -234,7 +244,7 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool rag
                 ", expected " + std::to_string(L->ffn));
   }
   long long row = 0;
-  int hmax = 0, chmax = 0;
+  int hmax = 0, chmax = 0, w2t_units = 0;
   for (int e = 0; e < L->E + L->S; ++e) {
     UnitInfo u{};
     const bool sh = e >= L->E;
@@ -259,15 +269,17 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool rag
       u.hwidth += u.sub_wpad[p];
       chunks += (u.sub_wpad[p] + kChunk - 1) / kChunk;
     }
-    u.w13_row = static_cast<int>(row);
-    u.w2t_row = e * L->d;
     u.shared = sh ? 1 : 0;
-    row += 2LL * u.hwidth;
+    if (L->holds(e)) {  // units outside an expert shard keep their shape but no storage
+      u.w13_row = static_cast<int>(row);
+      u.w2t_row = w2t_units++ * L->d;
+      row += 2LL * u.hwidth;
+    }
     hmax = std::max(hmax, u.hwidth);
     chmax = std::max(chmax, chunks);
     L->units.push_back(u);
   }
-  require(row < (1LL << 31) && static_cast<long long>(L->E + L->S) * L->d < (1LL << 31),
+  require(row < (1LL << 31) && static_cast<long long>(w2t_units) * L->d < (1LL << 31),
           DSMOE_E_INVALID_ARGUMENT, "layer: packed weights exceed 2^31 rows");
   L->w13_rows = row;
   L->hstride = hmax;
@@ -275,7 +287,7 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool rag
   L->Epad = round_up(L->E, 32);
   const int es = esize(L->dtype);
   L->w13.ensure(static_cast<size_t>(row) * L->d * es);
-  L->w2t.ensure(static_cast<size_t>(L->E + L->S) * L->d * L->hstride * es);
+  L->w2t.ensure(static_cast<size_t>(w2t_units) * L->d * L->hstride * es);
   L->gateT.ensure(static_cast<size_t>(L->Epad) * L->d * es);
   L->gate_exact.ensure(static_cast<size_t>(L->d) * L->E * 4);
   cuda_check(cudaMemset(L->w13.p, 0, L->w13.bytes), "memset");
@@ -287,12 +299,14 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool rag
              "upload units");
   if (L->dtype == DSMOE_B200_BF16) {
     L->map_w13 = make_map(L->w13.p, row, L->d, L->d, 256);
-    L->map_w2t = make_map(L->w2t.p, static_cast<long long>(L->E + L->S) * L->d, L->hstride, L->hstride, 256);
+    L->map_w2t = make_map(L->w2t.p, static_cast<long long>(w2t_units) * L->d, L->hstride, L->hstride, 256);
     L->map_w13_h = make_map(L->w13.p, row, L->d, L->d, 128);
-    L->map_w2t_h = make_map(L->w2t.p, static_cast<long long>(L->E + L->S) * L->d, L->hstride, L->hstride, 128);
+    L->map_w2t_h = make_map(L->w2t.p, static_cast<long long>(w2t_units) * L->d, L->hstride, L->hstride, 128);
     L->map_gate = make_map(L->gateT.p, L->Epad, L->d, L->d, L->Epad);
   }
   L->block_set.assign(static_cast<size_t>(L->E * P), 0);
+  for (int b = 0; b < L->E * P; ++b)
+    if (!L->holds(b / P)) L->block_set[static_cast<size_t>(b)] = 1;  // not part of this shard
   L->shared_set.assign(static_cast<size_t>(L->S), 0);
 }
 
@@ -376,8 +390,10 @@ void regroup(const dsmoe_b200_layer* L, dsmoe_b200_layer* R, const std::vector<i
   std::vector<int> colmap(static_cast<size_t>(R->nunits()) * R->hstride, -1);
   std::vector<ColUnit> cu;
   for (int v = 0; v < R->nunits(); ++v) {
+    if (!R->holds(v)) continue;
     const UnitInfo& du = R->units[v];
     const UnitInfo& su = L->units[src_unit[v]];
+    require(L->holds(src_unit[v]), DSMOE_E_INVALID_STATE, "regroup: source unit not held by this expert shard");
     int off = 0;
     for (int p = 0; p < du.nsub; ++p) {
       const long long db = sub_w13_base(du, p);
@@ -436,6 +452,7 @@ constexpr int kModeComplete = 0, kModePartial = 1, kModeReverse = 2, kModeBlocks
 // complete_transform / partial_transform / reverse_partial (transform.hpp:66-170)
 // or the block view of a device layer, as a new device layer.
 dsmoe_b200_layer* transform_layer(const dsmoe_b200_layer* L, int mode, int p, cudaStream_t s) {
+  require(!L->sharded(), DSMOE_E_INVALID_STATE, "transform: layer is an expert shard");
   std::vector<int32_t> widths, swidths(L->swidths.begin(), L->swidths.end());
   dsmoe_b200_layer_config cfg{L->d, L->ffn, L->E, L->K, L->S, L->prenorm, 1, L->dtype, nullptr, nullptr};
   std::vector<int> src_unit, gmap;
@@ -1035,6 +1052,12 @@ void require_layer(const dsmoe_b200_layer* L) {
   require(L != nullptr, DSMOE_E_INVALID_ARGUMENT, "null layer");
   L->check_ready();
 }
+// entry points that evaluate arbitrary experts need every expert's weights
+void require_whole(const dsmoe_b200_layer* L) {
+  require_layer(L);
+  require(!L->sharded(), DSMOE_E_INVALID_STATE,
+          "layer is an expert shard (expert parallelism): it evaluates only its own experts");
+}
 
 }  // namespace
 
@@ -1089,6 +1112,7 @@ int dsmoe_b200_layer_set_block(dsmoe_b200_layer* L, int b, const void* w1, const
   return guarded([&] {
     require(L && w1 && w3 && w2, DSMOE_E_INVALID_ARGUMENT, "null argument");
     require(b >= 0 && b < L->E * L->P, DSMOE_E_INVALID_ARGUMENT, "block index out of range");
+    require(L->holds(b / L->P), DSMOE_E_INVALID_ARGUMENT, "block is not part of this expert shard");
     require(src_dtype == 0 || src_dtype == 1, DSMOE_E_INVALID_ARGUMENT, "bad source dtype");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int wd = L->widths[b];
@@ -1228,7 +1252,7 @@ int dsmoe_b200_moe_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
                            const int32_t* indices, const double* raw, const double* fraction, void* out) {
   return guarded([&] {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
-    require_layer(L);
+    require_whole(L);
     require(T >= 0, DSMOE_E_INVALID_ARGUMENT, "negative token count");
     g_launches = 0;
     if (T == 0) return;
@@ -1299,7 +1323,7 @@ int dsmoe_b200_forward_ex(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
                           dsmoe_b200_drop_stats_t* stats) {
   return guarded([&] {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
-    require_layer(L);
+    require_whole(L);
     require(T >= 0, DSMOE_E_INVALID_ARGUMENT, "negative token count");
     g_launches = 0;
     const PolicyResolved pol = resolve_policy(L, policy);
@@ -1405,7 +1429,7 @@ int dsmoe_b200_expert_ffn(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
                           const int32_t* seg_nfull, const int32_t* seg_ntot, void* y_out) {
   return guarded([&] {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
-    require_layer(L);
+    require_whole(L);
     require(nseg >= 0 && nseg <= 2048, DSMOE_E_INVALID_ARGUMENT, "expert_ffn: at most 2048 segments");
     require(nseg == 0 || (seg_unit && seg_start && seg_nfull && seg_ntot), DSMOE_E_INVALID_ARGUMENT, "null segments");
     g_launches = 0;
@@ -1519,10 +1543,42 @@ int dsmoe_b200_ep_pack(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void*
   });
 }
 
+}  // extern "C"
+
+namespace {
+void ep_expert_impl(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long U, const int32_t* rec_code,
+                    const int32_t* rec_row, const float* rec_raw, int rec_stride, long S, const int64_t* src_row_base,
+                    const int64_t* src_rec_base, int nranks, void* out);
+}  // namespace
+
+extern "C" {
+
 int dsmoe_b200_ep_expert(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long U,
                          const int32_t* rec_code, const int32_t* rec_row, const float* rec_raw, long S,
                          const int64_t* src_row_base, const int64_t* src_rec_base, int nranks, void* out) {
   return guarded([&] {
+    ep_expert_impl(C, L, rows, U, rec_code, rec_row, rec_raw, 1, S, src_row_base, src_rec_base, nranks, out);
+  });
+}
+
+int dsmoe_b200_ep_expert_packed(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long U,
+                                const int32_t* records, long S, const int64_t* src_row_base,
+                                const int64_t* src_rec_base, int nranks, void* out) {
+  return guarded([&] {
+    require(S == 0 || records != nullptr, DSMOE_E_INVALID_ARGUMENT, "null records");
+    ep_expert_impl(C, L, rows, U, records, records ? records + 1 : nullptr,
+                   records ? reinterpret_cast<const float*>(records + 2) : nullptr, 3, S, src_row_base, src_rec_base,
+                   nranks, out);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+void ep_expert_impl(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, long U, const int32_t* rec_code,
+                    const int32_t* rec_row, const float* rec_raw, int rec_stride, long S, const int64_t* src_row_base,
+                    const int64_t* src_rec_base, int nranks, void* out) {
+  {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
     require_layer(L);
     require(nranks >= 1 && nranks <= 32 && src_row_base && src_rec_base, DSMOE_E_INVALID_ARGUMENT, "null argument");
@@ -1544,16 +1600,20 @@ int dsmoe_b200_ep_expert(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const voi
     cuda_check(cudaMemsetAsync(C->sel_code.p, 0xFF, static_cast<size_t>(Ti) * L->K * 4, s), "memset");
     cuda_check(cudaMemsetAsync(C->cnt_chunk.p, 0, static_cast<size_t>(nchunks) * 2 * L->E * 4, s), "memset");
     const long long* b = C->ep_base.as<long long>();
-    launch_check(launch_ep_local_routing(rec_code, rec_row, rec_raw, S, b, b + nranks + 1, nranks, L->K, L->E,
-                                         C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), C->cnt_chunk.as<int>(),
-                                         num_sms(), s),
+    launch_check(launch_ep_local_routing(rec_code, rec_row, rec_raw, S, rec_stride, b, b + nranks + 1, nranks, L->K,
+                                         L->E, L->shard_lo, L->shard_hi, C->sel_code.as<int32_t>(),
+                                         C->sel_raw.as<float>(), C->cnt_chunk.as<int>(),
+                                         C->counters.as<unsigned long long>(), num_sms(), s),
                  "ep local routing");
     count_launch(1);
     count_launch(1);
     C->logits_T = -1;  // the routing codes on this context are no longer a gate routing
     stage_ffn(C, L, rows, Ti, out, nullptr, /*routed_only=*/true);
-  });
+  }
 }
+}  // namespace
+
+extern "C" {
 
 int dsmoe_b200_ep_combine(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* ret_rows, int T, void* out) {
   return guarded([&] {
@@ -1567,6 +1627,130 @@ int dsmoe_b200_ep_combine(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const vo
                                          C->Y.p, L->S, static_cast<int>(Rcap), out, T, L->d, num_sms(), C->stream),
                  "ep combine");
     count_launch(1);
+  });
+}
+
+int dsmoe_b200_ep_route_counts(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                               const dsmoe_b200_policy* policy, int logits_mode, int64_t* counts) {
+  return guarded([&] {
+    require(C != nullptr && counts != nullptr, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require_layer(L);
+    require(T >= 1 && x, DSMOE_E_INVALID_ARGUMENT, "ep_route_counts: empty batch");
+    g_launches = 0;
+    PolicyResolved pol = resolve_policy(L, nullptr);
+    if (policy && policy->normalize >= 0) pol.normalize = policy->normalize != 0;  // ensure_normalized only
+    C->ensure(L, T);
+    stage_route(C, L, x, T, pol, logits_mode, nullptr, nullptr, nullptr, nullptr);
+    launch_check(launch_ep_counts(C->cnt_chunk.as<int>(), (T + kRouterChunk - 1) / kRouterChunk, L->E,
+                                  reinterpret_cast<long long*>(counts), C->stream),
+                 "ep counts");
+    count_launch(1);
+  });
+}
+
+int dsmoe_b200_ep_last_counts(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, int64_t* counts) {
+  return guarded([&] {
+    require(C != nullptr && L != nullptr && counts != nullptr, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(C->logits_T == T && T >= 1, DSMOE_E_INVALID_STATE, "ep_last_counts: no routing of this batch on the context");
+    launch_check(launch_ep_counts(C->cnt_chunk.as<int>(), (T + kRouterChunk - 1) / kRouterChunk, L->E,
+                                  reinterpret_cast<long long*>(counts), C->stream),
+                 "ep counts");
+    count_launch(1);
+  });
+}
+
+int dsmoe_b200_ep_thresholds(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const int64_t* counts, int devices,
+                             const int32_t* device_of, double t_max, int load_aware, double* t_unit, double* loads) {
+  return guarded([&] {
+    require(C && L && counts && device_of && t_unit, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(devices >= 1 && devices <= 2048, DSMOE_E_INVALID_ARGUMENT, "ep_thresholds: bad device count");
+    require(t_max > 0.0 && t_max <= 1.0, DSMOE_E_INVALID_ARGUMENT, "load_aware_thresholds: t_max must be in (0, 1]");
+    g_launches = 0;
+    launch_check(launch_ep_thresholds(reinterpret_cast<const long long*>(counts), L->E, L->P, devices, device_of, t_max,
+                                      load_aware, t_unit, loads, C->stream),
+                 "ep thresholds");
+    count_launch(1);
+  });
+}
+
+int dsmoe_b200_ep_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                           const dsmoe_b200_policy* policy, int logits_mode, int nranks, const int32_t* owner,
+                           void* send_rows, int32_t* records, int64_t* counts) {
+  return guarded([&] {
+    require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
+    require_layer(L);
+    require(nranks >= 1 && nranks <= 32, DSMOE_E_INVALID_ARGUMENT, "ep_dispatch: 1 <= nranks <= 32");
+    require(T >= 1 && x && owner && send_rows && records && counts, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    g_launches = 0;
+    const PolicyResolved pol = resolve_policy(L, policy);
+    C->ensure(L, T);
+    cudaStream_t s = C->stream;
+    stage_route(C, L, x, T, pol, logits_mode, nullptr, nullptr, nullptr, nullptr);
+    const int nchunks = (T + 255) / 256;
+    C->ep_pos_td.ensure(static_cast<size_t>(T) * nranks * 4);
+    C->ep_send_token.ensure(static_cast<size_t>(T) * std::min(nranks, L->K) * 4 + 16);
+    C->ep_cnt.ensure(static_cast<size_t>(2) * nchunks * nranks * 4);
+    C->ep_tot.ensure(static_cast<size_t>(4) * nranks * 4 + 16);
+    int* cnt = C->ep_cnt.as<int>();
+    int* r_total = C->ep_tot.as<int>() + 4 * nranks;
+    launch_check(launch_ep_pack(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), owner, T, L->K, nranks, cnt,
+                                cnt + nchunks * nranks, C->ep_tot.as<int>(), C->ep_send_token.as<int32_t>(),
+                                C->ep_pos_td.as<int32_t>(), records, records + 1, reinterpret_cast<float*>(records + 2),
+                                r_total, num_sms(), s, 3, reinterpret_cast<long long*>(counts)),
+                 "ep_pack");
+    launch_check(launch_gather(x, send_rows, C->ep_send_token.as<int32_t>(), r_total, L->d * esize(L->dtype),
+                               num_sms(), s),
+                 "ep gather");
+    count_launch(2);
+    // the local shared experts (moe.hpp:267-268) into the context's Y rows
+    if (L->S > 0) {
+      const long long Rcap = static_cast<long long>(T) * L->K;
+      int* sc = C->scalars.as<int>();
+      PlanArgs pa{};
+      pa.units = L->d_units.as<UnitInfo>();
+      pa.seg_routed = C->seg.as<UnitSeg>();
+      pa.shared_unit0 = L->E;
+      pa.num_routed = 0;
+      pa.num_shared = L->S;
+      pa.T = T;
+      pa.d = L->d;
+      pa.shared_row0 = static_cast<int>(Rcap);
+      pa.tiles1 = C->tiles1.as<GemmTile>();
+      pa.n1 = sc + 1;
+      pa.tiles2 = C->tiles2.as<GemmTile>();
+      pa.n2 = sc + 2;
+      launch_check(launch_plan(pa, num_sms(), s), "plan shared");
+      count_launch(1);
+      const long long rows = Rcap + static_cast<long long>(L->S) * T + kTileM;
+      run_gemms(C, L, x, T, x, T, sc + 1, sc + 2, C->max_tiles1(L, T), C->max_tiles2(L, T), rows, C->Y.p,
+                C->row_scale.as<float>());
+    }
+    C->ep_N = nranks;
+    C->ep_T = T;
+  });
+}
+
+int dsmoe_b200_layer_shard(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int unit_lo, int unit_hi,
+                           dsmoe_b200_layer** out) {
+  return guarded([&] {
+    require(C && out, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require_whole(L);
+    std::vector<int32_t> widths(L->widths.begin(), L->widths.end()), swidths(L->swidths.begin(), L->swidths.end());
+    dsmoe_b200_layer_config cfg{L->d, L->ffn, L->E, L->K, L->S, L->prenorm, L->P, L->dtype, widths.data(),
+                                swidths.empty() ? nullptr : swidths.data()};
+    auto* R = new dsmoe_b200_layer;
+    try {
+      layer_build(R, cfg, false, unit_lo, unit_hi);
+      std::vector<int> src_unit(static_cast<size_t>(L->nunits())), gmap(static_cast<size_t>(L->E));
+      for (int v = 0; v < L->nunits(); ++v) src_unit[static_cast<size_t>(v)] = v;
+      for (int e = 0; e < L->E; ++e) gmap[static_cast<size_t>(e)] = e;
+      std::vector<float> scale(static_cast<size_t>(L->nunits()), 1.0f);
+      regroup(L, R, src_unit, scale, [](int, int n) { return n; }, gmap, C->stream);
+    } catch (...) {
+      delete R;
+      throw;
+    }
+    *out = R;
   });
 }
 
@@ -1771,7 +1955,7 @@ int dsmoe_b200_profile_importance(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, 
                                   const int32_t* indices, int metric, double* values) {
   return guarded([&] {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
-    require_layer(L);
+    require_whole(L);
     require(L->P == 1, DSMOE_E_INVALID_STATE,
             "profile_importance: profile the original layer, not a partitioned one");
     require(T >= 1, DSMOE_E_INVALID_ARGUMENT, "profile_importance: empty calibration set");
@@ -1827,7 +2011,7 @@ int dsmoe_b200_reconstruct(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const d
                            dsmoe_b200_layer** out) {
   return guarded([&] {
     require(C != nullptr && out != nullptr && values != nullptr, DSMOE_E_INVALID_ARGUMENT, "null argument");
-    require_layer(L);
+    require_whole(L);
     require(L->P == 1, DSMOE_E_INVALID_STATE, "reconstruct_experts: layer already partitioned");
     cudaStream_t s = C->stream;
     DevBuf ord;

@@ -41,10 +41,12 @@ struct PackArgs {
   int* tot;                 // [N unique rows | N records | base_u N | base_s N]
   int32_t* send_token;      // U_total
   int32_t* pos_td;          // T x N
-  int32_t* rec_code;        // S_total
+  int32_t* rec_code;        // S_total records, element stride rec_stride
   int32_t* rec_row;
   float* rec_raw;
   int* r_total;             // U_total (device scalar for the row gather)
+  int rec_stride;           // 1: three separate arrays; 3: one interleaved {code, row, raw} array
+  long long* counts_out;    // optional: N x {rows, records} as int64 (device), for a sync-free exchange
 };
 
 __global__ void __launch_bounds__(kPackChunk) ep_pack_kernel(const PackArgs a) {
@@ -101,6 +103,10 @@ __global__ void __launch_bounds__(kPackChunk) ep_pack_kernel(const PackArgs a) {
     }
     a.tot[d] = ru;
     a.tot[N + d] = rs;
+    if (a.counts_out) {
+      a.counts_out[2 * d] = ru;
+      a.counts_out[2 * d + 1] = rs;
+    }
   }
   cg::this_grid().sync();
   if (threadIdx.x == 0) {
@@ -166,7 +172,7 @@ __global__ void __launch_bounds__(kPackChunk) ep_pack_kernel(const PackArgs a) {
         const int c = a.sel_code[i];
         if (c < 0) continue;
         const int d = a.owner[c >> 2];
-        const int r = rec_next[d]++;
+        const long long r = static_cast<long long>(rec_next[d]++) * a.rec_stride;
         a.rec_code[r] = c;
         a.rec_row[r] = a.pos_td[static_cast<long long>(t) * N + d] - base_u[d];
         a.rec_raw[r] = a.sel_raw[i];
@@ -178,10 +184,11 @@ __global__ void __launch_bounds__(kPackChunk) ep_pack_kernel(const PackArgs a) {
 
 int launch_ep_pack(const int32_t* sel_code, const float* sel_raw, const int32_t* owner, int T, int K, int N,
                    int* cnt_u, int* cnt_s, int* tot, int32_t* send_token, int32_t* pos_td, int32_t* rec_code,
-                   int32_t* rec_row, float* rec_raw, int* r_total, int num_sms, cudaStream_t stream) {
+                   int32_t* rec_row, float* rec_raw, int* r_total, int num_sms, cudaStream_t stream, int rec_stride,
+                   long long* counts_out) {
   if (N < 1 || N > kMaxDest || K > 16) return -1;
   PackArgs a{sel_code, sel_raw, owner, T, K, N, (T + kPackChunk - 1) / kPackChunk, cnt_u, cnt_s, tot, send_token,
-             pos_td, rec_code, rec_row, rec_raw, r_total};
+             pos_td, rec_code, rec_row, rec_raw, r_total, rec_stride, counts_out};
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ep_pack_kernel, kPackChunk, 0);
   if (per_sm < 1) return -3;
@@ -200,35 +207,124 @@ int launch_ep_pack(const int32_t* sel_code, const float* sel_raw, const int32_t*
 // record's slot is the number of earlier records of the same row.
 // --------------------------------------------------------------------------
 __global__ void ep_local_routing_kernel(const int32_t* __restrict__ rec_code, const int32_t* __restrict__ rec_row,
-                                        const float* __restrict__ rec_raw, long long S,
+                                        const float* __restrict__ rec_raw, long long S, int stride,
                                         const long long* __restrict__ src_rec_base,
                                         const long long* __restrict__ src_row_base, int N, int K, int E,
-                                        int32_t* __restrict__ sel_code, float* __restrict__ sel_raw,
-                                        int* __restrict__ cnt_chunk) {
+                                        int unit_lo, int unit_hi, int32_t* __restrict__ sel_code,
+                                        float* __restrict__ sel_raw, int* __restrict__ cnt_chunk,
+                                        unsigned long long* __restrict__ flags) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < S;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     int src = 0;
     while (src + 1 < N && src_rec_base[src + 1] <= i) ++src;
     const long long lo = src_rec_base[src];
-    const int row_local = rec_row[i];
+    const int row_local = rec_row[i * stride];
     int j = 0;
-    while (i - 1 - j >= lo && rec_row[i - 1 - j] == row_local) ++j;
+    while (i - 1 - j >= lo && rec_row[(i - 1 - j) * stride] == row_local) ++j;
     const long long row = src_row_base[src] + row_local;
-    const int c = rec_code[i];
-    sel_code[row * K + j] = c;
-    sel_raw[row * K + j] = rec_raw[i];
+    const int c = rec_code[i * stride];
     const int unit = c >> 2, level = c & 3;
+    if (unit < unit_lo || unit >= unit_hi || j >= K) {  // an expert this rank does not hold
+      atomicOr(&flags[2], 4ull);
+      atomicOr(&flags[4], 4ull);
+      continue;
+    }
+    sel_code[row * K + j] = c;
+    sel_raw[row * K + j] = rec_raw[i * stride];
     atomicAdd(&cnt_chunk[(row / kRouterChunk) * 2 * E + 2 * unit + (level == 2 ? 0 : 1)], 1);
   }
 }
 
 int launch_ep_local_routing(const int32_t* rec_code, const int32_t* rec_row, const float* rec_raw, long long S,
-                            const long long* src_rec_base, const long long* src_row_base, int N, int K, int E,
-                            int32_t* sel_code, float* sel_raw, int* cnt_chunk, int num_sms, cudaStream_t stream) {
+                            int stride, const long long* src_rec_base, const long long* src_row_base, int N, int K,
+                            int E, int unit_lo, int unit_hi, int32_t* sel_code, float* sel_raw, int* cnt_chunk,
+                            unsigned long long* flags, int num_sms, cudaStream_t stream) {
   if (S <= 0) return 0;
   const long long b = (S + 255) / 256;
   ep_local_routing_kernel<<<static_cast<int>(b < num_sms * 8 ? b : num_sms * 8), 256, 0, stream>>>(
-      rec_code, rec_row, rec_raw, S, src_rec_base, src_row_base, N, K, E, sel_code, sel_raw, cnt_chunk);
+      rec_code, rec_row, rec_raw, S, stride, src_rec_base, src_row_base, N, K, E, unit_lo, unit_hi, sel_code, sel_raw,
+      cnt_chunk, flags);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// --------------------------------------------------------------------------
+// Per-expert selection counts of the last routing, from the router's 32-token
+// chunk histograms (full + major-only kept selections): the integers the EP
+// step all-reduces (device_loads of the whole batch, ep_sim.hpp:59-72).
+// --------------------------------------------------------------------------
+__global__ void ep_counts_kernel(const int* __restrict__ cnt_chunk, int nchunks, int E, long long* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    long long full = 0, major = 0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      full += cnt_chunk[static_cast<long long>(ch) * 2 * E + 2 * e];
+      major += cnt_chunk[static_cast<long long>(ch) * 2 * E + 2 * e + 1];
+    }
+    out[2 * e] = full;   // selections kept on every sub-block
+    out[2 * e + 1] = major;  // major-only selections
+  }
+}
+
+int launch_ep_counts(const int* cnt_chunk, int nchunks, int E, long long* out, cudaStream_t stream) {
+  ep_counts_kernel<<<(E + 127) / 128, 128, 0, stream>>>(cnt_chunk, nchunks, E, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// --------------------------------------------------------------------------
+// Device-side load-aware thresholds, right after the count all-reduce:
+// device_loads (ep_sim.hpp:59-72) of the no-drop routing — each selection
+// adds 1/P to the device of each of its P blocks, so device d's load is
+// copies_d additions of 1/P — then load_aware_thresholds (:76-89) and the
+// owner table t_unit[e] = threshold of the device of block e*P (:139-141).
+// Same IEEE double operations, same order as the host functions.  One block.
+// --------------------------------------------------------------------------
+__global__ void ep_thresholds_kernel(const long long* __restrict__ counts, int E, int P, int D,
+                                     const int32_t* __restrict__ device_of, double t_max, int load_aware,
+                                     double* __restrict__ t_unit, double* __restrict__ loads_out) {
+  extern __shared__ unsigned char smem_raw[];
+  long long* copies = reinterpret_cast<long long*>(smem_raw);
+  double* loads = reinterpret_cast<double*>(copies + D);
+  double* th = loads + D;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) copies[d] = 0;
+  __syncthreads();
+  for (int b = threadIdx.x; b < E * P; b += blockDim.x)  // no-drop counts: every selection keeps all P copies
+    atomicAdd(reinterpret_cast<unsigned long long*>(&copies[device_of[b]]),
+              static_cast<unsigned long long>(counts[2 * (b / P)] + counts[2 * (b / P) + 1]));
+  __syncthreads();
+  const double w = __ddiv_rn(1.0, static_cast<double>(P));
+  const bool pow2 = (P & (P - 1)) == 0;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    double l = 0.0;
+    if (pow2) {
+      l = __dmul_rn(static_cast<double>(copies[d]), w);  // every partial sum exact
+    } else {
+      for (long long i = 0; i < copies[d]; ++i) l = __dadd_rn(l, w);
+    }
+    loads[d] = l;
+    if (loads_out) loads_out[d] = l;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double total = 0.0;
+    for (int d = 0; d < D; ++d) total = __dadd_rn(total, loads[d]);
+    const double ideal = __ddiv_rn(total, static_cast<double>(D));
+    for (int d = 0; d < D; ++d) {
+      if (!load_aware) {
+        th[d] = t_max;
+      } else {
+        const double ratio = __ddiv_rn(loads[d], ideal);
+        th[d] = ratio >= 1.0 ? t_max : __dmul_rn(t_max, ratio);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) t_unit[e] = th[device_of[e * P]];
+}
+
+int launch_ep_thresholds(const long long* counts, int E, int P, int D, const int32_t* device_of, double t_max,
+                         int load_aware, double* t_unit, double* loads_out, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(D) * (8 + 8 + 8);
+  if (smem > 48 * 1024) return -1;
+  ep_thresholds_kernel<<<1, 256, smem, stream>>>(counts, E, P, D, device_of, t_max, load_aware, t_unit, loads_out);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

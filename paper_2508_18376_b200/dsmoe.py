@@ -129,6 +129,16 @@ SYMBOLS = {
                                            C.POINTER(Policy), C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.POINTER(DropStatsC), C.POINTER(RoutingOut), C.c_void_p,
                                            C.c_int]),
+    "dsmoe_b200_ep_route_counts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy),
+                                             C.c_int, C.c_void_p]),
+    "dsmoe_b200_ep_last_counts": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "dsmoe_b200_ep_thresholds": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_double,
+                                           C.c_int, C.c_void_p, C.c_void_p]),
+    "dsmoe_b200_ep_dispatch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
+                                         C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dsmoe_b200_ep_expert_packed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_long, C.c_void_p, C.c_long,
+                                              C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "dsmoe_b200_layer_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "dsmoe_b200_transform": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "dsmoe_b200_layer_widths": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsmoe_b200_layer_get_gate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
@@ -463,17 +473,27 @@ def forward(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None = None, 
     return (out, st.as_dict()) if with_stats else out
 
 
-def model_forward_dropped(ctx: Context, layers, x, policy: DropPolicy | None = None,
-                          logits_mode=LOGITS_TENSOR):
+def model_forward_dropped(ctx: Context, layers, x, policy=None, logits_mode=LOGITS_TENSOR):
     """model_forward_dropped (dropping.hpp:263-274): x_{l+1} = x_l + moe_l(x_l)
-    with per-layer route_and_drop; returns (output, [DropStats per layer])."""
+    with per-layer route_and_drop; returns (output, [DropStats per layer]).
+    `policy` is one DropPolicy for every layer (the reference's signature) or
+    a sequence with one DropPolicy per layer — per-layer thresholds, since the
+    drop rate a threshold yields varies by layer."""
     torch = _torch()
+    layers = list(layers)
+    if isinstance(policy, (list, tuple)):
+        if len(policy) != len(layers):
+            raise DsmoeError(1, f"model_forward_dropped: {len(policy)} policies for {len(layers)} layers")
+        policies = list(policy)
+    else:
+        policies = [policy] * len(layers)
     cur = x
     stats = []
     bufs = [torch.empty_like(x), torch.empty_like(x)]
     for i, layer in enumerate(layers):
         nxt = bufs[i & 1]
-        _, st = forward(ctx, layer, cur, policy, out=nxt, logits_mode=logits_mode, with_stats=True, residual=True)
+        _, st = forward(ctx, layer, cur, policies[i], out=nxt, logits_mode=logits_mode, with_stats=True,
+                        residual=True)
         stats.append(st)
         cur = nxt
     return cur.clone() if layers else x.clone(), stats
@@ -655,6 +675,81 @@ def ep_combine(ctx: Context, layer: MoeLayer, ret_rows, T: int, out=None):
     if out is None:
         out = torch.empty((T, layer.d), dtype=layer.torch_dtype, device=ret_rows.device)
     _chk(lib().dsmoe_b200_ep_combine(ctx.h, layer.h, C.c_void_p(ret_rows.data_ptr()), T, C.c_void_p(out.data_ptr())))
+    return out
+
+
+# ---------------------------------- EP with one host synchronisation per step
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def ep_route_counts(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None = None, counts=None,
+                    logits_mode=LOGITS_TENSOR):
+    """Route x without drop; per-expert (full, major-only) selection counts
+    (E x 2 int64 CUDA tensor), no host sync."""
+    torch = _torch()
+    x = _x(x, layer)
+    if counts is None:
+        counts = torch.empty((layer.E, 2), dtype=torch.int64, device=x.device)
+    _chk(lib().dsmoe_b200_ep_route_counts(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
+                                          C.byref((policy or DropPolicy()).c()), logits_mode, _p(counts)))
+    return counts
+
+
+def ep_last_counts(ctx: Context, layer: MoeLayer, T: int, counts=None):
+    """(full, major-only) kept-selection counts of the last routing on ctx."""
+    torch = _torch()
+    if counts is None:
+        counts = torch.empty((layer.E, 2), dtype=torch.int64, device="cuda")
+    _chk(lib().dsmoe_b200_ep_last_counts(ctx.h, layer.h, T, _p(counts)))
+    return counts
+
+
+def ep_thresholds(ctx: Context, layer: MoeLayer, counts, devices: int, device_of, t_max: float, load_aware: bool,
+                  t_unit=None, loads=None):
+    """Device-side device_loads -> load_aware_thresholds -> owner table
+    (ep_sim.hpp:59-89, :139-141) from all-reduced counts; returns (t_unit E
+    float64, loads devices float64), CUDA tensors, no host sync."""
+    torch = _torch()
+    if t_unit is None:
+        t_unit = torch.empty(layer.E, dtype=torch.float64, device=counts.device)
+    if loads is None:
+        loads = torch.empty(devices, dtype=torch.float64, device=counts.device)
+    _chk(lib().dsmoe_b200_ep_thresholds(ctx.h, layer.h, _p(counts), devices, _p(device_of), float(t_max),
+                                        int(load_aware), _p(t_unit), _p(loads)))
+    return t_unit, loads
+
+
+def ep_dispatch(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None, t_unit, nranks: int, owner, send_rows,
+                records, counts, logits_mode=LOGITS_REUSE):
+    """Re-route under the owner thresholds, pack one row per (token,
+    destination) + one 3 x int32 record per kept selection, counts (nranks x
+    2 int64: rows, records), local shared experts; no host sync."""
+    x = _x(x, layer)
+    _chk(lib().dsmoe_b200_ep_dispatch(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
+                                      C.byref((policy or DropPolicy()).c(t_unit)), logits_mode, nranks, _p(owner),
+                                      _p(send_rows), _p(records), _p(counts)))
+
+
+def ep_expert_packed(ctx: Context, layer: MoeLayer, rows, U: int, records, S: int, src_row_base, src_rec_base,
+                     out=None):
+    torch = _torch()
+    if out is None:
+        out = torch.empty((max(U, 1), layer.d), dtype=layer.torch_dtype, device=rows.device)
+    rb = np.ascontiguousarray(src_row_base, np.int64)
+    sb = np.ascontiguousarray(src_rec_base, np.int64)
+    _chk(lib().dsmoe_b200_ep_expert_packed(ctx.h, layer.h, C.c_void_p(rows.data_ptr()), U, _p(records), S,
+                                           rb.ctypes.data, sb.ctypes.data, len(rb) - 1, C.c_void_p(out.data_ptr())))
+    return out
+
+
+def layer_shard(ctx: Context, layer: MoeLayer, unit_lo: int, unit_hi: int) -> MoeLayer:
+    """An expert shard: the same gate and shared experts, routed experts
+    [unit_lo, unit_hi) only (dsmoe_b200_layer_shard)."""
+    h = C.c_void_p()
+    _chk(lib().dsmoe_b200_layer_shard(ctx.h, layer.h, unit_lo, unit_hi, C.byref(h)))
+    out = MoeLayer._wrap(h, layer)
+    out.shard = (unit_lo, unit_hi)
     return out
 
 

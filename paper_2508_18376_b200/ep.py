@@ -182,14 +182,16 @@ class _Coll:
 
 
 class ExpertParallelMoE:
-    """One rank of an expert-parallel MoE layer.  Every rank holds the full
-    (replicated) layer object but evaluates only the experts it owns."""
+    """One rank of an expert-parallel MoE layer.  With shard=True (default)
+    the rank keeps only its own experts' weights (dsmoe_b200_layer_shard:
+    the gate and the shared experts are whole, routed experts [lo, hi) of the
+    contiguous placement) and evaluates only them."""
 
-    def __init__(self, layer: D.MoeLayer, group=None, strategy: str = "contiguous"):
+    def __init__(self, layer: D.MoeLayer, group=None, strategy: str = "contiguous", shard: bool = True):
+        import torch
         import torch.distributed as dist
         self.dist = dist
         self.group = group
-        self.layer = layer
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         if strategy != "contiguous":
@@ -202,73 +204,104 @@ class ExpertParallelMoE:
         self.local = np.nonzero(self.owner == self.rank)[0]
         self.ctx = D.Context()
         self.ctx_exp = D.Context()
+        self.full = layer
+        if shard and self.world > 1:
+            layer = D.layer_shard(self.ctx, layer, int(self.local[0]), int(self.local[-1]) + 1)
+        self.layer = layer
         self.coll = _Coll(dist, group)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.d_device_of = torch.from_numpy(self.device_of.astype(np.int32)).to(dev)
+        self.d_owner = torch.from_numpy(self.owner.astype(np.int32)).to(dev)
+        self._bufs = {}
+
+    def _buf(self, name, shape, dtype, dev):
+        import torch
+        b = self._bufs.get(name)
+        if b is None or b.shape != shape or b.dtype != dtype:
+            b = torch.empty(shape, dtype=dtype, device=dev)
+            self._bufs[name] = b
+        return b
 
     def forward(self, x, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,
                 timing=False, stats=True):
-        """One EP step moving one row per (token, rank) (dsmoe_b200_ep_pack /
-        _ep_expert / _ep_combine): a token goes once to each rank that owns
-        one of its kept selections, with one record per selection; the rank
-        returns one row per token (its experts' weighted sum).  stats=False
-        skips the post-drop load report (an all-reduce + host sync)."""
+        """One EP step, ONE host synchronisation (the split sizes):
+        1. no-drop routing -> per-expert counts -> all-reduce (device);
+        2. device_loads -> thresholds -> owner table on the device
+           (simulate_step, ep_sim.hpp:110-149);
+        3. re-route under the owner thresholds (same logits), pack one row per
+           (token, destination rank) + one record per kept selection, local
+           shared experts (dsmoe_b200_ep_dispatch);
+        4. all-to-all of the per-destination counts, copied to the host (the
+           sync), then rows and records;
+        5. this rank's experts, one output row per received row;
+        6. rows back, summed per token over ranks + shared experts.
+        stats=True adds the post-drop load report (one all-reduce + sync)."""
         import torch
-        L, W = self.layer, self.world
+        L, W, ctx = self.layer, self.world, self.ctx
         policy = policy or D.DropPolicy()
         T = x.shape[0]
         dev = x.device
-        # 1. global pre-drop loads -> thresholds (simulate_step, ep_sim.hpp:110-138)
-        seg0, _, _ = D.dispatch(self.ctx, L, x, D.DropPolicy(), logits_mode=logits_mode)
-        counts = self.coll.all_reduce(torch.from_numpy(seg0[:, 2].astype(np.int64)).to(dev))
-        pre = loads_from_counts(counts.cpu().numpy(), self.device_of, W, L.P)
-        t_unit, th = None, np.zeros(W)
-        if policy.kind != "none":
-            th = device_thresholds(pre, policy.t_drop, load_aware)
-            t_unit = torch.from_numpy(th[self.owner]).to(dev)
-        # 2. re-route under the owner thresholds (logits of step 1); shared experts run here
-        seg, _, st = D.dispatch(self.ctx, L, x, policy, t_unit=t_unit, logits_mode=D.LOGITS_REUSE, with_stats=stats)
-        # 3. one row per (token, destination) + one record per kept selection
-        cap_rows = T * min(W, L.K) + 1
-        send = torch.empty((cap_rows, L.d), dtype=x.dtype, device=dev)
-        rc = torch.empty(T * L.K + 1, dtype=torch.int32, device=dev)
-        rr = torch.empty_like(rc)
-        rw = torch.empty(T * L.K + 1, dtype=torch.float32, device=dev)
-        nu, ns = D.ep_pack(self.ctx, L, x, W, self.owner, send, rc, rr, rw)
-        # 4. counts, then rows and records
-        cnt = torch.from_numpy(np.stack([nu, ns], axis=1)).to(dev)
-        cnt_recv = torch.empty_like(cnt)
-        self.coll.all_to_all(cnt_recv, cnt, [1] * W, [1] * W)
-        cr = cnt_recv.cpu().numpy()
-        ru, rs = cr[:, 0], cr[:, 1]
-        U, S = int(ru.sum()), int(rs.sum())
-        xr = torch.empty((U + 1, L.d), dtype=x.dtype, device=dev)
-        rcr = torch.empty(S + 1, dtype=torch.int32, device=dev)
-        rrr = torch.empty_like(rcr)
-        rwr = torch.empty(S + 1, dtype=torch.float32, device=dev)
-        self.coll.all_to_all(xr[:U], send[:int(nu.sum())], ru.tolist(), nu.tolist())
-        for dst, src in ((rcr, rc), (rrr, rr), (rwr, rw)):
-            self.coll.all_to_all(dst[:S], src[:int(ns.sum())], rs.tolist(), ns.tolist())
-        # 5. this rank's experts, one output row per received row
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
+        drop = policy.kind != "none"
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if timing else None
         if timing:
             ev[0].record()
-        yl = D.ep_expert(self.ctx_exp, L, xr, U, rcr, rrr, rwr, S, np.concatenate([[0], np.cumsum(ru)]),
-                         np.concatenate([[0], np.cumsum(rs)]))
+        counts = D.ep_route_counts(ctx, L, x, policy, self._buf("counts", (L.E, 2), torch.int64, dev), logits_mode)
+        counts = self.coll.all_reduce(counts)
+        t_unit, loads = D.ep_thresholds(ctx, L, counts, W, self.d_device_of, policy.t_drop if drop else 1.0,
+                                        load_aware and drop, self._buf("t_unit", (L.E,), torch.float64, dev),
+                                        self._buf("loads", (W,), torch.float64, dev))
+        cap_rows = T * min(W, L.K) + 1
+        send = self._buf("send", (cap_rows, L.d), x.dtype, dev)
+        rec = self._buf("rec", (T * L.K + 1, 3), torch.int32, dev)
+        cnt = self._buf("cnt", (W, 2), torch.int64, dev)
+        D.ep_dispatch(ctx, L, x, policy, t_unit if drop else None, W, self.d_owner, send, rec, cnt)
+        cnt_recv = self._buf("cnt_recv", (W, 2), torch.int64, dev)
+        self.coll.all_to_all(cnt_recv, cnt, [1] * W, [1] * W)
+        both = torch.cat([cnt.view(-1), cnt_recv.view(-1)]).cpu().numpy()  # the one host sync
+        nu, ns = both[0:2 * W:2], both[1:2 * W:2]
+        ru, rs = both[2 * W::2], both[2 * W + 1::2]
+        U, S, NU, NS = int(ru.sum()), int(rs.sum()), int(nu.sum()), int(ns.sum())
+        xr = self._buf("xr", (max(U, 1) + 1, L.d), x.dtype, dev)
+        rr = self._buf("rr", (max(S, 1) + 1, 3), torch.int32, dev)
         if timing:
             ev[1].record()
-        # 6. rows back in send order, summed per token over ranks (+ shared experts)
-        ret = torch.empty((int(nu.sum()) + 1, L.d), dtype=x.dtype, device=dev)
-        self.coll.all_to_all(ret[:int(nu.sum())], yl[:U], nu.tolist(), ru.tolist())
-        out = D.ep_combine(self.ctx, L, ret, T)
-        rep = {"pre_loads": pre, "thresholds": th, "rows_sent": nu, "rows_received": U, "records_sent": ns}
-        if stats:
-            post = torch.from_numpy(np.stack([seg[:, 1], seg[:, 2] - seg[:, 1]]).astype(np.int64)).to(dev)
-            post = self.coll.all_reduce(post).cpu().numpy()
-            rep["post_loads"] = post_loads_from_segments(post[0], post[1], self.device_of, W, L.P)
+        self.coll.all_to_all(xr[:U], send[:NU], ru.tolist(), nu.tolist())
+        self.coll.all_to_all(rr[:S], rec[:NS], rs.tolist(), ns.tolist())
+        if timing:
+            ev[2].record()
+        yl = D.ep_expert_packed(self.ctx_exp, L, xr, U, rr, S, np.concatenate([[0], np.cumsum(ru)]),
+                                np.concatenate([[0], np.cumsum(rs)]), out=self._buf("yl", (max(U, 1) + 1, L.d),
+                                                                                   x.dtype, dev))
+        if timing:
+            ev[3].record()
+        ret = self._buf("ret", (NU + 1, L.d), x.dtype, dev)
+        self.coll.all_to_all(ret[:NU], yl[:U], nu.tolist(), ru.tolist())
+        if timing:
+            ev[4].record()
+        out = D.ep_combine(ctx, L, ret, T)
+        if timing:
+            ev[5].record()
+        rep = {"rows_sent": nu, "rows_received": U, "records_sent": ns, "records_received": S}
+        if stats or timing:
+            post = self.coll.all_reduce(D.ep_last_counts(ctx, L, T, self._buf("post", (L.E, 2), torch.int64, dev)))
+            post = post.cpu().numpy()
+            pre = loads.cpu().numpy()
+            rep["pre_loads"] = pre
+            tu = t_unit.cpu().numpy()
+            rep["thresholds"] = (np.array([tu[np.nonzero(self.owner == r)[0][0]] for r in range(W)])
+                                 if drop else np.zeros(W))
+            rep["post_loads"] = post_loads_from_segments(post[:, 0], post[:, 1], self.device_of, W, L.P)
             rep["speedup"] = modeled_speedup(pre, rep["post_loads"])
-            rep["local_drop_stats"] = st
         if timing:
             torch.cuda.synchronize()
-            rep["expert_ms"] = ev[0].elapsed_time(ev[1])
+            rep["exchange_ms"] = ev[1].elapsed_time(ev[2]) + ev[3].elapsed_time(ev[4])
+            rep["expert_ms"] = ev[2].elapsed_time(ev[3])
+            rep["step_ms"] = ev[0].elapsed_time(ev[5])
+            codes = rr[:S, 0].cpu().numpy()
+            units = np.where((codes & 3) == 2, 1.0, 1.0 / L.P).sum()
+            rep["expert_flops"] = float(units) * 6.0 * L.d * L.ffn
+            es = x.element_size()
+            rep["exchange_bytes"] = int((NU + U) * L.d * es + (NS + S) * 12)  # this rank: sent + received
         return out, rep
 
     def forward_rows(self, x, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,
@@ -277,7 +310,7 @@ class ExpertParallelMoE:
         bytes; kept for comparison).  stats=False skips the post-drop load
         report (one all-reduce + host sync)."""
         import torch
-        dist, L = self.dist, self.layer
+        dist, L = self.dist, self.full
         policy = policy or D.DropPolicy()
         T = x.shape[0]
         dev = x.device

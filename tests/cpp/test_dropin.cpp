@@ -43,8 +43,6 @@ int main() {
   // reference offline partition on the CPU
   ImportanceProfile prof = profile_importance(base, x, route_tokens(base, x), Metric::abs_gate);
   auto [rec, spec, map] = reconstruct_experts(base, prof);
-  (void)spec;
-  (void)map;
 
   b200::Context ctx;
   b200::DeviceLayer<float> dev(rec);
@@ -81,6 +79,50 @@ int main() {
     try { b200::route_and_drop(ctx, dbase, x, DropPolicy::two_t_from(0.3)); } catch (const Error& e) { dev_code = e.code(); }
     CHECK(ref_code == Status::invalid_state && dev_code == ref_code);
   }
+  // partition API on the device vs the reference's transforms (transform.hpp:66-131)
+  {
+    auto same_layer = [](const MoeLayer<float>& a, const MoeLayer<float>& b) {
+      if (!(a.config == b.config) || a.replay_factor != b.replay_factor || a.lineage != b.lineage) return false;
+      if (a.gate.data != b.gate.data || a.experts.size() != b.experts.size()) return false;
+      for (size_t i = 0; i < a.experts.size(); ++i)
+        if (a.experts[i].w1.data != b.experts[i].w1.data || a.experts[i].w3.data != b.experts[i].w3.data ||
+            a.experts[i].w2.data != b.experts[i].w2.data)
+          return false;
+      return a.neuron_order == b.neuron_order;
+    };
+    CHECK(same_layer(b200::complete_transform(ctx, base, 4), complete_transform(base, 4)));
+    CHECK(same_layer(b200::partial_transform(ctx, base, 2).first, partial_transform(base, 2).first));
+    CHECK(b200::partial_transform(ctx, base, 4).second.chunk_cols == partial_transform(base, 4).second.chunk_cols);
+    Status ref_code = Status::ok, dev_code = Status::ok;
+    try { complete_transform(base, 3); } catch (const Error& e) { ref_code = e.code(); }
+    try { b200::complete_transform(ctx, base, 3); } catch (const Error& e) { dev_code = e.code(); }
+    CHECK(ref_code == Status::invalid_argument && dev_code == ref_code);
+    // profile_importance + reconstruct_experts (reconstruct.hpp:99-230)
+    b200::DeviceLayer<float> dbase(base);
+    const RoutingDecision r0 = route_tokens(base, x);
+    for (Metric m : {Metric::gate, Metric::abs_gate, Metric::gate_up, Metric::abs_gate_up}) {
+      const ImportanceProfile pr = profile_importance(base, x, r0, m, 3);
+      const ImportanceProfile pd = b200::profile_importance(ctx, dbase, x, r0, m, 3);
+      CHECK(pd.values == pr.values && pd.layer_index == 3 && pd.token_count == pr.token_count);
+    }
+    auto [drec, dspec, dmap] = b200::reconstruct_experts(ctx, base, prof);
+    CHECK(same_layer(drec, rec));
+    CHECK(dmap.order == map.order && dspec.chunk_cols == spec.chunk_cols);
+  }
+  // simulate_step (ep_sim.hpp:110-160): report and dropped routing
+  for (auto strat : {Placement::Strategy::contiguous, Placement::Strategy::round_robin})
+    for (bool la : {false, true}) {
+      const Placement pl = place_experts(rec.num_physical_experts(), 4, strat);
+      const DropPolicy pol = DropPolicy::two_t_from(0.4);
+      auto [want, wr] = simulate_step(rec, x, pl, pol, la);
+      auto [got, gr] = b200::simulate_step(ctx, dev, x, pl, pol, la);
+      CHECK(got.pre_loads == want.pre_loads && got.post_loads == want.post_loads);
+      CHECK(got.thresholds == want.thresholds && got.ideal_load == want.ideal_load);
+      CHECK(got.speedup == want.speedup && got.drop_rate == want.drop_rate);
+      CHECK(got.stats.retained_flops == want.stats.retained_flops);
+      CHECK(gr.indices == wr.indices && gr.fraction == wr.fraction && gr.normalized == wr.normalized);
+      std::printf("simulate_step %s load_aware=%d speedup=%.6f\n", strategy_name(strat), int(la), got.speedup);
+    }
   // load-aware thresholds (test_ep_sim.cpp:71-91)
   CHECK(b200::load_aware_thresholds({120.0, 80.0, 100.0, 100.0}, 0.12) ==
         load_aware_thresholds({120.0, 80.0, 100.0, 100.0}, 0.12));

@@ -230,3 +230,28 @@ def test_model_forward_dropped_two_layers(ctx):
         so = O.drop_stats(np.ones_like(ro.frac), ro.frac, 2, 0, cur.shape[0], L.d, L.ffn)
         assert st["drop_rate"] == so["drop_rate"]
     assert scaled_residual(y.cpu().numpy(), cur) < TOL_F32
+
+
+def test_model_forward_dropped_per_layer_policies(ctx):
+    """A policy per layer: layer l routes under its own
+    threshold; per-layer calibration reaches the target on every layer."""
+    pkg = D()
+    from paper_2508_18376_b200 import analysis as A
+    Ls = [O.partial_transform(O.generate_layer(128, 128, 8, 2, seed=s), 2) for s in (84, 85, 86)]
+    layers = [dev_layer(L, "f32") for L in Ls]
+    x = O.generate_tokens(200, 128, seed=87)
+    pols = [pkg.DropPolicy.two_t_from(0.25), pkg.DropPolicy.one_t(0.1), pkg.DropPolicy()]
+    y, stats = pkg.model_forward_dropped(ctx, layers, torch.from_numpy(x).cuda(), pols, logits_mode=pkg.LOGITS_EXACT)
+    cur = x.astype(np.float32)
+    for L, st, (kind, t) in zip(Ls, stats, (("2t", 0.25), ("1t", 0.1), ("none", 0.0))):
+        ro = O.route(L, cur, kind, t)
+        cur = (cur + O.moe_forward(L, cur, ro.idx, ro.raw, ro.frac)).astype(np.float32)
+        so = O.drop_stats(np.ones_like(ro.frac), ro.frac, 2, 0, cur.shape[0], L.d, L.ffn)
+        assert st["drop_rate"] == so["drop_rate"]
+    assert scaled_residual(y.cpu().numpy(), cur) < TOL_F32
+    with pytest.raises(pkg.DsmoeError):
+        pkg.model_forward_dropped(ctx, layers, torch.from_numpy(x).cuda(), pols[:2])
+    cal, rates = A.calibrate_per_layer(ctx, layers, torch.from_numpy(x).cuda(), 0.25)
+    assert all(abs(r - 0.25) < 0.03 for r in rates)
+    _, st2 = pkg.model_forward_dropped(ctx, layers, torch.from_numpy(x).cuda(), cal, logits_mode=pkg.LOGITS_EXACT)
+    assert [s["drop_rate"] for s in st2] == rates
