@@ -312,7 +312,7 @@ def run_reference(args, world):
     gate = make_weights(bc)[0] if skew else None
     xs = np.ascontiguousarray(bench_tokens(bc, 1024, skew=skew, gate=gate).float().numpy())
     t_drop, rate = ref_calibrate(R, xs, K, args.drop)
-    sample = args.cpu_sample or {"c2": 96, "c3": 8, "c4": 96, "c5": 8}[cfg]
+    sample = args.cpu_sample or {"c2": 256, "c3": 8, "c4": 256, "c5": 8}[cfg]
     x = np.ascontiguousarray(xs[:sample])
     setup_s = time.perf_counter() - t_setup
     ref_rate(R, x[:max(2, sample // 4)], K, t_drop, ncores)  # warm-up
