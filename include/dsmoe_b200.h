@@ -266,7 +266,11 @@ int dsmoe_b200_ep_combine(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, co
  *                     into send_rows and one 3 x int32 record {expert*4+level,
  *                     row, raw-score bits} per kept selection into records,
  *                     counts (device, nranks x {rows, records} int64), and
- *                     evaluate the local shared experts; owner (device, E);
+ *                     evaluate the local shared experts; dest (device, 2E
+ *                     uint32): destination-rank bit masks of a full and of a
+ *                     major-only selection of each expert — the ranks holding
+ *                     its blocks / its block 0, so an expert's sub-blocks may
+ *                     live on different ranks (S-ETP placement);
  *   ep_expert_packed  dsmoe_b200_ep_expert with the interleaved records.
  * None of them synchronises the host. */
 int dsmoe_b200_ep_route_counts(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
@@ -275,7 +279,7 @@ int dsmoe_b200_ep_last_counts(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer
 int dsmoe_b200_ep_thresholds(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const int64_t* counts, int devices,
                              const int32_t* device_of, double t_max, int load_aware, double* t_unit, double* loads);
 int dsmoe_b200_ep_dispatch(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
-                           const dsmoe_b200_policy* policy, int logits_mode, int nranks, const int32_t* owner,
+                           const dsmoe_b200_policy* policy, int logits_mode, int nranks, const uint32_t* dest,
                            void* send_rows, int32_t* records, int64_t* counts);
 int dsmoe_b200_ep_expert_packed(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* rows, long U,
                                 const int32_t* records, long S, const int64_t* src_row_base,
@@ -288,6 +292,15 @@ int dsmoe_b200_ep_expert_packed(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* lay
  * reconstruct, transform) reject it with DSMOE_E_INVALID_STATE. */
 int dsmoe_b200_layer_shard(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, int unit_lo, int unit_hi,
                            dsmoe_b200_layer** out);
+/* The general shard: held (host, E*P flags) marks the physical blocks this
+ * rank stores — e.g. Placement::device_of == rank for any placement
+ * (ep_sim.hpp:38-54), including S-ETP placements that put the sub-blocks
+ * of one expert on different ranks.  A unit's sub-blocks are its held
+ * blocks in order; a full selection evaluates them all, a major-only one
+ * block 0 (dsmoe_b200_ep_dispatch's dest masks send it only where block 0
+ * lives). */
+int dsmoe_b200_layer_shard_blocks(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const uint8_t* held,
+                                  dsmoe_b200_layer** out);
 
 /* dsmoe_b200_forward with flags.  DSMOE_B200_RESIDUAL: out = x + moe(x), the
  * residual step of model_forward_dropped (dropping.hpp:271) fused into the

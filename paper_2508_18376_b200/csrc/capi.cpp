@@ -166,14 +166,33 @@ struct dsmoe_b200_layer {
   // block, any fraction per slot, moe.hpp:239-271) runs on the same kernels
   mutable dsmoe_b200_layer* bview = nullptr;
   mutable std::mutex bview_mu;
-  // expert shard (expert parallelism): only routed units [shard_lo, shard_hi)
-  // (and the shared experts) hold weights; the gate is whole
-  int shard_lo = 0, shard_hi = 0;
+  // expert shard (expert parallelism): held[b] marks the physical blocks this
+  // layer stores (empty = all).  A routed unit's sub-blocks are its held
+  // blocks in order, so the blocks of one expert may live on different ranks
+  // (S-ETP placement); the gate and the shared experts are whole.
+  std::vector<char> held;
+  DevBuf d_hold;  // per routed unit: bit 0 any block held, bit 1 block 0 held
   ~dsmoe_b200_layer();
 
   int nunits() const { return E + S; }
-  bool sharded() const { return shard_lo > 0 || shard_hi < E; }
-  bool holds(int unit) const { return unit >= E || (unit >= shard_lo && unit < shard_hi); }
+  bool held_block(int b) const { return held.empty() || held[static_cast<size_t>(b)]; }
+  bool sharded() const {
+    for (char h : held)
+      if (!h) return true;
+    return false;
+  }
+  bool holds(int unit) const {
+    if (unit >= E || held.empty()) return true;
+    for (int p = 0; p < P; ++p)
+      if (held[static_cast<size_t>(unit * P + p)]) return true;
+    return false;
+  }
+  // index of block (e, p) among unit e's stored sub-blocks
+  int local_sub(int b) const {
+    int q = 0;
+    for (int i = (b / P) * P; i < b; ++i) q += held_block(i) ? 1 : 0;
+    return q;
+  }
   // sub-block p of routed unit e <- block (e, p) columns [col0, col0 + n)
   void check_ready() const {
     require(gate_set, DSMOE_E_INVALID_STATE, "layer: gate weights not set");
@@ -203,8 +222,8 @@ int pair_mask(const dsmoe_b200_layer* L) {
 
 namespace {
 
-void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool ragged = false, int shard_lo = 0,
-                 int shard_hi = -1) {
+void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool ragged = false,
+                 const char* held = nullptr) {
   require(c.d_model >= 1, DSMOE_E_INVALID_ARGUMENT, "config: d_model must be >= 1");
   require(c.d_ffn >= 2, DSMOE_E_INVALID_ARGUMENT, "config: d_ffn must be >= 2");
   require(c.num_experts >= 1, DSMOE_E_INVALID_ARGUMENT, "config: num_experts must be >= 1");
@@ -226,11 +245,8 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool rag
   L->P = c.replay_factor;
   L->prenorm = c.gate_prenormalized != 0;
   L->dtype = c.dtype;
-  L->shard_lo = shard_lo;
-  L->shard_hi = shard_hi < 0 ? c.num_experts : shard_hi;
-  require(L->shard_lo >= 0 && L->shard_lo < L->shard_hi && L->shard_hi <= c.num_experts, DSMOE_E_INVALID_ARGUMENT,
-          "layer: shard range must satisfy 0 <= lo < hi <= num_experts");
   const int P = L->P;
+  if (held) L->held.assign(held, held + static_cast<size_t>(c.num_experts) * c.replay_factor);
   for (int b = 0; b < L->E * P; ++b) L->widths.push_back(c.block_widths ? c.block_widths[b] : c.d_ffn / P);
   for (int s = 0; s < L->S; ++s) L->swidths.push_back(c.shared_widths ? c.shared_widths[s] : c.d_ffn);
   for (int e = 0; e < L->E; ++e) {
@@ -254,11 +270,14 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool rag
     } else if (P == 1) {
       // virtual split at ceil(w/2): fraction 0.5 evaluates the first half
       // (moe.hpp:264), i.e. sub-block 0; the routed layer needs no copy.
-      const int wd = L->widths[e], h0 = (wd + 1) / 2;
-      w = {h0};
-      if (wd - h0 > 0) w.push_back(wd - h0);
+      if (L->held_block(e)) {
+        const int wd = L->widths[e], h0 = (wd + 1) / 2;
+        w = {h0};
+        if (wd - h0 > 0) w.push_back(wd - h0);
+      }
     } else {
-      for (int p = 0; p < P; ++p) w.push_back(L->widths[e * P + p]);
+      for (int p = 0; p < P; ++p)
+        if (L->held_block(e * P + p)) w.push_back(L->widths[e * P + p]);
     }
     u.nsub = static_cast<int>(w.size());
     u.hwidth = 0;
@@ -270,7 +289,7 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool rag
       chunks += (u.sub_wpad[p] + kChunk - 1) / kChunk;
     }
     u.shared = sh ? 1 : 0;
-    if (L->holds(e)) {  // units outside an expert shard keep their shape but no storage
+    if (!w.empty()) {  // units without held blocks (expert shards) have no storage
       u.w13_row = static_cast<int>(row);
       u.w2t_row = w2t_units++ * L->d;
       row += 2LL * u.hwidth;
@@ -306,7 +325,14 @@ void layer_build(dsmoe_b200_layer* L, const dsmoe_b200_layer_config& c, bool rag
   }
   L->block_set.assign(static_cast<size_t>(L->E * P), 0);
   for (int b = 0; b < L->E * P; ++b)
-    if (!L->holds(b / P)) L->block_set[static_cast<size_t>(b)] = 1;  // not part of this shard
+    if (!L->held_block(b)) L->block_set[static_cast<size_t>(b)] = 1;  // not part of this shard
+  if (L->sharded()) {
+    std::vector<unsigned char> hold(static_cast<size_t>(L->E));
+    for (int e = 0; e < L->E; ++e)
+      hold[static_cast<size_t>(e)] = (L->holds(e) ? 1 : 0) | (L->held_block(e * P) ? 2 : 0);
+    L->d_hold.ensure(hold.size());
+    cuda_check(cudaMemcpy(L->d_hold.p, hold.data(), hold.size(), cudaMemcpyHostToDevice), "upload shard");
+  }
   L->shared_set.assign(static_cast<size_t>(L->S), 0);
 }
 
@@ -1112,7 +1138,7 @@ int dsmoe_b200_layer_set_block(dsmoe_b200_layer* L, int b, const void* w1, const
   return guarded([&] {
     require(L && w1 && w3 && w2, DSMOE_E_INVALID_ARGUMENT, "null argument");
     require(b >= 0 && b < L->E * L->P, DSMOE_E_INVALID_ARGUMENT, "block index out of range");
-    require(L->holds(b / L->P), DSMOE_E_INVALID_ARGUMENT, "block is not part of this expert shard");
+    require(L->held_block(b), DSMOE_E_INVALID_ARGUMENT, "block is not part of this expert shard");
     require(src_dtype == 0 || src_dtype == 1, DSMOE_E_INVALID_ARGUMENT, "bad source dtype");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int wd = L->widths[b];
@@ -1124,7 +1150,7 @@ int dsmoe_b200_layer_set_block(dsmoe_b200_layer* L, int b, const void* w1, const
       pack_sub(L, e, 0, a1.p, a3.p, a2.p, wd, nullptr, 0, src_dtype, s);
       if (u.nsub > 1) pack_sub(L, e, 1, a1.p, a3.p, a2.p, wd, nullptr, u.sub_w[0], src_dtype, s);
     } else {
-      pack_sub(L, e, p, a1.p, a3.p, a2.p, wd, nullptr, 0, src_dtype, s);
+      pack_sub(L, e, L->local_sub(b), a1.p, a3.p, a2.p, wd, nullptr, 0, src_dtype, s);
     }
     cuda_check(cudaStreamSynchronize(s), "sync");
     L->block_set[b] = 1;
@@ -1521,11 +1547,15 @@ int dsmoe_b200_ep_pack(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void*
     C->ep_send_token.ensure(static_cast<size_t>(T) * std::min(nranks, L->K) * 4 + 16);
     C->ep_cnt.ensure(static_cast<size_t>(2) * nchunks * nranks * 4);
     C->ep_tot.ensure(static_cast<size_t>(4) * nranks * 4 + 16);
-    C->ep_owner.ensure(static_cast<size_t>(L->E) * 4);
-    cuda_check(cudaMemcpyAsync(C->ep_owner.p, owner, static_cast<size_t>(L->E) * 4, cudaMemcpyHostToDevice, s), "H2D");
+    // expert-aligned placement: a selection of expert e goes to owner[e] whatever its level
+    std::vector<uint32_t> dest(static_cast<size_t>(2) * L->E);
+    for (int e = 0; e < L->E; ++e) dest[2 * e] = dest[2 * e + 1] = 1u << owner[e];
+    C->ep_owner.ensure(dest.size() * 4);
+    cuda_check(cudaMemcpyAsync(C->ep_owner.p, dest.data(), dest.size() * 4, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaStreamSynchronize(s), "sync");
     int* cnt = C->ep_cnt.as<int>();
     int* r_total = C->ep_tot.as<int>() + 4 * nranks;
-    launch_check(launch_ep_pack(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), C->ep_owner.as<int32_t>(), T, L->K,
+    launch_check(launch_ep_pack(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), C->ep_owner.as<uint32_t>(), T, L->K,
                                 nranks, cnt, cnt + nchunks * nranks, C->ep_tot.as<int>(), C->ep_send_token.as<int32_t>(),
                                 C->ep_pos_td.as<int32_t>(), rec_code, rec_row, rec_raw, r_total, num_sms(), s),
                  "ep_pack");
@@ -1601,7 +1631,8 @@ void ep_expert_impl(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* ro
     cuda_check(cudaMemsetAsync(C->cnt_chunk.p, 0, static_cast<size_t>(nchunks) * 2 * L->E * 4, s), "memset");
     const long long* b = C->ep_base.as<long long>();
     launch_check(launch_ep_local_routing(rec_code, rec_row, rec_raw, S, rec_stride, b, b + nranks + 1, nranks, L->K,
-                                         L->E, L->shard_lo, L->shard_hi, C->sel_code.as<int32_t>(),
+                                         L->E, L->sharded() ? L->d_hold.as<unsigned char>() : nullptr,
+                                         C->sel_code.as<int32_t>(),
                                          C->sel_raw.as<float>(), C->cnt_chunk.as<int>(),
                                          C->counters.as<unsigned long long>(), num_sms(), s),
                  "ep local routing");
@@ -1674,13 +1705,13 @@ int dsmoe_b200_ep_thresholds(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const
 }
 
 int dsmoe_b200_ep_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
-                           const dsmoe_b200_policy* policy, int logits_mode, int nranks, const int32_t* owner,
+                           const dsmoe_b200_policy* policy, int logits_mode, int nranks, const uint32_t* dest,
                            void* send_rows, int32_t* records, int64_t* counts) {
   return guarded([&] {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
     require_layer(L);
     require(nranks >= 1 && nranks <= 32, DSMOE_E_INVALID_ARGUMENT, "ep_dispatch: 1 <= nranks <= 32");
-    require(T >= 1 && x && owner && send_rows && records && counts, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(T >= 1 && x && dest && send_rows && records && counts, DSMOE_E_INVALID_ARGUMENT, "null argument");
     g_launches = 0;
     const PolicyResolved pol = resolve_policy(L, policy);
     C->ensure(L, T);
@@ -1693,7 +1724,7 @@ int dsmoe_b200_ep_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
     C->ep_tot.ensure(static_cast<size_t>(4) * nranks * 4 + 16);
     int* cnt = C->ep_cnt.as<int>();
     int* r_total = C->ep_tot.as<int>() + 4 * nranks;
-    launch_check(launch_ep_pack(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), owner, T, L->K, nranks, cnt,
+    launch_check(launch_ep_pack(C->sel_code.as<int32_t>(), C->sel_raw.as<float>(), dest, T, L->K, nranks, cnt,
                                 cnt + nchunks * nranks, C->ep_tot.as<int>(), C->ep_send_token.as<int32_t>(),
                                 C->ep_pos_td.as<int32_t>(), records, records + 1, reinterpret_cast<float*>(records + 2),
                                 r_total, num_sms(), s, 3, reinterpret_cast<long long*>(counts)),
@@ -1730,27 +1761,59 @@ int dsmoe_b200_ep_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
   });
 }
 
-int dsmoe_b200_layer_shard(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int unit_lo, int unit_hi,
-                           dsmoe_b200_layer** out) {
+int dsmoe_b200_layer_shard_blocks(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const uint8_t* held,
+                                  dsmoe_b200_layer** out) {
   return guarded([&] {
-    require(C && out, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(C && out && held, DSMOE_E_INVALID_ARGUMENT, "null argument");
     require_whole(L);
+    const int P = L->P;
+    std::vector<char> h(static_cast<size_t>(L->E) * P);
+    bool any = false;
+    for (size_t b = 0; b < h.size(); ++b) any |= (h[b] = held[b] ? 1 : 0) != 0;
+    require(any, DSMOE_E_INVALID_ARGUMENT, "layer_shard: the shard holds no expert block");
     std::vector<int32_t> widths(L->widths.begin(), L->widths.end()), swidths(L->swidths.begin(), L->swidths.end());
-    dsmoe_b200_layer_config cfg{L->d, L->ffn, L->E, L->K, L->S, L->prenorm, L->P, L->dtype, widths.data(),
+    dsmoe_b200_layer_config cfg{L->d, L->ffn, L->E, L->K, L->S, L->prenorm, P, L->dtype, widths.data(),
                                 swidths.empty() ? nullptr : swidths.data()};
     auto* R = new dsmoe_b200_layer;
     try {
-      layer_build(R, cfg, false, unit_lo, unit_hi);
+      layer_build(R, cfg, false, h.data());
       std::vector<int> src_unit(static_cast<size_t>(L->nunits())), gmap(static_cast<size_t>(L->E));
       for (int v = 0; v < L->nunits(); ++v) src_unit[static_cast<size_t>(v)] = v;
       for (int e = 0; e < L->E; ++e) gmap[static_cast<size_t>(e)] = e;
       std::vector<float> scale(static_cast<size_t>(L->nunits()), 1.0f);
-      regroup(L, R, src_unit, scale, [](int, int n) { return n; }, gmap, C->stream);
+      // dst neuron n of unit v (over its held blocks) -> src neuron (over all blocks)
+      auto nmap = [L, R, P](int v, int n) {
+        if (v >= L->E || P == 1) return n;
+        int off = 0;
+        for (int p = 0; p < P; ++p) {
+          const int w = L->widths[static_cast<size_t>(v * P + p)];
+          if (R->held_block(v * P + p)) {
+            if (n < w) return off + n;
+            n -= w;
+          }
+          off += w;
+        }
+        return off;  // unreachable for n inside the unit
+      };
+      regroup(L, R, src_unit, scale, nmap, gmap, C->stream);
     } catch (...) {
       delete R;
       throw;
     }
     *out = R;
+  });
+}
+
+int dsmoe_b200_layer_shard(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int unit_lo, int unit_hi,
+                           dsmoe_b200_layer** out) {
+  return guarded([&] {
+    require(L != nullptr, DSMOE_E_INVALID_ARGUMENT, "null layer");
+    require(unit_lo >= 0 && unit_lo < unit_hi && unit_hi <= L->E, DSMOE_E_INVALID_ARGUMENT,
+            "layer_shard: need 0 <= lo < hi <= num_experts");
+    std::vector<uint8_t> held(static_cast<size_t>(L->E) * L->P, 0);
+    for (int b = unit_lo * L->P; b < unit_hi * L->P; ++b) held[static_cast<size_t>(b)] = 1;
+    const int rc = dsmoe_b200_layer_shard_blocks(C, L, held.data(), out);
+    if (rc != DSMOE_OK) fail(rc, g_last_error);
   });
 }
 

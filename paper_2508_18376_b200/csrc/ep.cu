@@ -34,7 +34,8 @@ constexpr int kMaxDest = 32;
 struct PackArgs {
   const int32_t* sel_code;  // T x K: unit * 4 + level, -1 dropped
   const float* sel_raw;     // T x K
-  const int32_t* owner;     // unit -> destination rank
+  const uint32_t* dest;     // 2 x unit: destination-rank masks of a full / a major-only selection
+                            // (the holders of all the unit's blocks / of its block 0)
   int T, K, N, nchunks;
   int* cnt_u;               // nchunks x N  (in place -> exclusive offsets)
   int* cnt_s;               // nchunks x N
@@ -56,16 +57,17 @@ __global__ void __launch_bounds__(kPackChunk) ep_pack_kernel(const PackArgs a) {
   __shared__ int base_u[kMaxDest], base_s[kMaxDest];
   const int N = a.N, K = a.K;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  auto token_info = [&](int t, uint32_t& mask, int* cnt) {  // destinations of t, selections per destination
+  auto dest_of = [&](int c) { return a.dest[2 * (c >> 2) + ((c & 3) == 2 ? 0 : 1)]; };
+  auto token_info = [&](int t, uint32_t& mask, int* cnt) {  // destinations of t, records per destination
     mask = 0u;
     for (int d = 0; d < N; ++d) cnt[d] = 0;
     if (t >= a.T) return;
     for (int s = 0; s < K; ++s) {
       const int c = a.sel_code[static_cast<long long>(t) * K + s];
       if (c < 0) continue;
-      const int d = a.owner[c >> 2];
-      mask |= 1u << d;
-      ++cnt[d];
+      const uint32_t m = dest_of(c);
+      mask |= m;
+      for (int d = 0; d < N; ++d) cnt[d] += (m >> d) & 1u;
     }
   };
   // ---- phase 1: per-chunk counts
@@ -167,27 +169,29 @@ __global__ void __launch_bounds__(kPackChunk) ep_pack_kernel(const PackArgs a) {
           a.pos_td[q] = -1;
         }
       }
-      for (int s = 0; s < K; ++s) {  // records in slot order
+      for (int s = 0; s < K; ++s) {  // records in slot order, one per destination holding a needed block
         const long long i = static_cast<long long>(t) * K + s;
         const int c = a.sel_code[i];
         if (c < 0) continue;
-        const int d = a.owner[c >> 2];
-        const long long r = static_cast<long long>(rec_next[d]++) * a.rec_stride;
-        a.rec_code[r] = c;
-        a.rec_row[r] = a.pos_td[static_cast<long long>(t) * N + d] - base_u[d];
-        a.rec_raw[r] = a.sel_raw[i];
+        for (uint32_t m = dest_of(c); m; m &= m - 1u) {
+          const int d = __ffs(m) - 1;
+          const long long r = static_cast<long long>(rec_next[d]++) * a.rec_stride;
+          a.rec_code[r] = c;
+          a.rec_row[r] = a.pos_td[static_cast<long long>(t) * N + d] - base_u[d];
+          a.rec_raw[r] = a.sel_raw[i];
+        }
       }
     }
     __syncthreads();
   }
 }
 
-int launch_ep_pack(const int32_t* sel_code, const float* sel_raw, const int32_t* owner, int T, int K, int N,
+int launch_ep_pack(const int32_t* sel_code, const float* sel_raw, const uint32_t* dest, int T, int K, int N,
                    int* cnt_u, int* cnt_s, int* tot, int32_t* send_token, int32_t* pos_td, int32_t* rec_code,
                    int32_t* rec_row, float* rec_raw, int* r_total, int num_sms, cudaStream_t stream, int rec_stride,
                    long long* counts_out) {
   if (N < 1 || N > kMaxDest || K > 16) return -1;
-  PackArgs a{sel_code, sel_raw, owner, T, K, N, (T + kPackChunk - 1) / kPackChunk, cnt_u, cnt_s, tot, send_token,
+  PackArgs a{sel_code, sel_raw, dest, T, K, N, (T + kPackChunk - 1) / kPackChunk, cnt_u, cnt_s, tot, send_token,
              pos_td, rec_code, rec_row, rec_raw, r_total, rec_stride, counts_out};
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ep_pack_kernel, kPackChunk, 0);
@@ -210,7 +214,7 @@ __global__ void ep_local_routing_kernel(const int32_t* __restrict__ rec_code, co
                                         const float* __restrict__ rec_raw, long long S, int stride,
                                         const long long* __restrict__ src_rec_base,
                                         const long long* __restrict__ src_row_base, int N, int K, int E,
-                                        int unit_lo, int unit_hi, int32_t* __restrict__ sel_code,
+                                        const unsigned char* __restrict__ hold, int32_t* __restrict__ sel_code,
                                         float* __restrict__ sel_raw, int* __restrict__ cnt_chunk,
                                         unsigned long long* __restrict__ flags) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < S;
@@ -224,7 +228,10 @@ __global__ void ep_local_routing_kernel(const int32_t* __restrict__ rec_code, co
     const long long row = src_row_base[src] + row_local;
     const int c = rec_code[i * stride];
     const int unit = c >> 2, level = c & 3;
-    if (unit < unit_lo || unit >= unit_hi || j >= K) {  // an expert this rank does not hold
+    // an expert block this rank does not hold: a full selection needs any of
+    // the unit's blocks here, a major-only one its block 0
+    const bool ok = unit >= 0 && unit < E && j < K && (!hold || (hold[unit] & (level == 2 ? 1 : 2)));
+    if (!ok) {
       atomicOr(&flags[2], 4ull);
       atomicOr(&flags[4], 4ull);
       continue;
@@ -237,13 +244,13 @@ __global__ void ep_local_routing_kernel(const int32_t* __restrict__ rec_code, co
 
 int launch_ep_local_routing(const int32_t* rec_code, const int32_t* rec_row, const float* rec_raw, long long S,
                             int stride, const long long* src_rec_base, const long long* src_row_base, int N, int K,
-                            int E, int unit_lo, int unit_hi, int32_t* sel_code, float* sel_raw, int* cnt_chunk,
+                            int E, const unsigned char* hold, int32_t* sel_code, float* sel_raw, int* cnt_chunk,
                             unsigned long long* flags, int num_sms, cudaStream_t stream) {
   if (S <= 0) return 0;
   const long long b = (S + 255) / 256;
   ep_local_routing_kernel<<<static_cast<int>(b < num_sms * 8 ? b : num_sms * 8), 256, 0, stream>>>(
-      rec_code, rec_row, rec_raw, S, stride, src_rec_base, src_row_base, N, K, E, unit_lo, unit_hi, sel_code, sel_raw,
-      cnt_chunk, flags);
+      rec_code, rec_row, rec_raw, S, stride, src_rec_base, src_row_base, N, K, E, hold, sel_code, sel_raw, cnt_chunk,
+      flags);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

@@ -93,13 +93,13 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
 int gemm_tc_store_box_cols();  // TMA-store box width the gemm_tc build expects (64: SW128, 32: SW64)
 
 // ep.cu (EP with one row per (token, destination rank))
-int launch_ep_pack(const int32_t* sel_code, const float* sel_raw, const int32_t* owner, int T, int K, int N,
+int launch_ep_pack(const int32_t* sel_code, const float* sel_raw, const uint32_t* dest, int T, int K, int N,
                    int* cnt_u, int* cnt_s, int* tot, int32_t* send_token, int32_t* pos_td, int32_t* rec_code,
                    int32_t* rec_row, float* rec_raw, int* r_total, int num_sms, cudaStream_t stream,
                    int rec_stride = 1, long long* counts_out = nullptr);
 int launch_ep_local_routing(const int32_t* rec_code, const int32_t* rec_row, const float* rec_raw, long long S,
                             int stride, const long long* src_rec_base, const long long* src_row_base, int N, int K,
-                            int E, int unit_lo, int unit_hi, int32_t* sel_code, float* sel_raw, int* cnt_chunk,
+                            int E, const unsigned char* hold, int32_t* sel_code, float* sel_raw, int* cnt_chunk,
                             unsigned long long* flags, int num_sms, cudaStream_t stream);
 int launch_ep_counts(const int* cnt_chunk, int nchunks, int E, long long* out, cudaStream_t stream);
 int launch_ep_thresholds(const long long* counts, int E, int P, int D, const int32_t* device_of, double t_max,

@@ -139,6 +139,7 @@ SYMBOLS = {
     "dsmoe_b200_ep_expert_packed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_long, C.c_void_p, C.c_long,
                                               C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "dsmoe_b200_layer_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "dsmoe_b200_layer_shard_blocks": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     "dsmoe_b200_transform": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "dsmoe_b200_layer_widths": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsmoe_b200_layer_get_gate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
@@ -720,14 +721,16 @@ def ep_thresholds(ctx: Context, layer: MoeLayer, counts, devices: int, device_of
     return t_unit, loads
 
 
-def ep_dispatch(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None, t_unit, nranks: int, owner, send_rows,
+def ep_dispatch(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None, t_unit, nranks: int, dest, send_rows,
                 records, counts, logits_mode=LOGITS_REUSE):
     """Re-route under the owner thresholds, pack one row per (token,
-    destination) + one 3 x int32 record per kept selection, counts (nranks x
-    2 int64: rows, records), local shared experts; no host sync."""
+    destination) + one 3 x int32 record per (kept selection, destination),
+    counts (nranks x 2 int64: rows, records), local shared experts; no host
+    sync.  dest: E x 2 int32 (bit masks) CUDA tensor — the ranks a full /
+    a major-only selection of each expert goes to."""
     x = _x(x, layer)
     _chk(lib().dsmoe_b200_ep_dispatch(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
-                                      C.byref((policy or DropPolicy()).c(t_unit)), logits_mode, nranks, _p(owner),
+                                      C.byref((policy or DropPolicy()).c(t_unit)), logits_mode, nranks, _p(dest),
                                       _p(send_rows), _p(records), _p(counts)))
 
 
@@ -740,6 +743,16 @@ def ep_expert_packed(ctx: Context, layer: MoeLayer, rows, U: int, records, S: in
     sb = np.ascontiguousarray(src_rec_base, np.int64)
     _chk(lib().dsmoe_b200_ep_expert_packed(ctx.h, layer.h, C.c_void_p(rows.data_ptr()), U, _p(records), S,
                                            rb.ctypes.data, sb.ctypes.data, len(rb) - 1, C.c_void_p(out.data_ptr())))
+    return out
+
+
+def layer_shard_blocks(ctx: Context, layer: MoeLayer, held) -> MoeLayer:
+    """An expert shard holding the physical blocks flagged in `held` (E*P)."""
+    h = C.c_void_p()
+    hm = np.ascontiguousarray(held, np.uint8)
+    _chk(lib().dsmoe_b200_layer_shard_blocks(ctx.h, layer.h, hm.ctypes.data, C.byref(h)))
+    out = MoeLayer._wrap(h, layer)
+    out.shard = tuple(np.nonzero(hm)[0].tolist())
     return out
 
 

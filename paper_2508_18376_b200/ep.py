@@ -194,24 +194,30 @@ class ExpertParallelMoE:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        if strategy != "contiguous":
-            raise D.DsmoeError(1, "expert-parallel data path needs contiguous placement")
-        self.device_of = block_devices(layer.E, layer.P, self.world, strategy)
-        if not expert_aligned(self.device_of, layer.P):
-            raise D.DsmoeError(1, "expert-parallel data path: an expert's sub-blocks straddle two ranks "
-                                  "(contiguous placement needs E*P/world to be a multiple of P)")
-        self.owner = owner_of_experts(layer.E, layer.P, self.world, strategy)
+        W, P = self.world, layer.P
+        # Placement::device_of of the physical blocks (ep_sim.hpp:38-54): any
+        # placement, including ones that put an expert's sub-blocks on
+        # different ranks (S-ETP; contiguous with E*P/W odd)
+        self.device_of = block_devices(layer.E, P, W, strategy)
+        self.aligned = expert_aligned(self.device_of, P)
+        self.owner = owner_of_experts(layer.E, P, W, strategy)  # threshold owner: block 0's device
+        self.held = (self.device_of == self.rank).astype(np.uint8)
         self.local = np.nonzero(self.owner == self.rank)[0]
+        dv = self.device_of.reshape(-1, P)
+        dest = np.zeros((layer.E, 2), np.int64)
+        for p in range(P):
+            dest[:, 0] |= 1 << dv[:, p]       # a full selection: every rank holding one of its blocks
+        dest[:, 1] = 1 << dv[:, 0]             # a major-only selection: the rank holding block 0
         self.ctx = D.Context()
         self.ctx_exp = D.Context()
         self.full = layer
-        if shard and self.world > 1:
-            layer = D.layer_shard(self.ctx, layer, int(self.local[0]), int(self.local[-1]) + 1)
+        if shard and W > 1:
+            layer = D.layer_shard_blocks(self.ctx, layer, self.held)
         self.layer = layer
         self.coll = _Coll(dist, group)
         dev = torch.device("cuda", torch.cuda.current_device())
         self.d_device_of = torch.from_numpy(self.device_of.astype(np.int32)).to(dev)
-        self.d_owner = torch.from_numpy(self.owner.astype(np.int32)).to(dev)
+        self.d_dest = torch.from_numpy(dest.astype(np.uint32).view(np.int32)).to(dev)
         self._bufs = {}
 
     def _buf(self, name, shape, dtype, dev):
@@ -250,11 +256,11 @@ class ExpertParallelMoE:
         t_unit, loads = D.ep_thresholds(ctx, L, counts, W, self.d_device_of, policy.t_drop if drop else 1.0,
                                         load_aware and drop, self._buf("t_unit", (L.E,), torch.float64, dev),
                                         self._buf("loads", (W,), torch.float64, dev))
-        cap_rows = T * min(W, L.K) + 1
+        cap_rows = T * min(W, L.K * L.P) + 1  # one row per (token, destination rank)
         send = self._buf("send", (cap_rows, L.d), x.dtype, dev)
-        rec = self._buf("rec", (T * L.K + 1, 3), torch.int32, dev)
+        rec = self._buf("rec", (T * L.K * min(W, L.P) + 1, 3), torch.int32, dev)
         cnt = self._buf("cnt", (W, 2), torch.int64, dev)
-        D.ep_dispatch(ctx, L, x, policy, t_unit if drop else None, W, self.d_owner, send, rec, cnt)
+        D.ep_dispatch(ctx, L, x, policy, t_unit if drop else None, W, self.d_dest, send, rec, cnt)
         cnt_recv = self._buf("cnt_recv", (W, 2), torch.int64, dev)
         self.coll.all_to_all(cnt_recv, cnt, [1] * W, [1] * W)
         both = torch.cat([cnt.view(-1), cnt_recv.view(-1)]).cpu().numpy()  # the one host sync
@@ -287,9 +293,7 @@ class ExpertParallelMoE:
             post = post.cpu().numpy()
             pre = loads.cpu().numpy()
             rep["pre_loads"] = pre
-            tu = t_unit.cpu().numpy()
-            rep["thresholds"] = (np.array([tu[np.nonzero(self.owner == r)[0][0]] for r in range(W)])
-                                 if drop else np.zeros(W))
+            rep["thresholds"] = device_thresholds(pre, policy.t_drop, load_aware) if drop else np.zeros(W)
             rep["post_loads"] = post_loads_from_segments(post[:, 0], post[:, 1], self.device_of, W, L.P)
             rep["speedup"] = modeled_speedup(pre, rep["post_loads"])
         if timing:
@@ -297,9 +301,11 @@ class ExpertParallelMoE:
             rep["exchange_ms"] = ev[1].elapsed_time(ev[2]) + ev[3].elapsed_time(ev[4])
             rep["expert_ms"] = ev[2].elapsed_time(ev[3])
             rep["step_ms"] = ev[0].elapsed_time(ev[5])
+            # this rank's expert FLOPs: 6 d x (the widths of the blocks it holds that each record needs)
             codes = rr[:S, 0].cpu().numpy()
-            units = np.where((codes & 3) == 2, 1.0, 1.0 / L.P).sum()
-            rep["expert_flops"] = float(units) * 6.0 * L.d * L.ffn
+            bw = np.asarray(self.full.widths()[0], np.float64).reshape(-1, L.P) * self.held.reshape(-1, L.P)
+            unit, full = codes >> 2, (codes & 3) == 2
+            rep["expert_flops"] = float(6.0 * L.d * np.where(full, bw.sum(axis=1)[unit], bw[unit, 0]).sum())
             es = x.element_size()
             rep["exchange_bytes"] = int((NU + U) * L.d * es + (NS + S) * 12)  # this rank: sent + received
         return out, rep
@@ -310,6 +316,8 @@ class ExpertParallelMoE:
         bytes; kept for comparison).  stats=False skips the post-drop load
         report (one all-reduce + host sync)."""
         import torch
+        if not self.aligned:
+            raise D.DsmoeError(1, "forward_rows: the per-selection path needs expert-aligned placement")
         dist, L = self.dist, self.full
         policy = policy or D.DropPolicy()
         T = x.shape[0]

@@ -35,18 +35,18 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, load_aware, method, q):
+def _worker(rank, world, port, load_aware, method, q, strategy="contiguous", E=12):
     import torch.distributed as dist
     import paper_2508_18376_b200 as D
     from paper_2508_18376_b200 import ep
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
-    rec, x = skewed()
+    rec, x = skewed(E=E)
     layer = D.MoeLayer(rec.d, rec.ffn, rec.E, rec.K, rec.gate, rec.blocks, rec.shared, replay_factor=rec.P,
                        dtype="f32")
     shard = np.array_split(np.arange(x.shape[0]), world)[rank]
-    m = ep.ExpertParallelMoE(layer)
+    m = ep.ExpertParallelMoE(layer, strategy=strategy)
     y, rep = getattr(m, method)(torch.from_numpy(x[shard]).cuda(), D.DropPolicy.two_t_from(0.3),
                                 load_aware=load_aware, logits_mode=D.LOGITS_EXACT)
     q.put((rank, y.cpu().numpy(), rep["pre_loads"], rep["thresholds"], rep["post_loads"], rep["speedup"]))
@@ -71,6 +71,38 @@ def test_ep_multiprocess_matches_simulate_step(world, load_aware, method):
         assert p.exitcode == 0
     rec, x = skewed()
     ref = O.simulate_step(O.gate_logits(x, rec.gate), rec, world, "2t", 0.3, load_aware=load_aware)
+    for _, _, pre, th, post, sp in res:
+        assert np.array_equal(pre, ref["pre_loads"])
+        assert np.array_equal(th, ref["thresholds"])
+        assert np.array_equal(post, ref["post_loads"])
+        assert sp == ref["speedup"]
+    ro = O.route_from_logits(O.gate_logits(x, rec.gate), rec.K, rec.P)
+    yo = O.moe_forward(rec, x, ref["idx"], ro.raw, ref["frac"])
+    y = np.concatenate([r[1] for r in res])
+    assert np.abs(y - yo).max() / np.abs(yo).max() < 1e-5
+
+
+@pytest.mark.parametrize("strategy,world,E", [("round_robin", 2, 12), ("contiguous", 4, 6)])
+def test_ep_sub_blocks_on_different_ranks(strategy, world, E):
+    """S-ETP placement: round-robin puts block 2e on rank 0
+    and its minor half 2e+1 on rank 1; contiguous with 3 blocks per rank
+    splits every other expert's halves.  A full selection goes to both
+    holders, each evaluating its half, a major-only one to block 0's rank;
+    loads, thresholds and outputs still equal simulate_step + moe_forward."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, True, "forward", q, strategy, E)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    rec, x = skewed(E=E)
+    ref = O.simulate_step(O.gate_logits(x, rec.gate), rec, world, "2t", 0.3, load_aware=True,
+                          round_robin=strategy == "round_robin")
     for _, _, pre, th, post, sp in res:
         assert np.array_equal(pre, ref["pre_loads"])
         assert np.array_equal(th, ref["thresholds"])
