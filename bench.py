@@ -548,6 +548,22 @@ def run_ep(args, dist, rank, world, local):
     _, rep = m.forward(x, pol, load_aware=True, timing=True)
     launches_per_step = D.total_launch_count() - l0
     ms_step = res["load_aware"]
+    # S-ETP placement: round-robin blocks put the major and
+    # minor halves of an expert on different ranks; a full selection then
+    # travels to both (measured next to the contiguous placement)
+    setp = None
+    if world > 1:
+        try:
+            m_rr = ep.ExpertParallelMoE(layer, strategy="round_robin")
+            ms_rr = time_steps(lambda: m_rr.forward(x, pol, load_aware=True, stats=False), args.steps,
+                               max(3, args.warmup), dist) / args.steps
+            _, rep_rr = m_rr.forward(x, pol, load_aware=True, timing=True)
+            setp = {"placement": "round_robin (halves of an expert on different ranks)", "ms_per_step": r4(ms_rr),
+                    "speedup_vs_contiguous": r4(ms_step / ms_rr), "modeled_speedup": r4(rep_rr["speedup"]),
+                    "exchange_bytes_rank0": rep_rr.get("exchange_bytes")}
+            del m_rr
+        except Exception as e:  # noqa: BLE001 — the line must still print
+            setp = {"error": str(e)}
     # e2e through the public API with host buffers
     xh = x.cpu().pin_memory()
     oh = torch.empty_like(xh).pin_memory()
@@ -603,7 +619,7 @@ def run_ep(args, dist, rank, world, local):
                    "speedup_load_aware_vs_no_drop": r4(res["no_drop"] / res["load_aware"]),
                    "speedup_load_aware_vs_uniform": r4(res["uniform"] / res["load_aware"]),
                    "pre_loads": rep["pre_loads"].tolist(), "post_loads": rep["post_loads"].tolist(),
-                   "modeled_speedup": r4(rep["speedup"])}}
+                   "modeled_speedup": r4(rep["speedup"]), "setp": setp}}
         json.dump({"line": line, "report": {k: (v.tolist() if hasattr(v, "tolist") else v) for k, v in rep.items()
                                             if k != "local_drop_stats"}},
                   open(detail_path(cfg, world), "w"), indent=1, default=str)

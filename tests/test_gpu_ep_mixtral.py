@@ -48,7 +48,7 @@ def _worker(rank, port, t_drop, load_aware, q):
     ctx = D.Context()
     layer, _ = B.build_layer("c5", ctx)
     m = ep.ExpertParallelMoE(layer)
-    assert m.layer.shard == (16 * rank, 16 * rank + 16)
+    assert m.layer.shard == tuple(range(32 * rank, 32 * rank + 32))  # this rank's 16 experts' 32 blocks
     del layer
     x = _tokens(rank).cuda()
     y, rep = m.forward(x, D.DropPolicy.two_t_from(t_drop), load_aware=load_aware, logits_mode=D.LOGITS_EXACT)
