@@ -81,17 +81,43 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml(self):
+        """NVML directly (microseconds per query, so the sampler keeps up with
+        a sub-second timed region); None when unavailable."""
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+
+            def q():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                return [str(sm), str(mx), hex(r)] + ["Active" if r & b else "Not Active" for b in bits.values()]
+            q()
+            return q
+        except Exception:
+            return None
+
     def _run(self):
+        q = self._nvml()
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
+                if q is not None:
+                    self.samples.append(q())
+                else:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([v.strip() for v in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.02)
+            self._stop.wait(0.005 if q is not None else 0.02)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
