@@ -260,9 +260,11 @@ int dsmoe_b200_ep_combine(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, co
  *                     load-aware or uniform thresholds, and the owner table
  *                     t_unit (device, E doubles) simulate_step applies
  *                     (ep_sim.hpp:59-89, :139-141); loads (device, optional);
- *   ep_dispatch       re-route under policy->t_unit (pass logits_mode
- *                     DSMOE_B200_LOGITS_REUSE to reuse the logits of
- *                     ep_route_counts), pack one row per (token, destination)
+ *   ep_dispatch       re-route under policy->t_unit (logits_mode
+ *                     DSMOE_B200_LOGITS_REUSE reuses the logits of
+ *                     ep_route_counts on the same context; `logits` (device,
+ *                     row stride logits_ld, optional) routes a token chunk
+ *                     from another context's logits), pack one row per (token, destination)
  *                     into send_rows and one 3 x int32 record {expert*4+level,
  *                     row, raw-score bits} per kept selection into records,
  *                     counts (device, nranks x {rows, records} int64), and
@@ -279,8 +281,13 @@ int dsmoe_b200_ep_last_counts(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer
 int dsmoe_b200_ep_thresholds(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const int64_t* counts, int devices,
                              const int32_t* device_of, double t_max, int load_aware, double* t_unit, double* loads);
 int dsmoe_b200_ep_dispatch(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
-                           const dsmoe_b200_policy* policy, int logits_mode, int nranks, const uint32_t* dest,
-                           void* send_rows, int32_t* records, int64_t* counts);
+                           const dsmoe_b200_policy* policy, int logits_mode, const float* logits, int logits_ld,
+                           int nranks, const uint32_t* dest, void* send_rows, int32_t* records, int64_t* counts);
+/* The gate logits of the last routing on ctx (device, T rows, row stride ld
+ * floats; valid until the next routing there): token chunks of one batch
+ * re-route from them on other contexts (ep_dispatch's logits / logits_ld:
+ * pass logits + c0 * ld for the chunk starting at token c0). */
+int dsmoe_b200_ctx_logits(dsmoe_b200_ctx* ctx, const float** logits, int* ld, int* T);
 int dsmoe_b200_ep_expert_packed(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* rows, long U,
                                 const int32_t* records, long S, const int64_t* src_row_base,
                                 const int64_t* src_rec_base, int nranks, void* out);

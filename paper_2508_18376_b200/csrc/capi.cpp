@@ -577,6 +577,7 @@ struct dsmoe_b200_ctx {
   // logits left in `logits` by the last routing on this context (LOGITS_REUSE)
   const void* logits_layer = nullptr;
   int logits_T = -1, logits_ld = 0;
+  int routed_T = -1;  // token count of the last routing (any logits source)
   long long scale_fill_key = -1;
   unsigned long long last_err_flags = 0;
   // optional per-stage CUDA-event timing (bench.py): 0 gate, 1 router,
@@ -804,11 +805,12 @@ void check_flags(dsmoe_b200_ctx* C) {
 // -------------------------------------------------- stage: gate logits + K1
 void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
                  const PolicyResolved& pol, int logits_mode, const float* logits_in, float* logits_out,
-                 const dsmoe_b200_routing* out, uint8_t* frac_ws) {
+                 const dsmoe_b200_routing* out, uint8_t* frac_ws, int logits_in_ld = 0) {
   cudaStream_t s = C->stream;
   bool counters_zeroed = false;  // the tensor-core gate kernel zeroes them in its prologue
   const float* lg = logits_in;
-  int ld = L->E;
+  int ld = logits_in_ld > 0 ? logits_in_ld : L->E;
+  C->routed_T = T;
   int nsplit = 1;               // split-K gate: partial logit planes the router sums
   long long split_stride = 0;
   C->mark(0);
@@ -1682,7 +1684,8 @@ int dsmoe_b200_ep_route_counts(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, con
 int dsmoe_b200_ep_last_counts(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, int64_t* counts) {
   return guarded([&] {
     require(C != nullptr && L != nullptr && counts != nullptr, DSMOE_E_INVALID_ARGUMENT, "null argument");
-    require(C->logits_T == T && T >= 1, DSMOE_E_INVALID_STATE, "ep_last_counts: no routing of this batch on the context");
+    require(C->routed_T == T && T >= 1, DSMOE_E_INVALID_STATE,
+            "ep_last_counts: no routing of this batch on the context");
     launch_check(launch_ep_counts(C->cnt_chunk.as<int>(), (T + kRouterChunk - 1) / kRouterChunk, L->E,
                                   reinterpret_cast<long long*>(counts), C->stream),
                  "ep counts");
@@ -1704,9 +1707,19 @@ int dsmoe_b200_ep_thresholds(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const
   });
 }
 
+int dsmoe_b200_ctx_logits(dsmoe_b200_ctx* C, const float** logits, int* ld, int* T) {
+  return guarded([&] {
+    require(C && logits && ld && T, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require(C->logits_T >= 0 && C->logits.p, DSMOE_E_INVALID_STATE, "ctx_logits: no gate logits on this context");
+    *logits = C->logits.as<float>();
+    *ld = C->logits_ld;
+    *T = C->logits_T;
+  });
+}
+
 int dsmoe_b200_ep_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
-                           const dsmoe_b200_policy* policy, int logits_mode, int nranks, const uint32_t* dest,
-                           void* send_rows, int32_t* records, int64_t* counts) {
+                           const dsmoe_b200_policy* policy, int logits_mode, const float* logits, int logits_ld,
+                           int nranks, const uint32_t* dest, void* send_rows, int32_t* records, int64_t* counts) {
   return guarded([&] {
     require(C != nullptr, DSMOE_E_INVALID_ARGUMENT, "null ctx");
     require_layer(L);
@@ -1716,7 +1729,7 @@ int dsmoe_b200_ep_dispatch(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
     const PolicyResolved pol = resolve_policy(L, policy);
     C->ensure(L, T);
     cudaStream_t s = C->stream;
-    stage_route(C, L, x, T, pol, logits_mode, nullptr, nullptr, nullptr, nullptr);
+    stage_route(C, L, x, T, pol, logits_mode, logits, nullptr, nullptr, nullptr, logits_ld);
     const int nchunks = (T + 255) / 256;
     C->ep_pos_td.ensure(static_cast<size_t>(T) * nranks * 4);
     C->ep_send_token.ensure(static_cast<size_t>(T) * std::min(nranks, L->K) * 4 + 16);

@@ -135,7 +135,10 @@ SYMBOLS = {
     "dsmoe_b200_ep_thresholds": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_double,
                                            C.c_int, C.c_void_p, C.c_void_p]),
     "dsmoe_b200_ep_dispatch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_int,
-                                         C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                         C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p]),
+    "dsmoe_b200_ctx_logits": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int)]),
     "dsmoe_b200_ep_expert_packed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_long, C.c_void_p, C.c_long,
                                               C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "dsmoe_b200_layer_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
@@ -721,17 +724,25 @@ def ep_thresholds(ctx: Context, layer: MoeLayer, counts, devices: int, device_of
     return t_unit, loads
 
 
+def ctx_logits(ctx: Context):
+    """(device pointer, row stride, T) of the gate logits of the last routing on ctx."""
+    p, ld, T = C.c_void_p(), C.c_int(), C.c_int()
+    _chk(lib().dsmoe_b200_ctx_logits(ctx.h, C.byref(p), C.byref(ld), C.byref(T)))
+    return p.value, ld.value, T.value
+
+
 def ep_dispatch(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None, t_unit, nranks: int, dest, send_rows,
-                records, counts, logits_mode=LOGITS_REUSE):
+                records, counts, logits_mode=LOGITS_REUSE, logits=None):
     """Re-route under the owner thresholds, pack one row per (token,
     destination) + one 3 x int32 record per (kept selection, destination),
     counts (nranks x 2 int64: rows, records), local shared experts; no host
     sync.  dest: E x 2 int32 (bit masks) CUDA tensor — the ranks a full /
     a major-only selection of each expert goes to."""
     x = _x(x, layer)
+    lp, ld = (None, 0) if logits is None else (C.c_void_p(logits[0]), int(logits[1]))
     _chk(lib().dsmoe_b200_ep_dispatch(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
-                                      C.byref((policy or DropPolicy()).c(t_unit)), logits_mode, nranks, _p(dest),
-                                      _p(send_rows), _p(records), _p(counts)))
+                                      C.byref((policy or DropPolicy()).c(t_unit)), logits_mode, lp, ld, nranks,
+                                      _p(dest), _p(send_rows), _p(records), _p(counts)))
 
 
 def ep_expert_packed(ctx: Context, layer: MoeLayer, rows, U: int, records, S: int, src_row_base, src_rec_base,

@@ -187,7 +187,8 @@ class ExpertParallelMoE:
     the gate and the shared experts are whole, routed experts [lo, hi) of the
     contiguous placement) and evaluates only them."""
 
-    def __init__(self, layer: D.MoeLayer, group=None, strategy: str = "contiguous", shard: bool = True):
+    def __init__(self, layer: D.MoeLayer, group=None, strategy: str = "contiguous", shard: bool = True,
+                 chunks: int | None = None):
         import torch
         import torch.distributed as dist
         self.dist = dist
@@ -219,6 +220,10 @@ class ExpertParallelMoE:
         self.d_device_of = torch.from_numpy(self.device_of.astype(np.int32)).to(dev)
         self.d_dest = torch.from_numpy(dest.astype(np.uint32).view(np.int32)).to(dev)
         self._bufs = {}
+        self._chunks = []
+        # token chunks per step: the dispatch all-to-all of chunk c+1 overlaps
+        # the expert GEMMs of chunk c (one chunk when there is nothing to overlap)
+        self.chunks = chunks if chunks is not None else (2 if W > 1 else 1)
 
     def _buf(self, name, shape, dtype, dev):
         import torch
@@ -228,69 +233,123 @@ class ExpertParallelMoE:
             self._bufs[name] = b
         return b
 
+    def _chunk_state(self, c):
+        import torch
+        while len(self._chunks) <= c:
+            st = torch.cuda.Stream()
+            self._chunks.append({"stream": st, "ctx": D.Context(stream=st), "ctx_exp": D.Context(stream=st),
+                                 "host": torch.empty(4 * self.world, dtype=torch.int64).pin_memory(),
+                                 "ev": torch.cuda.Event()})
+        return self._chunks[c]
+
     def forward(self, x, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,
-                timing=False, stats=True):
-        """One EP step, ONE host synchronisation (the split sizes):
-        1. no-drop routing -> per-expert counts -> all-reduce (device);
+                timing=False, stats=True, chunks=None):
+        """One EP step with one host synchronisation point (the split sizes):
+        1. no-drop routing of the whole batch -> per-expert counts ->
+           all-reduce (device);
         2. device_loads -> thresholds -> owner table on the device
            (simulate_step, ep_sim.hpp:110-149);
-        3. re-route under the owner thresholds (same logits), pack one row per
-           (token, destination rank) + one record per kept selection, local
-           shared experts (dsmoe_b200_ep_dispatch);
-        4. all-to-all of the per-destination counts, copied to the host (the
-           sync), then rows and records;
-        5. this rank's experts, one output row per received row;
-        6. rows back, summed per token over ranks + shared experts.
-        stats=True adds the post-drop load report (one all-reduce + sync)."""
+        then per token chunk, each on its own stream and contexts:
+        3. re-route the chunk under the owner thresholds from the step-1
+           logits, pack one row per (token, destination rank) + one record per
+           (kept selection, destination), local shared experts
+           (dsmoe_b200_ep_dispatch);
+        4. all-to-all of the per-destination counts, copied to pinned host
+           memory; the host waits for all chunks' counts once;
+        5. all-to-all of rows and records; this rank's experts (one output
+           row per received row); rows back; summed per token over ranks +
+           shared experts.
+        The collectives are issued chunk-interleaved (rows of every chunk,
+        then experts, then the returns), so on the one NCCL stream chunk c+1's
+        dispatch all-to-all overlaps chunk c's expert GEMMs and chunk c's
+        return overlaps chunk c+1's.  stats=True adds the post-drop load report
+        (one all-reduce + sync)."""
         import torch
         L, W, ctx = self.layer, self.world, self.ctx
         policy = policy or D.DropPolicy()
         T = x.shape[0]
         dev = x.device
         drop = policy.kind != "none"
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if timing else None
+        nch = max(1, min(self.chunks if chunks is None else int(chunks), T))
+        main = torch.cuda.current_stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timing else None
         if timing:
-            ev[0].record()
+            ev[0].record(main)
         counts = D.ep_route_counts(ctx, L, x, policy, self._buf("counts", (L.E, 2), torch.int64, dev), logits_mode)
         counts = self.coll.all_reduce(counts)
         t_unit, loads = D.ep_thresholds(ctx, L, counts, W, self.d_device_of, policy.t_drop if drop else 1.0,
                                         load_aware and drop, self._buf("t_unit", (L.E,), torch.float64, dev),
                                         self._buf("loads", (W,), torch.float64, dev))
-        cap_rows = T * min(W, L.K * L.P) + 1  # one row per (token, destination rank)
-        send = self._buf("send", (cap_rows, L.d), x.dtype, dev)
-        rec = self._buf("rec", (T * L.K * min(W, L.P) + 1, 3), torch.int32, dev)
-        cnt = self._buf("cnt", (W, 2), torch.int64, dev)
-        D.ep_dispatch(ctx, L, x, policy, t_unit if drop else None, W, self.d_dest, send, rec, cnt)
-        cnt_recv = self._buf("cnt_recv", (W, 2), torch.int64, dev)
-        self.coll.all_to_all(cnt_recv, cnt, [1] * W, [1] * W)
-        both = torch.cat([cnt.view(-1), cnt_recv.view(-1)]).cpu().numpy()  # the one host sync
-        nu, ns = both[0:2 * W:2], both[1:2 * W:2]
-        ru, rs = both[2 * W::2], both[2 * W + 1::2]
-        U, S, NU, NS = int(ru.sum()), int(rs.sum()), int(nu.sum()), int(ns.sum())
-        xr = self._buf("xr", (max(U, 1) + 1, L.d), x.dtype, dev)
-        rr = self._buf("rr", (max(S, 1) + 1, 3), torch.int32, dev)
+        lg, ld, _ = D.ctx_logits(ctx)
+        ready = torch.cuda.Event()
+        ready.record(main)
+        out = torch.empty((T, L.d), dtype=x.dtype, device=dev)
+        bounds = np.linspace(0, T, nch + 1).astype(np.int64)
+        ch = []
+        for c in range(nch):  # 3-4: dispatch + count exchange, all chunks
+            c0, c1 = int(bounds[c]), int(bounds[c + 1])
+            st = self._chunk_state(c)
+            Tc = c1 - c0
+            with torch.cuda.stream(st["stream"]):
+                st["stream"].wait_event(ready)
+                send = self._buf(f"send{c}", (Tc * min(W, L.K * L.P) + 1, L.d), x.dtype, dev)
+                rec = self._buf(f"rec{c}", (Tc * L.K * min(W, L.P) + 1, 3), torch.int32, dev)
+                cnt = self._buf(f"cnt{c}", (2, W, 2), torch.int64, dev)
+                D.ep_dispatch(st["ctx"], L, x[c0:c1], policy, t_unit if drop else None, W, self.d_dest, send, rec,
+                              cnt[0], logits=(lg + c0 * ld * 4, ld))
+                self.coll.all_to_all(cnt[1], cnt[0], [1] * W, [1] * W)
+                st["host"].copy_(cnt.view(-1), non_blocking=True)
+                st["ev"].record(st["stream"])
+            ch.append({"c0": c0, "c1": c1, "T": Tc, "st": st, "send": send, "rec": rec})
+        for k in ch:  # the host synchronisation point: split sizes of every chunk
+            k["st"]["ev"].synchronize()
+            h = k["st"]["host"].numpy()
+            k["nu"], k["ns"] = h[0:2 * W:2].copy(), h[1:2 * W:2].copy()
+            k["ru"], k["rs"] = h[2 * W:4 * W:2].copy(), h[2 * W + 1:4 * W:2].copy()
+            k["U"], k["S"], k["NU"], k["NS"] = (int(k["ru"].sum()), int(k["rs"].sum()), int(k["nu"].sum()),
+                                                int(k["ns"].sum()))
+        tev = []
+        for c, k in enumerate(ch):  # 5: rows and records, every chunk
+            with torch.cuda.stream(k["st"]["stream"]):
+                k["xr"] = self._buf(f"xr{c}", (max(k["U"], 1) + 1, L.d), x.dtype, dev)
+                k["rr"] = self._buf(f"rr{c}", (max(k["S"], 1) + 1, 3), torch.int32, dev)
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timing else None
+                if timing:
+                    e[0].record()
+                self.coll.all_to_all(k["xr"][:k["U"]], k["send"][:k["NU"]], k["ru"].tolist(), k["nu"].tolist())
+                self.coll.all_to_all(k["rr"][:k["S"]], k["rec"][:k["NS"]], k["rs"].tolist(), k["ns"].tolist())
+                if timing:
+                    e[1].record()
+                tev.append(e)
+        for c, k in enumerate(ch):  # this rank's experts
+            with torch.cuda.stream(k["st"]["stream"]):
+                k["yl"] = D.ep_expert_packed(k["st"]["ctx_exp"], L, k["xr"], k["U"], k["rr"], k["S"],
+                                             np.concatenate([[0], np.cumsum(k["ru"])]),
+                                             np.concatenate([[0], np.cumsum(k["rs"])]),
+                                             out=self._buf(f"yl{c}", (max(k["U"], 1) + 1, L.d), x.dtype, dev))
+                if timing:
+                    tev[c][2].record()
+        for c, k in enumerate(ch):  # rows back, combine into this chunk's output rows
+            with torch.cuda.stream(k["st"]["stream"]):
+                ret = self._buf(f"ret{c}", (k["NU"] + 1, L.d), x.dtype, dev)
+                self.coll.all_to_all(ret[:k["NU"]], k["yl"][:k["U"]], k["nu"].tolist(), k["ru"].tolist())
+                if timing:
+                    tev[c][3].record()
+                D.ep_combine(k["st"]["ctx"], L, ret, k["T"], out=out[k["c0"]:k["c1"]])
+                if stats or timing:  # this chunk's kept (full, major-only) selections per expert
+                    D.ep_last_counts(k["st"]["ctx"], L, k["T"], self._buf(f"post{c}", (L.E, 2), torch.int64, dev))
+        for k in ch:
+            main.wait_stream(k["st"]["stream"])
         if timing:
-            ev[1].record()
-        self.coll.all_to_all(xr[:U], send[:NU], ru.tolist(), nu.tolist())
-        self.coll.all_to_all(rr[:S], rec[:NS], rs.tolist(), ns.tolist())
-        if timing:
-            ev[2].record()
-        yl = D.ep_expert_packed(self.ctx_exp, L, xr, U, rr, S, np.concatenate([[0], np.cumsum(ru)]),
-                                np.concatenate([[0], np.cumsum(rs)]), out=self._buf("yl", (max(U, 1) + 1, L.d),
-                                                                                   x.dtype, dev))
-        if timing:
-            ev[3].record()
-        ret = self._buf("ret", (NU + 1, L.d), x.dtype, dev)
-        self.coll.all_to_all(ret[:NU], yl[:U], nu.tolist(), ru.tolist())
-        if timing:
-            ev[4].record()
-        out = D.ep_combine(ctx, L, ret, T)
-        if timing:
-            ev[5].record()
-        rep = {"rows_sent": nu, "rows_received": U, "records_sent": ns, "records_received": S}
+            ev[1].record(main)
+        sm = lambda key: np.sum([k[key] for k in ch], axis=0)
+        rep = {"rows_sent": sm("nu"), "rows_received": int(sm("U")), "records_sent": sm("ns"),
+               "records_received": int(sm("S")), "chunks": nch}
         if stats or timing:
-            post = self.coll.all_reduce(D.ep_last_counts(ctx, L, T, self._buf("post", (L.E, 2), torch.int64, dev)))
-            post = post.cpu().numpy()
+            post = self._bufs["post0"].clone()
+            for c in range(1, nch):
+                post += self._bufs[f"post{c}"]
+            post = self.coll.all_reduce(post).cpu().numpy()
             pre = loads.cpu().numpy()
             rep["pre_loads"] = pre
             rep["thresholds"] = device_thresholds(pre, policy.t_drop, load_aware) if drop else np.zeros(W)
@@ -298,16 +357,19 @@ class ExpertParallelMoE:
             rep["speedup"] = modeled_speedup(pre, rep["post_loads"])
         if timing:
             torch.cuda.synchronize()
-            rep["exchange_ms"] = ev[1].elapsed_time(ev[2]) + ev[3].elapsed_time(ev[4])
-            rep["expert_ms"] = ev[2].elapsed_time(ev[3])
-            rep["step_ms"] = ev[0].elapsed_time(ev[5])
+            rep["exchange_ms"] = float(sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in tev))
+            rep["expert_ms"] = float(sum(e[1].elapsed_time(e[2]) for e in tev))
+            rep["step_ms"] = ev[0].elapsed_time(ev[1])
             # this rank's expert FLOPs: 6 d x (the widths of the blocks it holds that each record needs)
-            codes = rr[:S, 0].cpu().numpy()
             bw = np.asarray(self.full.widths()[0], np.float64).reshape(-1, L.P) * self.held.reshape(-1, L.P)
-            unit, full = codes >> 2, (codes & 3) == 2
-            rep["expert_flops"] = float(6.0 * L.d * np.where(full, bw.sum(axis=1)[unit], bw[unit, 0]).sum())
-            es = x.element_size()
-            rep["exchange_bytes"] = int((NU + U) * L.d * es + (NS + S) * 12)  # this rank: sent + received
+            fl, nbytes = 0.0, 0
+            for k in ch:
+                codes = k["rr"][:k["S"], 0].cpu().numpy()
+                unit, full = codes >> 2, (codes & 3) == 2
+                fl += float(6.0 * L.d * np.where(full, bw.sum(axis=1)[unit], bw[unit, 0]).sum())
+                nbytes += int((k["NU"] + k["U"]) * L.d * x.element_size() + (k["NS"] + k["S"]) * 12)
+            rep["expert_flops"] = fl
+            rep["exchange_bytes"] = nbytes  # this rank: sent + received, both directions
         return out, rep
 
     def forward_rows(self, x, policy: D.DropPolicy | None = None, load_aware=True, logits_mode=D.LOGITS_TENSOR,

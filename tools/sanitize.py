@@ -81,16 +81,16 @@ x = torch.from_numpy(O.generate_tokens(T, 256, 11)).cuda().bfloat16()
 held = np.zeros(16, np.uint8)
 held[::2] = 1  # S-ETP-like: only the major halves
 sh = D.layer_shard_blocks(ctx, dl, held)
-cnt = D.ep_route_counts(ctx, sh, x, D.DropPolicy())
+cnt = D.ep_route_counts(ctx, dl, x, D.DropPolicy())
 dv = torch.zeros(16, dtype=torch.int32, device="cuda")
-t_unit, loads = D.ep_thresholds(ctx, sh, cnt, 1, dv, 0.3, True)
+t_unit, loads = D.ep_thresholds(ctx, dl, cnt, 1, dv, 0.3, True)
 send = torch.empty((T * 2 + 1, 256), dtype=x.dtype, device="cuda")
 rec = torch.empty((T * 4 + 1, 3), dtype=torch.int32, device="cuda")
 cn = torch.empty((1, 2), dtype=torch.int64, device="cuda")
 dest = torch.full((8, 2), 1, dtype=torch.int32, device="cuda")
 D.ep_dispatch(ctx, dl, x, D.DropPolicy.two_t_from(0.3), t_unit, 1, dest, send, rec, cn)
 c = cn.cpu().numpy()[0]
-yl = D.ep_expert_packed(ctx2, dl, send, int(c[0]), rec, int(c[1]), [0, int(c[0])], [0, int(c[1])])
+yl = D.ep_expert_packed(ctx2, sh, send, int(c[0]), rec, int(c[1]), [0, int(c[0])], [0, int(c[1])])
 out = DS.ep_combine(ctx, dl, yl, T)
 D.ep_last_counts(ctx, dl, T)
 torch.cuda.synchronize()
