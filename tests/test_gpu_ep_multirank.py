@@ -35,7 +35,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, load_aware, method, q, strategy="contiguous", E=12):
+def _worker(rank, world, port, load_aware, method, q, strategy="contiguous", E=12, chunks=None):
     import torch.distributed as dist
     import paper_2508_18376_b200 as D
     from paper_2508_18376_b200 import ep
@@ -46,7 +46,7 @@ def _worker(rank, world, port, load_aware, method, q, strategy="contiguous", E=1
     layer = D.MoeLayer(rec.d, rec.ffn, rec.E, rec.K, rec.gate, rec.blocks, rec.shared, replay_factor=rec.P,
                        dtype="f32")
     shard = np.array_split(np.arange(x.shape[0]), world)[rank]
-    m = ep.ExpertParallelMoE(layer, strategy=strategy)
+    m = ep.ExpertParallelMoE(layer, strategy=strategy, chunks=chunks)
     y, rep = getattr(m, method)(torch.from_numpy(x[shard]).cuda(), D.DropPolicy.two_t_from(0.3),
                                 load_aware=load_aware, logits_mode=D.LOGITS_EXACT)
     q.put((rank, y.cpu().numpy(), rep["pre_loads"], rep["thresholds"], rep["post_loads"], rep["speedup"]))
@@ -76,6 +76,34 @@ def test_ep_multiprocess_matches_simulate_step(world, load_aware, method):
         assert np.array_equal(th, ref["thresholds"])
         assert np.array_equal(post, ref["post_loads"])
         assert sp == ref["speedup"]
+    ro = O.route_from_logits(O.gate_logits(x, rec.gate), rec.K, rec.P)
+    yo = O.moe_forward(rec, x, ref["idx"], ro.raw, ref["frac"])
+    y = np.concatenate([r[1] for r in res])
+    assert np.abs(y - yo).max() / np.abs(yo).max() < 1e-5
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_ep_token_chunks(chunks):
+    """The overlapped step (token chunks on their own streams) gives the same
+    reports and outputs for any chunk count."""
+    import torch.multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, True, "forward", q, "contiguous", 12, chunks))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    rec, x = skewed()
+    ref = O.simulate_step(O.gate_logits(x, rec.gate), rec, world, "2t", 0.3, load_aware=True)
+    for _, _, pre, th, post, sp in res:
+        assert np.array_equal(pre, ref["pre_loads"]) and np.array_equal(post, ref["post_loads"])
+        assert np.array_equal(th, ref["thresholds"]) and sp == ref["speedup"]
     ro = O.route_from_logits(O.gate_logits(x, rec.gate), rec.K, rec.P)
     yo = O.moe_forward(rec, x, ref["idx"], ro.raw, ref["frac"])
     y = np.concatenate([r[1] for r in res])
