@@ -224,6 +224,8 @@ def calibrate(ctx, layer, x, target, tol=0.005, kind="2t", t_unit=None):
     import paper_2508_18376_b200 as D
     if target <= 0:
         return D.DropPolicy(), 0.0
+    if t_unit is None:  # the same bisection in one device kernel (dsmoe_b200_calibrate_rate): the same t
+        return D.calibrate_rate(ctx, layer, x, target, kind=kind, tol=tol)
     mk = D.DropPolicy.two_t_from if kind == "2t" else D.DropPolicy.one_t
     lo, hi = 0.0, 1.0
     best = None

@@ -317,6 +317,24 @@ int dsmoe_b200_forward_ex(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, co
                           const dsmoe_b200_policy* policy, int logits_mode, int flags, void* out,
                           dsmoe_b200_drop_stats_t* stats);
 
+/* Rate-targeted drop (north star item 2).  The reference reaches a drop
+ * rate by bisecting the threshold (acceptance.cpp:342-352); here the
+ * bisection runs on the device in one kernel over the batch's normalized
+ * scores: t = (lo + hi) / 2, the exact drop_stats rate of one_t(t) /
+ * two_t_from(t) (policy->kind 1T / 2T, keep_top1, normalize as in the
+ * policy; its thresholds are ignored), the closest t so far kept, stop at
+ * |rate - target| <= tol or after `iters` rounds — the same t, bit for bit,
+ * as that host loop.  calibrate_rate returns t and its rate on the host
+ * (synchronises); forward_rate routes the batch under that t and runs the
+ * forward without a host round trip (t_rate: device, optional, receives
+ * [t, rate]; stats: host, optional, synchronises). */
+int dsmoe_b200_calibrate_rate(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
+                              const dsmoe_b200_policy* policy, double target, double tol, int iters, int logits_mode,
+                              double* t_out, double* rate_out);
+int dsmoe_b200_forward_rate(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer, const void* x, int T,
+                            const dsmoe_b200_policy* policy, double target, double tol, int iters, int logits_mode,
+                            int flags, void* out, double* t_rate, dsmoe_b200_drop_stats_t* stats);
+
 /* analyze_gating (dropping.hpp:207-228) on the device: Top-K (no drop, always
  * normalized) of the layer's own gate; host outputs selection_counts[E],
  * raw_hist[bins], norm_hist[bins] with bin = clamp(int(v * bins), 0, bins-1). */

@@ -570,6 +570,7 @@ struct dsmoe_b200_ctx {
   DevBuf logits, sel_code, sel_raw, slot_pos, cnt_chunk, chunk_off, code_base, counters, row_token, row_scale, seg,
       scalars;
   DevBuf tiles1, tiles2, tiles_gate, xperm, H, Y, frac_ws, vseg, vseg_unit;
+  DevBuf rate_norm, rate_cnt, rate_tunit, rate_result;  // rate-targeted drop (dsmoe_b200_forward_rate)
   // EP with one row per (token, rank): last ep_pack's layout on this context
   DevBuf ep_pos_td, ep_send_token, ep_cnt, ep_tot, ep_owner, ep_base;
   int ep_N = 0, ep_T = -1;
@@ -1704,6 +1705,106 @@ int dsmoe_b200_ep_thresholds(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const
                                       load_aware, t_unit, loads, C->stream),
                  "ep thresholds");
     count_launch(1);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+// The rate-targeted threshold on the device: a no-drop routing writes the
+// normalized scores, the bisection kernel (router.cu) picks t exactly as the
+// host bisection over drop_stats would and fills the per-expert threshold
+// table.  Returns the device pointer of [t, rate].
+double* stage_rate(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T, const PolicyResolved& pol,
+                   double target, double tol, int iters, int logits_mode) {
+  require(pol.kind == DSMOE_B200_DROP_1T || pol.kind == DSMOE_B200_DROP_2T, DSMOE_E_INVALID_ARGUMENT,
+          "rate-targeted drop: the policy kind must be 1t or 2t");
+  require(target >= 0.0 && target <= 1.0 && tol >= 0.0 && iters >= 1 && iters <= 64, DSMOE_E_INVALID_ARGUMENT,
+          "rate-targeted drop: target in [0, 1], tol >= 0, 1 <= iters <= 64");
+  require(is_pow2(L->P), DSMOE_E_INVALID_STATE, "rate-targeted drop: replay factor must be a power of two");
+  cudaStream_t s = C->stream;
+  const size_t n = static_cast<size_t>(T) * L->K * L->P;
+  C->rate_norm.ensure(n * 8 + 16);
+  C->rate_cnt.ensure(static_cast<size_t>(64) * 2 * 8);
+  C->rate_tunit.ensure(static_cast<size_t>(L->E) * 8 + 16);
+  C->rate_result.ensure(2 * 8);
+  PolicyResolved none = pol;
+  none.kind = DSMOE_B200_DROP_NONE;
+  none.t_unit = nullptr;
+  dsmoe_b200_routing r{nullptr, nullptr, C->rate_norm.as<double>(), nullptr};
+  stage_route(C, L, x, T, none, logits_mode, nullptr, nullptr, &r, nullptr);
+  cuda_check(cudaMemsetAsync(C->rate_cnt.p, 0, static_cast<size_t>(iters) * 2 * 8, s), "memset");
+  launch_check(launch_rate_calibrate(C->rate_norm.as<double>(), T, L->K, L->P, L->S, pol.kind == DSMOE_B200_DROP_2T,
+                                     pol.keep_top1, target, tol, iters, C->rate_cnt.as<unsigned long long>(),
+                                     C->rate_tunit.as<double>(), L->E, C->rate_result.as<double>(), num_sms(), s),
+               "rate calibration");
+  count_launch(1);
+  return C->rate_result.as<double>();
+}
+
+// the policy the router's second pass applies: one_t(t) / two_t_from(t) with t
+// per expert from the device table (t_major = t + (-0.01) == t - 0.01 exactly)
+PolicyResolved rate_policy(const PolicyResolved& pol, const double* t_unit) {
+  PolicyResolved p = pol;
+  p.t_drop = 0.0;
+  p.t_unit = t_unit;
+  p.maj_off = pol.kind == DSMOE_B200_DROP_2T ? -0.01 : 0.0;
+  p.min_off = pol.kind == DSMOE_B200_DROP_2T ? 0.01 : 0.0;
+  p.t_major = p.maj_off;
+  p.t_minor = p.min_off;
+  return p;
+}
+}  // namespace
+
+extern "C" {
+
+int dsmoe_b200_calibrate_rate(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                              const dsmoe_b200_policy* policy, double target, double tol, int iters, int logits_mode,
+                              double* t_out, double* rate_out) {
+  return guarded([&] {
+    require(C != nullptr && policy != nullptr, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require_layer(L);
+    require(T >= 1 && x, DSMOE_E_INVALID_ARGUMENT, "calibrate_rate: empty batch");
+    g_launches = 0;
+    dsmoe_b200_policy pc = *policy;
+    if (pc.kind == DSMOE_B200_DROP_2T) pc.t_major = pc.t_minor = 0.0;  // the band comes from t
+    const PolicyResolved pol = resolve_policy(L, &pc);
+    C->ensure(L, T);
+    const double* res = stage_rate(C, L, x, T, pol, target, tol, iters, logits_mode);
+    double h[2];
+    cuda_check(cudaMemcpyAsync(h, res, sizeof(h), cudaMemcpyDeviceToHost, C->stream), "D2H");
+    unsigned long long cnt[5];
+    read_counters(C, cnt);
+    if (t_out) *t_out = h[0];
+    if (rate_out) *rate_out = h[1];
+  });
+}
+
+int dsmoe_b200_forward_rate(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, int T,
+                            const dsmoe_b200_policy* policy, double target, double tol, int iters, int logits_mode,
+                            int flags, void* out, double* t_rate, dsmoe_b200_drop_stats_t* stats) {
+  return guarded([&] {
+    require(C != nullptr && policy != nullptr, DSMOE_E_INVALID_ARGUMENT, "null argument");
+    require_whole(L);
+    require(T >= 1 && x && out, DSMOE_E_INVALID_ARGUMENT, "forward_rate: empty batch");
+    g_launches = 0;
+    dsmoe_b200_policy pc = *policy;
+    if (pc.kind == DSMOE_B200_DROP_2T) pc.t_major = pc.t_minor = 0.0;
+    const PolicyResolved pol = resolve_policy(L, &pc);
+    C->ensure(L, T);
+    C->prof_begin();
+    const double* res = stage_rate(C, L, x, T, pol, target, tol, iters, logits_mode);
+    stage_route(C, L, x, T, rate_policy(pol, C->rate_tunit.as<double>()), DSMOE_B200_LOGITS_REUSE, nullptr, nullptr,
+                nullptr, nullptr);
+    stage_ffn(C, L, x, T, out, (flags & DSMOE_B200_RESIDUAL) ? x : nullptr);
+    C->prof_end();
+    if (t_rate)
+      cuda_check(cudaMemcpyAsync(t_rate, res, 2 * sizeof(double), cudaMemcpyDeviceToDevice, C->stream), "copy t");
+    if (stats) {
+      unsigned long long h[5];
+      read_counters(C, h);
+      stats_from_counts(L, T, h[0], h[1], nullptr, stats);
+    }
   });
 }
 

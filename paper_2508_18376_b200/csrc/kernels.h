@@ -43,6 +43,9 @@ struct ImportArgs {
 };
 constexpr int kRouterChunk = 32;  // tokens per router block (one warp each) / scatter chunk
 int launch_router(const RouterArgs& a, cudaStream_t stream);
+int launch_rate_calibrate(const double* norm, int T, int K, int P, int S, int two_t, int keep_top1, double target,
+                          double tol, int iters, unsigned long long* cnt, double* t_unit, int E, double* result,
+                          int num_sms, cudaStream_t stream);
 int launch_import_routing(const ImportArgs& a, cudaStream_t stream);
 int launch_gate_logits_exact(const void* x, int x_bf16, const float* gate, float* out, int T, int d,
                              int E, cudaStream_t stream);

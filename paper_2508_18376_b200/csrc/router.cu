@@ -22,6 +22,8 @@
 //
 // This translation unit is compiled with -fmad=false: every float / double
 // operation rounds exactly where the reference's (-ffp-contract=off) does.
+#include <cooperative_groups.h>
+
 #include "kernels.h"
 
 namespace dsb {
@@ -645,6 +647,162 @@ int launch_gating_hist(const int32_t* idx, const float* raw, const double* norm,
   if (smem > 48 * 1024) return -1;
   gating_hist_kernel<<<num_sms, 256, smem, stream>>>(idx, raw, norm, T, K, P, E, bins, counts, rh, nh);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// ---------------------------------------------------------------------------
+// Rate-targeted drop on the device (north star item 2, "rate-based drop
+// mask"; the reference has thresholds only, and its tests reach a rate by
+// bisecting the threshold, acceptance.cpp:342-352).  Input: the normalized
+// scores ns of a no-drop routing (copy 0 of every selection, T x K) — the
+// band decision of drop_1t / drop_2t depends on nothing else
+// (dropping.hpp:93-122).  The kernel replays the host bisection exactly:
+//   t = 0.5 (lo + hi); rate = drop_stats(...).drop_rate under one_t(t) /
+//   two_t_from(t) (2T band t -/+ 0.01 in double); keep the closest; stop
+//   when |rate - target| <= tol; rate < target ? lo = t : hi = t.
+// The drop rate of a candidate t is exact: retained copies are integer
+// counts (P a power of two; stats_from_counts' arithmetic).  Every thread
+// holds one selection's ns in a register across iterations; per iteration
+// the grid counts kept copies and one grid barrier separates the rounds
+// (iteration-indexed counters, so nothing is reset).  Output: t and its rate,
+// and t_unit[e] = t for every expert — the threshold table the router applies
+// in its second pass without a host round trip.
+// ---------------------------------------------------------------------------
+struct RateArgs {
+  const double* norm;   // T x (K*P), copy-major: slot s of copy 0 at [t*K*P + s]
+  int T, K, P, S;
+  int two_t, keep_top1;
+  double target, tol;
+  int iters;
+  unsigned long long* cnt;  // iters x 2 (copies kept at fraction 1, at 0.5); zeroed by the host
+  double* t_unit;           // E
+  int E;
+  double* result;           // [t, rate]
+};
+
+__global__ void __launch_bounds__(1024) rate_calibrate_kernel(const RateArgs a) {
+  namespace cg = cooperative_groups;
+  __shared__ unsigned long long s1, sh;
+  __shared__ double s_lo, s_hi, s_best_t, s_best_r;
+  __shared__ int s_done;
+  const long long n = static_cast<long long>(a.T) * a.K;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long g0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  constexpr int kPer = 4;  // selections per thread held in registers (T*K <= 4 x grid threads)
+  double ns[kPer];
+  bool top[kPer], live[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const long long g = g0 + i * stride;
+    live[i] = g < n;
+    ns[i] = 0.0;
+    top[i] = false;
+    if (live[i]) {
+      const long long t = g / a.K;
+      const int s = static_cast<int>(g - t * a.K);
+      const double* row = a.norm + t * a.K * a.P;
+      ns[i] = row[s];
+      bool first_max = true;  // top_slot: the first strict maximum of ns (dropping.hpp:99)
+      for (int j = 0; j < a.K; ++j) {
+        if (j < s && !(ns[i] > row[j])) first_max = false;
+        if (j > s && row[j] > ns[i]) first_max = false;
+      }
+      top[i] = first_max;
+    }
+  }
+  const long long ncopies = n * a.P;
+  const double w = 1.0 / a.P;
+  const double total = __dmul_rn(static_cast<double>(ncopies), w);
+  const double denom = __dadd_rn(total, static_cast<double>(a.S) * a.T);
+  if (threadIdx.x == 0) {
+    s_lo = 0.0;
+    s_hi = 1.0;
+    s_best_t = 0.0;
+    s_best_r = -1.0;
+    s_done = 0;
+  }
+  __syncthreads();
+  for (int it = 0; it < a.iters; ++it) {
+    const double t = __dmul_rn(0.5, __dadd_rn(s_lo, s_hi));
+    const double tmaj = a.two_t ? __dsub_rn(t, 0.01) : t;
+    const double tmin = a.two_t ? __dadd_rn(t, 0.01) : t;
+    unsigned long long c1 = 0, ch = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      if (!live[i]) continue;
+      int lv = ns[i] >= tmin ? 2 : (ns[i] >= tmaj ? 1 : 0);
+      if (a.keep_top1 && top[i]) lv = 2;
+      if (a.P == 1) {
+        c1 += lv == 2;
+        ch += lv == 1;
+      } else {  // full: every copy at fraction 1; major-only: copy 0 at fraction 1
+        c1 += lv == 2 ? a.P : (lv == 1 ? 1 : 0);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      ch += __shfl_xor_sync(0xffffffffu, ch, o);
+    }
+    if (threadIdx.x == 0) {
+      s1 = 0;
+      sh = 0;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && (c1 | ch)) {
+      atomicAdd(&s1, c1);
+      atomicAdd(&sh, ch);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicAdd(&a.cnt[2 * it], s1);
+      atomicAdd(&a.cnt[2 * it + 1], sh);
+    }
+    cg::this_grid().sync();
+    if (threadIdx.x == 0) {  // every block derives the same next step from the same totals
+      const unsigned long long n1 = atomicAdd(&a.cnt[2 * it], 0ull), nh = atomicAdd(&a.cnt[2 * it + 1], 0ull);
+      const double retained = __dmul_rn(static_cast<double>(2 * n1 + nh), __dmul_rn(0.5, w));
+      const double dropped = __dsub_rn(total, retained);
+      const double rate = denom > 0.0 ? __ddiv_rn(dropped, denom) : 0.0;
+      const double err = fabs(__dsub_rn(rate, a.target));
+      if (s_best_r < 0.0 || err < fabs(__dsub_rn(s_best_r, a.target))) {
+        s_best_t = t;
+        s_best_r = rate;
+      }
+      if (err <= a.tol) {
+        s_done = 1;
+      } else if (rate < a.target) {
+        s_lo = t;
+      } else {
+        s_hi = t;
+      }
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
+  if (blockIdx.x == 0) {
+    for (int e = threadIdx.x; e < a.E; e += blockDim.x) a.t_unit[e] = s_best_t;
+    if (threadIdx.x == 0) {
+      a.result[0] = s_best_t;
+      a.result[1] = s_best_r;
+    }
+  }
+}
+
+int launch_rate_calibrate(const double* norm, int T, int K, int P, int S, int two_t, int keep_top1, double target,
+                          double tol, int iters, unsigned long long* cnt, double* t_unit, int E, double* result,
+                          int num_sms, cudaStream_t stream) {
+  if (P < 1 || (P & (P - 1)) != 0 || iters < 1) return -1;
+  RateArgs a{norm, T, K, P, S, two_t, keep_top1, target, tol, iters, cnt, t_unit, E, result};
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rate_calibrate_kernel, 1024, 0);
+  if (per_sm < 1) return -3;
+  const long long n = static_cast<long long>(T) * K;
+  const long long need = (n + 4 * 1024 - 1) / (4 * 1024);
+  if (need > static_cast<long long>(num_sms) * per_sm) return -1;  // > 4 selections per thread
+  const int grid = static_cast<int>(need < 1 ? 1 : need);
+  void* args[] = {&a};
+  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(rate_calibrate_kernel), dim3(grid),
+                                                    dim3(1024), args, 0, stream);
+  return e == cudaSuccess ? 0 : -2;
 }
 
 }  // namespace dsb

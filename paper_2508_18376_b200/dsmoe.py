@@ -143,6 +143,12 @@ SYMBOLS = {
                                               C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "dsmoe_b200_layer_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "dsmoe_b200_layer_shard_blocks": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "dsmoe_b200_calibrate_rate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy),
+                                            C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                            C.POINTER(C.c_double)]),
+    "dsmoe_b200_forward_rate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(Policy), C.c_double,
+                                          C.c_double, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                          C.POINTER(DropStatsC)]),
     "dsmoe_b200_transform": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "dsmoe_b200_layer_widths": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "dsmoe_b200_layer_get_gate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
@@ -387,6 +393,10 @@ class RoutingDecision:
                 self.normalized.cpu().numpy(), self.fraction.cpu().numpy())
 
 
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
 def _x(x, layer: MoeLayer):
     torch = _torch()
     if not (isinstance(x, torch.Tensor) and x.is_cuda):
@@ -474,6 +484,41 @@ def forward(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None = None, 
     _chk(lib().dsmoe_b200_forward_ex(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0],
                                      C.byref((policy or DropPolicy()).c()), logits_mode, 1 if residual else 0,
                                      C.c_void_p(out.data_ptr()), C.byref(st) if with_stats else None))
+    return (out, st.as_dict()) if with_stats else out
+
+
+def calibrate_rate(ctx: Context, layer: MoeLayer, x, target: float, kind: str = "2t", keep_top1=True, tol=0.005,
+                   iters=40, normalize=None, logits_mode=LOGITS_TENSOR):
+    """The threshold that reaches `target` drop rate on batch x, bisected on
+    the device in one kernel (the acceptance.cpp:342-352 method; the same t as
+    the host loop over route_and_drop stats).  Returns (DropPolicy, rate)."""
+    x = _x(x, layer)
+    if target <= 0:
+        return DropPolicy(), 0.0
+    base = DropPolicy("2t" if kind == "2t" else "1t", 0.0, keep_top1=keep_top1, normalize=normalize)
+    t, r = C.c_double(), C.c_double()
+    _chk(lib().dsmoe_b200_calibrate_rate(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0], C.byref(base.c()),
+                                         float(target), float(tol), int(iters), logits_mode, C.byref(t), C.byref(r)))
+    pol = DropPolicy.two_t_from(t.value, keep_top1) if kind == "2t" else DropPolicy.one_t(t.value, keep_top1)
+    pol.normalize = normalize
+    return pol, r.value
+
+
+def forward_rate(ctx: Context, layer: MoeLayer, x, target: float, kind: str = "2t", keep_top1=True, tol=0.005,
+                 iters=40, out=None, normalize=None, logits_mode=LOGITS_TENSOR, with_stats=False, t_rate=None,
+                 residual=False):
+    """The forward under a per-batch rate-targeted drop mask: the threshold is
+    bisected on the device and applied without a host round trip.
+    t_rate (optional float64 CUDA tensor of 2) receives [t, rate]."""
+    torch = _torch()
+    x = _x(x, layer)
+    if out is None:
+        out = torch.empty_like(x)
+    base = DropPolicy("2t" if kind == "2t" else "1t", 0.0, keep_top1=keep_top1, normalize=normalize)
+    st = DropStatsC()
+    _chk(lib().dsmoe_b200_forward_rate(ctx.h, layer.h, C.c_void_p(x.data_ptr()), x.shape[0], C.byref(base.c()),
+                                       float(target), float(tol), int(iters), logits_mode, 1 if residual else 0,
+                                       C.c_void_p(out.data_ptr()), _p(t_rate), C.byref(st) if with_stats else None))
     return (out, st.as_dict()) if with_stats else out
 
 
@@ -683,10 +728,6 @@ def ep_combine(ctx: Context, layer: MoeLayer, ret_rows, T: int, out=None):
 
 
 # ---------------------------------- EP with one host synchronisation per step
-def _p(t):
-    return None if t is None else C.c_void_p(t.data_ptr())
-
-
 def ep_route_counts(ctx: Context, layer: MoeLayer, x, policy: DropPolicy | None = None, counts=None,
                     logits_mode=LOGITS_TENSOR):
     """Route x without drop; per-expert (full, major-only) selection counts
