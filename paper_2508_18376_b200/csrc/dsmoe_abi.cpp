@@ -200,13 +200,19 @@ struct dsmoe_model {
   int width = 4;
   std::vector<Layer<float>> f;
   std::vector<Layer<double>> d;
-  // device copies of the fp32 layers, built on first use (the model is
-  // immutable, so the cache never goes stale)
+  // device copies of the fp32 layers, built on first use per CUDA device (the
+  // model is immutable, so the cache never goes stale); dev_id = the device
+  // the `dev` copies live on
   mutable std::mutex mu;
   mutable std::vector<dsmoe_b200_layer*> dev;
+  mutable int dev_id = -1;
+  mutable std::vector<std::pair<int, std::vector<dsmoe_b200_layer*>>> other;  // copies on other devices
   ~dsmoe_model() {
     for (auto* L : dev)
       if (L) dsmoe_b200_layer_free(L);
+    for (auto& o : other)
+      for (auto* L : o.second)
+        if (L) dsmoe_b200_layer_free(L);
   }
   int num_layers() const { return width == 4 ? static_cast<int>(f.size()) : static_cast<int>(d.size()); }
 };
@@ -692,10 +698,24 @@ dsmoe_b200_layer* upload_layer(const Layer<float>& L, cudaStream_t s) {
 
 // device copy of layer l of an fp32 model (cached on the handle)
 const dsmoe_b200_layer* device_layer(const dsmoe_model& m, int l, cudaStream_t s) {
+  int cur = 0;
+  cuda(cudaGetDevice(&cur), "cudaGetDevice");
   std::lock_guard<std::mutex> lock(m.mu);
-  if (m.dev.size() != m.f.size()) m.dev.assign(m.f.size(), nullptr);
-  if (!m.dev[static_cast<size_t>(l)]) m.dev[static_cast<size_t>(l)] = upload_layer(m.f[static_cast<size_t>(l)], s);
-  return m.dev[static_cast<size_t>(l)];
+  if (m.dev_id < 0) m.dev_id = cur;
+  std::vector<dsmoe_b200_layer*>* cache = &m.dev;
+  if (cur != m.dev_id) {  // the handle is used from another GPU: a separate set of copies there
+    cache = nullptr;
+    for (auto& o : m.other)
+      if (o.first == cur) cache = &o.second;
+    if (!cache) {
+      m.other.emplace_back(cur, std::vector<dsmoe_b200_layer*>{});
+      cache = &m.other.back().second;
+    }
+  }
+  if (cache->size() != m.f.size()) cache->assign(m.f.size(), nullptr);
+  auto& slot = (*cache)[static_cast<size_t>(l)];
+  if (!slot) slot = upload_layer(m.f[static_cast<size_t>(l)], s);
+  return slot;
 }
 
 // device fp32 layer -> host Layer<float> (weights in the reference layout)
@@ -1036,6 +1056,7 @@ int dsmoe_transform(const dsmoe_model* m, const char* mode, int p, dsmoe_model**
     const auto& layers = fp32_layers(model_ref(m));
     Device g;
     auto res = std::make_unique<dsmoe_model>();
+    cuda(cudaGetDevice(&res->dev_id), "cudaGetDevice");  // seeded with this device's copies
     res->width = 4;
     for (size_t l = 0; l < layers.size(); ++l) {
       const dsmoe_b200_layer* D = device_layer(*m, static_cast<int>(l), g.s);
@@ -1059,6 +1080,7 @@ int dsmoe_reverse_partial(const dsmoe_model* m, dsmoe_model** out) {
     const auto& layers = fp32_layers(model_ref(m));
     Device g;
     auto res = std::make_unique<dsmoe_model>();
+    cuda(cudaGetDevice(&res->dev_id), "cudaGetDevice");  // seeded with this device's copies
     for (size_t l = 0; l < layers.size(); ++l) {
       const Layer<float>& S = layers[l];
       require(S.replay > 1, DSMOE_E_INVALID_STATE, "reverse: model does not carry a partial transformation");
@@ -1087,6 +1109,7 @@ int dsmoe_reconstruct(const dsmoe_model* m, const char* tokens_path, const char*
     Buf nxt(cur.n);
     const int T = calib.rows;
     auto res = std::make_unique<dsmoe_model>();
+    cuda(cudaGetDevice(&res->dev_id), "cudaGetDevice");  // seeded with this device's copies
     Value profiles = Value::array();
     for (size_t l = 0; l < layers.size(); ++l) {
       const Layer<float>& S = layers[l];
