@@ -183,9 +183,9 @@ class _Coll:
 
 class ExpertParallelMoE:
     """One rank of an expert-parallel MoE layer.  With shard=True (default)
-    the rank keeps only its own experts' weights (dsmoe_b200_layer_shard:
-    the gate and the shared experts are whole, routed experts [lo, hi) of the
-    contiguous placement) and evaluates only them."""
+    the rank keeps only the weights of the physical blocks the placement puts
+    on it (dsmoe_b200_layer_shard_blocks: the gate and the shared experts are
+    whole) and evaluates only them."""
 
     def __init__(self, layer: D.MoeLayer, group=None, strategy: str = "contiguous", shard: bool = True,
                  chunks: int | None = None):
