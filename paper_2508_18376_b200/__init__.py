@@ -11,5 +11,5 @@ from .dsmoe import (  # noqa: F401
     LOGITS_EXACT,
     profile_importance, reconstruct_experts, model_forward_dropped, dispatch, expert_ffn, combine,
     LOGITS_REUSE, transform, complete_transform, partial_transform, layer_weights,
-    calibrate_rate, forward_rate, ep_route_counts, ep_last_counts, ep_thresholds, ep_dispatch, ep_expert_packed, layer_shard, layer_shard_blocks,
+    calibrate_rate, forward_rate, simulate_step, ep_route_counts, ep_last_counts, ep_thresholds, ep_dispatch, ep_expert_packed, layer_shard, layer_shard_blocks,
 )

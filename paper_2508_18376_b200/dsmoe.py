@@ -569,6 +569,40 @@ def load_aware_thresholds(loads, t_max) -> np.ndarray:
     return out
 
 
+def simulate_step(ctx: Context, layer: MoeLayer, x, device_of, devices: int, policy: DropPolicy | None = None,
+                  load_aware=True, logits_mode=LOGITS_EXACT, forward=False, routing=False):
+    """simulate_step (ep_sim.hpp:110-160) on the device: the EpReport fields
+    (pre / post loads, thresholds, ideal load, drop rate, speed-up, stats);
+    routing=True adds the dropped RoutingDecision, forward=True the output
+    moe_forward(x, post)."""
+    torch = _torch()
+    x = _x(x, layer)
+    T = x.shape[0]
+    dv = np.ascontiguousarray(device_of, np.int32)
+    pre, post, th = (np.zeros(devices) for _ in range(3))
+    sc = np.zeros(3)
+    st = DropStatsC()
+    r = None
+    if routing:
+        r = RoutingDecision(T, layer.K * layer.P, layer.K, layer.P,
+                            torch.empty((T, layer.K * layer.P), dtype=torch.int32, device=x.device),
+                            torch.empty((T, layer.K * layer.P), dtype=torch.float32, device=x.device),
+                            torch.empty((T, layer.K * layer.P), dtype=torch.float64, device=x.device),
+                            torch.empty((T, layer.K * layer.P), dtype=torch.uint8, device=x.device))
+    ro = RoutingOut(r.indices.data_ptr(), r.raw.data_ptr(), r.normalized.data_ptr(),
+                    r.fraction_code.data_ptr()) if routing else None
+    y = torch.empty_like(x) if forward else None
+    _chk(lib().dsmoe_b200_simulate_step(ctx.h, layer.h, C.c_void_p(x.data_ptr()), T, devices, dv.ctypes.data,
+                                        C.byref((policy or DropPolicy()).c()), int(load_aware), logits_mode,
+                                        pre.ctypes.data, post.ctypes.data, th.ctypes.data, sc.ctypes.data,
+                                        C.byref(st), C.byref(ro) if routing else None, _p(y), 0))
+    rep = {"devices": devices, "load_aware": bool(load_aware), "pre_loads": pre, "post_loads": post,
+           "thresholds": th, "ideal_load": sc[0], "drop_rate": sc[1], "speedup": sc[2], "stats": st.as_dict()}
+    if routing:
+        r.stats = rep["stats"]
+    return rep, r, y
+
+
 def place_experts(num_experts: int, devices: int, strategy: str = "contiguous") -> np.ndarray:
     """place_experts (ep_sim.hpp:38-54)."""
     if not (devices >= 1 and num_experts >= devices):
