@@ -897,9 +897,7 @@ int dsmoe_b200_simulate_step(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer,
     std::vector<double> tu(static_cast<size_t>(E));
     for (int e = 0; e < E; ++e) tu[static_cast<size_t>(e)] = thresholds[device_of[e * P]];
     Buf d_tu(tu.size() * 8);
-    cudaStream_t s = nullptr;
     cuda(cudaMemcpy(d_tu.p, tu.data(), tu.size() * 8, cudaMemcpyHostToDevice), "H2D thresholds");
-    (void)s;
     dsmoe_b200_policy pol = *policy;
     pol.t_unit = policy->kind == DSMOE_B200_DROP_NONE ? nullptr : d_tu.as<double>();
     // 3. the dropped routing (from the same logits), its forward and its loads
@@ -914,6 +912,7 @@ int dsmoe_b200_simulate_step(dsmoe_b200_ctx* ctx, const dsmoe_b200_layer* layer,
       dev(dsmoe_b200_dispatch(ctx, layer, x, T, &pol, DSMOE_B200_LOGITS_REUSE, nullptr, nullptr, seg.data(), &R, &st));
     }
     if (post) dev(dsmoe_b200_route(ctx, layer, x, T, &pol, DSMOE_B200_LOGITS_REUSE, nullptr, nullptr, post, nullptr));
+    dev(dsmoe_b200_ctx_check(ctx));  // the threshold table is read until here
     std::fill(copies.begin(), copies.end(), 0);
     std::vector<double> halves(static_cast<size_t>(devices), 0.0);
     for (int e = 0; e < E; ++e) {
