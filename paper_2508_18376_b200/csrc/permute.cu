@@ -367,7 +367,18 @@ struct PermuteArgs {
   int do_plan;
 };
 
+#ifndef DSB_PERMUTE_PHASES
+#define DSB_PERMUTE_PHASES 0  // 1: block 0 prints the phase durations (diagnostic builds only)
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a) {
+  unsigned long long tp[6];
+  if (DSB_PERMUTE_PHASES) tp[0] = gtimer();
   namespace cg = cooperative_groups;
   extern __shared__ int dsm[];  // [2E bases | 4 x (2E carry | 8 x 2E warp counts)]
   __shared__ int off1[kPlanMaxUnits + 1], off2[kPlanMaxUnits + 1];
@@ -379,6 +390,7 @@ __global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   pdl_wait();
   pdl_trigger();
+  if (DSB_PERMUTE_PHASES) tp[1] = gtimer();
   // ---- phase A: per-code exclusive scans over chunks (scan_codes_kernel)
   for (int c = blockIdx.x; c < ncode; c += gridDim.x) {
     if (threadIdx.x == 0) s_carry = 0;
@@ -407,7 +419,9 @@ __global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a
     if (threadIdx.x == 0) a.code_tot[c] = s_carry;
     __syncthreads();
   }
+  if (DSB_PERMUTE_PHASES) tp[2] = gtimer();
   cg::this_grid().sync();
+  if (DSB_PERMUTE_PHASES) tp[3] = gtimer();
   // ---- phase B1: unit segments (every CTA, in shared memory)
   for (int u = threadIdx.x; u < a.E; u += blockDim.x) s_rows[u] = a.code_tot[2 * u] + a.code_tot[2 * u + 1];
   __syncthreads();
@@ -478,8 +492,15 @@ __global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a
       }
     }
   }
+  if (DSB_PERMUTE_PHASES) tp[4] = gtimer();
   // ---- phase B3: this CTA's share of the GEMM work lists
   if (a.do_plan) plan_body(a.plan, s_seg, off1, off2);
+  if (DSB_PERMUTE_PHASES) {
+    tp[5] = gtimer();
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+      printf("permute block %d: wait %llu  A %llu  sync %llu  B12 %llu  B3 %llu ns\n", blockIdx.x, tp[1] - tp[0],
+             tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4]);
+  }
 }
 
 int launch_permute_fused(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,

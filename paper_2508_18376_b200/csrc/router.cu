@@ -452,6 +452,16 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
   const size_t smem = static_cast<size_t>(2 * a.E) * sizeof(int);
   if (blocks <= 0) return 0;
   if (a.nsplit > 1 && !(a.E <= 64 && a.K <= 16)) return -1;  // split planes: quad router only
+  // DSMOE_B200_ROUTER_LPT=8: eight lanes per token (8 experts each) for E <= 64,
+  // K <= 8 — shorter per-lane chains, more tokens resident per SM (A/B knob)
+  static const int lpt_env = [] {
+    const char* v = getenv("DSMOE_B200_ROUTER_LPT");
+    return v ? atoi(v) : 4;
+  }();
+  if (lpt_env == 8 && a.E <= 64 && a.K <= 8 && a.nsplit <= 1) {
+    launch_pdl(router_quad_kernel<8, 8, 8>, dim3(blocks), dim3(kRouterChunk * 8), smem, stream, a);
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  }
   if (a.E <= 64 && a.K <= 16) {
     if (a.E <= 32 && a.K <= 8)
       launch_pdl(router_quad_kernel<8, 4, 8>, dim3(blocks), dim3(kRouterChunk * 4), smem, stream, a);
