@@ -16,6 +16,7 @@
 //                       chunk (warp __match_any + per-warp prefix), final row
 //   gather           -> X_perm[row] = X[token(row)], 16-byte vectors
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include "kernels.h"
 
