@@ -74,7 +74,7 @@ constexpr int kPlanMaxUnits = 2048;
 // rows every sub-block's chunks, afterwards only sub-block 0's.  GEMM2 tiles:
 // m-tile major, then d_model tiles.  Minor sub-blocks get tiles only for the
 // full rows, so FLOPs fall with the drop rate (no masks).
-__device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int* off2) {
+__device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int* off2, UnitInfo* su = nullptr) {
   const int nu = a.num_routed + a.num_shared;
   const int tm = a.tile_m ? a.tile_m : kTileM;     // GEMM1 rows per tile: 128 (single CTA) or 256 (CTA pair)
   const int tm2 = a.tile_m2 ? a.tile_m2 : tm;      // GEMM2 rows per tile
@@ -86,9 +86,16 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     const int s = u - a.num_routed;
     return UnitSeg{a.shared_row0 + s * a.T, a.T, a.T, 0};
   };
+  // the units' descriptors staged in shared memory when the caller provides
+  // room: the tile builders below read them many times in dependent order
+  if (su) {
+    for (int u = threadIdx.x; u < nu; u += blockDim.x) su[u] = a.units[unit_of(u)];
+    __syncthreads();
+  }
+  auto unit_info = [&](int u) -> const UnitInfo& { return su ? su[u] : a.units[unit_of(u)]; };
   // tile counts per unit, then block-wide exclusive scans
   for (int u = threadIdx.x; u < nu; u += blockDim.x) {
-    const UnitInfo& ui = a.units[unit_of(u)];
+    const UnitInfo& ui = unit_info(u);
     const UnitSeg sg = seg_of(u);
     const int mt_all = cdiv(sg.n_tot, tm), mt_full = cdiv(sg.n_full, tm);
     int c1 = 0;
@@ -120,10 +127,12 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     }
     return lo;
   };
-  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  // tiles interleaved over the blocks (tile i -> block i % grid) so every
+  // block builds a few instead of the first ones building them all
+  const int gtid = threadIdx.x * gridDim.x + blockIdx.x, gstride = gridDim.x * blockDim.x;
   for (int i = gtid; i < off1[nu]; i += gstride) {
     const int u = find(off1, i);
-    const UnitInfo& ui = a.units[unit_of(u)];
+    const UnitInfo& ui = unit_info(u);
     const UnitSeg sg = seg_of(u);
     const bool sh = ui.shared != 0;
     const int mt_full = cdiv(sg.n_full, tm);
@@ -163,7 +172,7 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
   }
   for (int i = gtid; i < off2[nu]; i += gstride) {
     const int u = find(off2, i);
-    const UnitInfo& ui = a.units[unit_of(u)];
+    const UnitInfo& ui = unit_info(u);
     const UnitSeg sg = seg_of(u);
     const int li = i - off2[u];
     const int mt = li / ntd, nt = li - mt * ntd;
@@ -495,7 +504,11 @@ __global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a
   }
   if (DSB_PERMUTE_PHASES) tp[4] = gtimer();
   // ---- phase B3: this CTA's share of the GEMM work lists
-  if (a.do_plan) plan_body(a.plan, s_seg, off1, off2);
+  if (a.do_plan) {
+    // after the scatter's dynamic region: room for the units' descriptors
+    UnitInfo* su = reinterpret_cast<UnitInfo*>(dsm + ((2 * a.E * (1 + 4 * (1 + 8)) + 3) & ~3));
+    plan_body(a.plan, s_seg, off1, off2, su);
+  }
   if (DSB_PERMUTE_PHASES) {
     tp[5] = gtimer();
     if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
@@ -512,7 +525,8 @@ int launch_permute_fused(const int* cnt_chunk, int nchunks, int E, int* chunk_of
   PermuteArgs a{cnt_chunk, nchunks, E, chunk_off, code_tot, code_base, seg, r_total, sel_code, sel_raw, T, K,
                 row_token, row_scale, slot_pos, plan ? *plan : PlanArgs{}, plan != nullptr};
   const int threads = 1024;
-  const size_t smem = static_cast<size_t>(2 * E) * (1 + 4 * (1 + 8)) * sizeof(int);
+  const size_t smem = static_cast<size_t>((2 * E * (1 + 4 * (1 + 8)) + 3) & ~3) * sizeof(int) +
+                      (plan ? sizeof(UnitInfo) * static_cast<size_t>(plan->num_routed + plan->num_shared) : 0);
   if (set_max_dyn_smem(permute_fused_kernel, smem) != cudaSuccess) return -2;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, permute_fused_kernel, threads, smem);
