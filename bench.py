@@ -671,15 +671,18 @@ def cpu_baseline_ep(cfg, world, t_drop):
                       f"{ncores} threads, {dt:.1f} s"}
 
 
-def stage_bytes(T, d, E, K, R, S, es=2):
+def stage_bytes(T, d, E, K, R, S, es=2, fused=False):
     """Algorithmic HBM bytes per launch of the non-GEMM kernels:
     the gate reads X and W_g and writes fp32 logits; the router reads the
     logits and writes one (code, score) pair per selection; the permutation
     reads those and writes row_token / row_scale per kept row and slot_pos per
     selection; the combine reads the R weighted expert rows (+ S*T shared
     rows) and writes the output."""
-    return {"gate": T * d * es + d * E * es + T * E * 4,
-            "router": T * E * 4 + T * K * 8,
+    if fused:  # K0 + K1 in one kernel: x and W_g in, logits + one (code, score) pair per selection out
+        first = {"gate_route": T * d * es + d * E * es + T * E * 4 + T * K * 8}
+    else:
+        first = {"gate": T * d * es + d * E * es + T * E * 4, "router": T * E * 4 + T * K * 8}
+    return {**first,
             "permute_plan": T * K * 8 + R * 8 + T * K * 4,
             "combine": (R + S * T) * d * es + T * d * es}
 
@@ -750,7 +753,10 @@ def run_single(args, local):
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    kb = stage_bytes(T, d, E, K, R, S)
+    fused = per["router"] == 0.0  # gate + router fused: the one kernel is timed as stage "gate"
+    if fused:
+        per["gate_route"] = per["gate"]
+    kb = stage_bytes(T, d, E, K, R, S, fused=fused)
     kernels = {k: {"us": r4(per[k] * 1e3), "GBps": r4(b / (per[k] * 1e-3) / 1e9),
                    "frac_hbm": r4(b / (per[k] * 1e-3) / 1e9 / hbm)} for k, b in kb.items() if per[k] > 0}
     kernels["gemm2"] = {"us": r4(per["gemm2"] * 1e3), "TFLOPs": r4(g2_tf), "frac": r4(g2_tf / peak_burst)}

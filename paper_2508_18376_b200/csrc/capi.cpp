@@ -660,8 +660,9 @@ struct dsmoe_b200_ctx {
     cnt_chunk.ensure(nchunks * 2 * L->E * 4 + 16);
     chunk_off.ensure(nchunks * 2 * L->E * 4 + 16);
     code_base.ensure(static_cast<size_t>(4 * L->E) * 4);  // [2E bases | 2E totals]
-    if (!counters.p) {  // [0..3] per call (zeroed by each routing), [4] sticky error flags
-      counters.ensure(8 * sizeof(unsigned long long));
+    if (!counters.p) {  // [0..3] per call (zeroed by each routing), [4] sticky error flags,
+                        // [8..11] the fused gate + router's accumulators (zero between launches)
+      counters.ensure(16 * sizeof(unsigned long long));
       cuda_check(cudaMemsetAsync(counters.p, 0, counters.bytes, stream), "memset");
     }
     row_token.ensure(static_cast<size_t>(Rcap + kRowSlack) * 4);
@@ -809,6 +810,7 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
                  const dsmoe_b200_routing* out, uint8_t* frac_ws, int logits_in_ld = 0) {
   cudaStream_t s = C->stream;
   bool counters_zeroed = false;  // the tensor-core gate kernel zeroes them in its prologue
+  bool fused = false;            // gate + router in one launch (tensor-mode logits)
   const float* lg = logits_in;
   int ld = logits_in_ld > 0 ? logits_in_ld : L->E;
   C->routed_T = T;
@@ -823,7 +825,21 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   }
   if (!lg) {
     const bool tc = logits_mode == DSMOE_B200_LOGITS_TENSOR && L->dtype == DSMOE_B200_BF16;
-    if (tc) {
+    // K0 + K1 in one kernel (gate_route_kernel, router.cu) unless a split gate
+    // is asked for; DSMOE_B200_GATE_ROUTE=0 keeps the two-kernel chain (A/B)
+    static const bool fuse_env = [] {
+      const char* v = std::getenv("DSMOE_B200_GATE_ROUTE");
+      return !v || std::atoi(v) != 0;
+    }();
+    static const bool split_req = [] {
+      const char* v = std::getenv("DSMOE_B200_GATE_SPLIT");
+      return v && std::atoi(v) > 1;
+    }();
+    fused = tc && fuse_env && !split_req && L->E <= 64 && L->K <= 16;
+    if (fused) {
+      C->logits.ensure(static_cast<size_t>(T) * L->Epad * 4 + 16);
+      ld = L->Epad;
+    } else if (tc) {
       // K may be split into S pieces over S CTAs per 128-token tile (partial
       // fp32 logit planes the router sums in ascending order and writes
       // back).  S depends on the layer only, never on T, so a token's logits
@@ -880,15 +896,15 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
                                             C->logits.as<float>(), T, L->d, L->E, s),
                    "gate logits");
     }
-    count_launch(1);
+    if (!fused) count_launch(1);
     lg = C->logits.as<float>();
     C->logits_layer = L;
     C->logits_T = T;
     C->logits_ld = ld;
   }
-  if (!counters_zeroed)
+  if (!counters_zeroed && !fused)  // the fused kernel publishes counters[0..3] itself
     cuda_check(cudaMemsetAsync(C->counters.p, 0, 4 * sizeof(unsigned long long), s), "memset");
-  C->mark(1);
+  if (!fused) C->mark(1);  // fused: the one kernel is timed as stage 0 (gate)
   RouterArgs a{};
   a.logits = lg;
   a.ld_logits = ld;
@@ -918,7 +934,14 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   a.nsplit = nsplit;
   a.split_stride = split_stride;
   a.logits_sum = nsplit > 1 ? C->logits.as<float>() : nullptr;
-  launch_check(launch_router(a, s), "router");
+  if (fused) {
+    const CUtensorMap mx = make_map(x, T, L->d, L->d, kTileM);
+    launch_check(launch_gate_route(&mx, &L->map_gate, a, L->Epad, L->d / kTileK, C->logits.as<float>(),
+                                   C->counters.as<unsigned long long>() + 8, num_sms(), s),
+                 "gate + router");
+  } else {
+    launch_check(launch_router(a, s), "router");
+  }
   count_launch(1);
   // after the router: with a split-K gate the summed logits exist only now
   if (logits_out && logits_out != lg) {

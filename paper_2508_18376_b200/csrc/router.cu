@@ -246,53 +246,21 @@ __device__ __forceinline__ void sort_desc(unsigned long long (&k)[N]) {
   }
 }
 
+// One token on a group of LPT lanes (lane q holds experts [q*EPT, (q+1)*EPT)
+// of its logits in v): softmax, top-K, replay, normalize, bands, and the
+// token's outputs (RoutingDecision slots, forward codes, s_hist counts).
+// Returns true when the token's top-K scores sum to <= 0 (normalize_topk
+// throws, dropping.hpp:67).  Shared by the standalone router and the fused
+// gate + router kernel, so both are the same arithmetic.
 template <int EPT, int LPT, int KK>
-__global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const RouterArgs a) {
-  extern __shared__ int s_hist[];  // 2E
-  __shared__ uint64_t tab[32];
-  __shared__ unsigned long long s_n1, s_nh;
-  static_assert(KK <= 16 && EPT <= 16, "quad router: at most 16 keys per lane");
+__device__ __forceinline__ bool quad_route(const RouterArgs& a, int t, bool tok_ok, float (&v)[EPT], int lane,
+                                           const uint64_t* tab, int* s_hist, unsigned long long& n1,
+                                           unsigned long long& nh) {
   constexpr int NS = KK > EPT ? KK : EPT;  // keys sorted per lane (padded with 0 = "no expert")
   const int E = a.E, K = a.K, P = a.P;
-  const int lane = threadIdx.x & 31, q = lane % LPT, qbase = lane - q;
-  for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) s_hist[i] = 0;
-  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
-  if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }
-  __syncthreads();
-  pdl_wait();
-  pdl_trigger();
-  unsigned long long n1 = 0, nh = 0;
-  const int t = blockIdx.x * kRouterChunk + threadIdx.x / LPT;
-  const bool tok_ok = t < a.T;  // uniform across the quad
+  const int q = lane % LPT, qbase = lane - q;
   const int e0 = q * EPT;
-  const float* row = a.logits + static_cast<long long>(tok_ok ? t : 0) * a.ld_logits;
-  float v[EPT];
-#pragma unroll
-  for (int i = 0; i < EPT; ++i) v[i] = (tok_ok && e0 + i < E) ? row[e0 + i] : -INFINITY;
-  if (a.nsplit > 1) {  // split-K gate: partial planes summed in ascending order, written back
-    for (int sp0 = 1; sp0 < a.nsplit; sp0 += 4) {  // 4 planes' loads in flight, then the ordered adds
-      float w[4][EPT];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float* rs = row + (sp0 + j) * a.split_stride;
-#pragma unroll
-        for (int i = 0; i < EPT; ++i) w[j][i] = (sp0 + j < a.nsplit && tok_ok && e0 + i < E) ? rs[e0 + i] : 0.0f;
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (sp0 + j < a.nsplit) {
-#pragma unroll
-          for (int i = 0; i < EPT; ++i)
-            if (e0 + i < E) v[i] = __fadd_rn(v[i], w[j][i]);
-        }
-    }
-    if (tok_ok) {
-      float* w = a.logits_sum + static_cast<long long>(t) * a.ld_logits;
-#pragma unroll
-      for (int i = 0; i < EPT; ++i)
-        if (e0 + i < E) w[e0 + i] = v[i];
-    }
-  }
+  bool bad = false;
   // softmax_inplace (matrix.hpp:68-78): max (order-free), expf, ascending-e sum, divide
   float mx = v[0];
 #pragma unroll
@@ -363,7 +331,7 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
 #pragma unroll
     for (int j = 0; j < KK; ++j)
       if (j < K) dsum = __dadd_rn(dsum, static_cast<double>(sraw[j]));
-    if (tok_ok && q == 0 && !(dsum > 0.0)) { atomicOr(&a.counters[2], 1ull); atomicOr(&a.counters[4], 1ull); }
+    bad = tok_ok && q == 0 && !(dsum > 0.0);
   }
   // this lane's slots j = q, q+LPT, ...; top_slot = first maximum of ns (dropping.hpp:99)
   constexpr int kSl = KK / LPT;
@@ -429,6 +397,59 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
       if (lv > 0) atomicAdd(&s_hist[2 * my_e + (lv == 2 ? 0 : 1)], 1);
     }
   }
+  return bad;
+}
+
+template <int EPT, int LPT, int KK>
+__global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const RouterArgs a) {
+  extern __shared__ int s_hist[];  // 2E
+  __shared__ uint64_t tab[32];
+  __shared__ unsigned long long s_n1, s_nh;
+  static_assert(KK <= 16 && EPT <= 16, "quad router: at most 16 keys per lane");
+  const int E = a.E;
+  const int lane = threadIdx.x & 31, q = lane % LPT, qbase = lane - q;
+  for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) s_hist[i] = 0;
+  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+  if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  unsigned long long n1 = 0, nh = 0;
+  const int t = blockIdx.x * kRouterChunk + threadIdx.x / LPT;
+  const bool tok_ok = t < a.T;  // uniform across the quad
+  const int e0 = q * EPT;
+  const float* row = a.logits + static_cast<long long>(tok_ok ? t : 0) * a.ld_logits;
+  float v[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) v[i] = (tok_ok && e0 + i < E) ? row[e0 + i] : -INFINITY;
+  if (a.nsplit > 1) {  // split-K gate: partial planes summed in ascending order, written back
+    for (int sp0 = 1; sp0 < a.nsplit; sp0 += 4) {  // 4 planes' loads in flight, then the ordered adds
+      float w[4][EPT];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float* rs = row + (sp0 + j) * a.split_stride;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) w[j][i] = (sp0 + j < a.nsplit && tok_ok && e0 + i < E) ? rs[e0 + i] : 0.0f;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (sp0 + j < a.nsplit) {
+#pragma unroll
+          for (int i = 0; i < EPT; ++i)
+            if (e0 + i < E) v[i] = __fadd_rn(v[i], w[j][i]);
+        }
+    }
+    if (tok_ok) {
+      float* w = a.logits_sum + static_cast<long long>(t) * a.ld_logits;
+#pragma unroll
+      for (int i = 0; i < EPT; ++i)
+        if (e0 + i < E) w[e0 + i] = v[i];
+    }
+  }
+  if (quad_route<EPT, LPT, KK>(a, t, tok_ok, v, lane, tab, s_hist, n1, nh)) {
+    atomicOr(&a.counters[2], 1ull);
+    atomicOr(&a.counters[4], 1ull);
+  }
   for (int o = 16; o > 0; o >>= 1) {
     n1 += __shfl_xor_sync(0xffffffffu, n1, o);
     nh += __shfl_xor_sync(0xffffffffu, nh, o);
@@ -482,6 +503,263 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
     launch_pdl(router_kernel<4>, dim3(blocks), dim3(kRouterChunk * 32), smem, stream, a);
   else
     launch_pdl(router_kernel<8>, dim3(blocks), dim3(kRouterChunk * 32), smem, stream, a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+// ---------------------------------------------------------------------------
+// K0 + K1 fused (bf16 layers on the tensor-mode gate, E <= 64, K <= 16): the
+// gate GEMM of one 128-token tile accumulates in TMEM and the same CTA routes
+// the tile — the logits never make a round trip through HBM, and the router's
+// launch, ramp and tail disappear into the gate kernel.
+//   warp 0       TMA producer: x rows (128 x 64) and gate rows (Epad x 64)
+//                into a kGrStages-deep ring, one full/empty barrier pair per
+//                stage;
+//   warp 1       TMEM allocator + tcgen05.mma issuer (M = 128, N = Epad),
+//                two accumulator stages (tile i+1's MMAs overlap tile i's
+//                routing when a CTA owns several tiles);
+//   warps 2..17  router: 8 (Epad 64) / 4 (Epad 32) of them drain the
+//                accumulator (tcgen05.ld 32x32b.x32) into a shared-memory
+//                logits tile (and the fp32 logits buffer that LOGITS_REUSE
+//                and the logits read-back use), then all 16 route 8 tokens
+//                each, four lanes per token — quad_route, the arithmetic of
+//                router_quad_kernel — and publish the tile's four 32-token
+//                chunk histograms.
+// The per-call counters (copies kept whole / half, error flags) are reduced
+// per CTA, accumulated in acc[0..2], and the last CTA to finish (acc[3]
+// counts them) moves them into counters[0..3] and re-zeroes acc: no memset and
+// no zeroing race with the atomics of other CTAs.
+// ---------------------------------------------------------------------------
+constexpr int kGrStages = 7;
+constexpr int kGrRouterWarps = 16;
+constexpr int kGrThreads = (2 + kGrRouterWarps) * 32;
+constexpr int kGrABytes = 128 * 64 * 2;
+constexpr int kGrBSlot = 64 * 64 * 2;
+
+template <int EPAD>
+struct GrGeo {
+  static constexpr int LGS = EPAD + 4;  // logits tile row stride (floats; 16-byte rows)
+  static constexpr int RING = kGrStages * (kGrABytes + kGrBSlot);
+  static constexpr int LG = 128 * LGS * 4;
+  static constexpr int HIST = 4 * 128 * 4;
+  static constexpr int SMEM = 1024 + RING + LG + HIST + 32 * 8 + (2 * kGrStages + 4) * 8 + 64;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
+struct GateRouteArgs {
+  RouterArgs r;
+  float* logits_out;         // T x Epad fp32 (row stride Epad), or null
+  int epad, nkb, ntiles;
+  unsigned long long* acc;   // [n1, nh, err, done], all zero between launches
+};
+
+__device__ __forceinline__ void router_bar_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kGrRouterWarps * 32) : "memory");
+}
+
+template <int EPAD, int EPT, int KK>
+__global__ void __launch_bounds__(kGrThreads, 1)
+    gate_route_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                      const GateRouteArgs g) {
+  using G = GrGeo<EPAD>;
+  constexpr int NS = kGrStages, LGS = G::LGS;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  uint8_t* ringA = smem;
+  uint8_t* ringB = smem + NS * kGrABytes;
+  float* lg = reinterpret_cast<float*>(smem + G::RING);
+  int* hist = reinterpret_cast<int*>(smem + G::RING + G::LG);
+  uint64_t* tab = reinterpret_cast<uint64_t*>(smem + G::RING + G::LG + G::HIST);
+  uint64_t* full = tab + 32;
+  uint64_t* empty = full + NS;
+  uint64_t* tfull = empty + NS;
+  uint64_t* tempty = tfull + 2;
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(tempty + 2);  // n1, nh, err
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red + 3);
+  const RouterArgs& a = g.r;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kLoaders = EPAD / 32 * 4;  // warps draining the accumulator: 32 columns x 32 lanes each
+  const uint32_t b_bytes = static_cast<uint32_t>(g.epad) * 128;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], kLoaders * 32);
+    }
+    red[0] = red[1] = red[2] = 0ull;
+    fence_mbar_init();
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+  }
+  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 2 * EPAD);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();     // x / the previous forward's readers of the routing buffers are done
+  pdl_trigger();  // the permutation may launch (it waits for this grid to complete)
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x)
+        for (int kb = 0; kb < g.nkb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], kGrABytes + b_bytes);
+          tma_load_2d(ringA + s * kGrABytes, &mapA, &full[s], kb * 64, tile * 128);
+          tma_load_2d(ringB + s * kGrBSlot, &mapB, &full[s], kb * 64, 0);
+          if (++s == NS) { s = 0; ph ^= 1; }
+        }
+    }
+  } else if (warp == 1) {
+    int s = 0, acc = 0;
+    uint32_t ph = 0, acc_phase = 0;
+    const uint64_t da0 = sdesc_sw128(smem_u32(ringA));
+    const uint64_t db0 = sdesc_sw128(smem_u32(ringB));
+    const uint32_t idesc = idesc_bf16(128, g.epad);
+    for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+      const uint32_t dtmem = tmem_base + acc * EPAD;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < g.nkb; ++kb) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint64_t adesc = da0 + static_cast<uint64_t>(s * (kGrABytes >> 4));
+        const uint64_t bdesc = db0 + static_cast<uint64_t>(s * (kGrBSlot >> 4));
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          umma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == NS) { s = 0; ph ^= 1; }
+      }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    const int rw = warp - 2;                 // router warp 0..15
+    const int quarter = warp & 3;            // TMEM lane quarter this warp may access
+    const int cb = rw >> 2;                  // loader: accumulator columns [32 cb, 32 cb + 32)
+    const int ncode = 2 * a.E;
+    const int nchunks = (a.T + kRouterChunk - 1) / kRouterChunk;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    unsigned long long n1 = 0, nh = 0;
+    bool bad = false;
+    for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+      if (rw < kLoaders) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld32(tmem_base + acc * EPAD + (static_cast<uint32_t>(quarter * 32) << 16) + 32 * cb, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        const int row = quarter * 32 + lane;
+        float4* dst = reinterpret_cast<float4*>(lg + row * LGS + 32 * cb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]), __uint_as_float(v[4 * i + 2]),
+                               __uint_as_float(v[4 * i + 3]));
+        const long long t = static_cast<long long>(tile) * 128 + row;
+        if (g.logits_out && t < a.T && 32 * cb < g.epad) {
+          uint4* o = reinterpret_cast<uint4*>(g.logits_out + t * g.epad + 32 * cb);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+      router_bar_sync();  // the tile's logits are in shared memory
+      {
+        const int tk = rw * 8 + (lane >> 2);
+        const int t = tile * 128 + tk;
+        const bool tok_ok = t < a.T;
+        const int e0 = (lane & 3) * EPT;
+        float v[EPT];
+        const float* src = lg + tk * LGS + e0;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) v[i] = (tok_ok && e0 + i < a.E) ? src[i] : -INFINITY;
+        bad |= quad_route<EPT, 4, KK>(a, t, tok_ok, v, lane, tab, hist + (rw >> 2) * ncode, n1, nh);
+      }
+      router_bar_sync();  // the tile's histograms are complete (and the logits tile is free)
+      for (int i = threadIdx.x - 64; i < 4 * ncode; i += kGrRouterWarps * 32) {
+        const int c = i / ncode, chunk = tile * 4 + c;
+        if (chunk < nchunks) a.cnt_chunk[static_cast<long long>(chunk) * ncode + (i - c * ncode)] = hist[i];
+        hist[i] = 0;  // the next tile's counts start after its first router_bar_sync
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+      nh += __shfl_xor_sync(0xffffffffu, nh, o);
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      if (n1) atomicAdd(&red[0], n1);
+      if (nh) atomicAdd(&red[1], nh);
+      if (bad) atomicOr(&red[2], 1ull);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, 2 * EPAD);
+  if (threadIdx.x == 0) {
+    if (red[0]) atomicAdd(&g.acc[0], red[0]);
+    if (red[1]) atomicAdd(&g.acc[1], red[1]);
+    if (red[2]) atomicOr(&g.acc[2], red[2]);
+    __threadfence();
+    if (atomicAdd(&g.acc[3], 1ull) == gridDim.x - 1) {  // last CTA: publish and re-arm
+      __threadfence();
+      const unsigned long long t1 = atomicExch(&g.acc[0], 0ull);
+      const unsigned long long th = atomicExch(&g.acc[1], 0ull);
+      const unsigned long long te = atomicExch(&g.acc[2], 0ull);
+      a.counters[0] = t1;
+      a.counters[1] = th;
+      a.counters[2] = te;
+      a.counters[3] = 0ull;
+      if (te) atomicOr(&a.counters[4], te);
+      atomicExch(&g.acc[3], 0ull);
+    }
+  }
+}
+
+int launch_gate_route(const CUtensorMap* mapA, const CUtensorMap* mapB, const RouterArgs& r, int epad, int nkb,
+                      float* logits_out, unsigned long long* acc, int num_sms, cudaStream_t stream) {
+  if (r.E > 64 || r.K > 16 || r.K < 1 || r.K > r.E || r.nsplit > 1 || (epad != 32 && epad != 64)) return -1;
+  const int ntiles = (r.T + 127) / 128;
+  if (ntiles <= 0) return 0;
+  GateRouteArgs g{r, logits_out, epad, nkb, ntiles, acc};
+  const int grid = ntiles < num_sms ? ntiles : num_sms;
+  cudaError_t err;
+#define DSB_GR(EP, EPT, KK)                                                                                  \
+  {                                                                                                          \
+    set_max_dyn_smem(gate_route_kernel<EP, EPT, KK>, GrGeo<EP>::SMEM);                                       \
+    err = launch_pdl(gate_route_kernel<EP, EPT, KK>, dim3(grid), dim3(kGrThreads), GrGeo<EP>::SMEM, stream, \
+                     *mapA, *mapB, g);                                                                       \
+  }
+  if (epad == 32) {
+    if (r.K <= 8)
+      DSB_GR(32, 8, 8)
+    else
+      DSB_GR(32, 8, 16)
+  } else {
+    if (r.K <= 8)
+      DSB_GR(64, 16, 8)
+    else
+      DSB_GR(64, 16, 16)
+  }
+#undef DSB_GR
+  if (err != cudaSuccess) return -2;
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
