@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kRouterChunk * LPT) router_quad_kernel(const R
   __shared__ unsigned long long s_n1, s_nh;
   static_assert(KK <= 16 && EPT <= 16, "quad router: at most 16 keys per lane");
   const int E = a.E;
-  const int lane = threadIdx.x & 31, q = lane % LPT, qbase = lane - q;
+  const int lane = threadIdx.x & 31, q = lane % LPT;
   for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) s_hist[i] = 0;
   if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
   if (threadIdx.x == 0) { s_n1 = 0; s_nh = 0; }

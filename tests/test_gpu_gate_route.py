@@ -31,9 +31,10 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 # (d, E, K, P, T, kind, t)
 CASES = [
     (256, 64, 8, 2, 40000, "2t", 0.10),  # 313 tiles: several tiles per CTA, both accumulator stages
-    (512, 32, 8, 1, 300, "2t", 0.10),    # Epad 32, partial last tile
+    (512, 32, 8, 2, 300, "2t", 0.10),    # Epad 32, partial last tile
     (256, 40, 6, 1, 1, "1t", 0.20),      # E < Epad = 64, one token
-    (256, 64, 16, 1, 777, "2t", 0.05),   # K = 16
+    (256, 64, 16, 2, 777, "2t", 0.05),   # K = 16
+    (256, 64, 8, 1, 2000, "1t", 0.08),   # P = 1
     (2048, 64, 8, 2, 4133, "2t", 0.085),  # C2 width
     (256, 24, 4, 2, 129, "none", 0.0),   # E < Epad = 32, no drop
 ]

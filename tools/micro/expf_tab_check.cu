@@ -3,6 +3,12 @@
 // tools/check_expf.sh) over all 2^32 float bit patterns, on the device.
 #include <cstdio>
 #include "../../paper_2508_18376_b200/csrc/router.cu"
+// router.cu's launchers opt kernels into large shared memory through pack.cu's helper
+namespace dsb {
+cudaError_t set_max_dyn_smem(const void* f, size_t b) {
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(b));
+}
+}  // namespace dsb
 using namespace dsb;
 __global__ void check(unsigned long long* bad, unsigned* first) {
   __shared__ uint64_t tab[32];
