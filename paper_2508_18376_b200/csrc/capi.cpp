@@ -935,7 +935,7 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   a.split_stride = split_stride;
   a.logits_sum = nsplit > 1 ? C->logits.as<float>() : nullptr;
   if (fused) {
-    const CUtensorMap mx = make_map(x, T, L->d, L->d, kTileM);
+    const CUtensorMap mx = make_map(x, T, L->d, L->d, gate_route_tile_rows());
     launch_check(launch_gate_route(&mx, &L->map_gate, a, L->Epad, L->d / kTileK, C->logits.as<float>(),
                                    C->counters.as<unsigned long long>() + 8, num_sms(), s),
                  "gate + router");

@@ -43,10 +43,11 @@ struct ImportArgs {
 };
 constexpr int kRouterChunk = 32;  // tokens per router block (one warp each) / scatter chunk
 int launch_router(const RouterArgs& a, cudaStream_t stream);
-// K0 + K1 fused (bf16, E <= 64, K <= 16, no split): mapA = x (128-row boxes),
+// K0 + K1 fused (bf16, E <= 64, K <= 16, no split): mapA = x (gate_route_tile_rows()-row boxes),
 // mapB = the layer's gate rows (Epad-row boxes); acc = 4 zeroed u64 per context
 int launch_gate_route(const CUtensorMap* mapA, const CUtensorMap* mapB, const RouterArgs& r, int epad, int nkb,
                       float* logits_out, unsigned long long* acc, int num_sms, cudaStream_t stream);
+int gate_route_tile_rows();
 int launch_rate_calibrate(const double* norm, int T, int K, int P, int S, int two_t, int keep_top1, double target,
                           double tol, int iters, unsigned long long* cnt, double* t_unit, int E, double* result,
                           int num_sms, cudaStream_t stream);

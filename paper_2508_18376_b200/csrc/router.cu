@@ -508,39 +508,48 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
 
 // ---------------------------------------------------------------------------
 // K0 + K1 fused (bf16 layers on the tensor-mode gate, E <= 64, K <= 16): the
-// gate GEMM of one 128-token tile accumulates in TMEM and the same CTA routes
+// gate GEMM of a 64-token tile accumulates in TMEM and the same CTA routes
 // the tile — the logits never make a round trip through HBM, and the router's
 // launch, ramp and tail disappear into the gate kernel.
-//   warp 0       TMA producer: x rows (128 x 64) and gate rows (Epad x 64)
-//                into a kGrStages-deep ring, one full/empty barrier pair per
-//                stage;
-//   warp 1       TMEM allocator + tcgen05.mma issuer (M = 128, N = Epad),
-//                two accumulator stages (tile i+1's MMAs overlap tile i's
-//                routing when a CTA owns several tiles);
-//   warps 2..17  router: 8 (Epad 64) / 4 (Epad 32) of them drain the
-//                accumulator (tcgen05.ld 32x32b.x32) into a shared-memory
-//                logits tile (and the fp32 logits buffer that LOGITS_REUSE
-//                and the logits read-back use), then all 16 route 8 tokens
-//                each, four lanes per token — quad_route, the arithmetic of
-//                router_quad_kernel — and publish the tile's four 32-token
+//   warp 0       TMA producer: x rows (64 x 64 boxes) and gate rows (Epad x
+//                64) into a kGrStages-deep ring, one full/empty barrier pair
+//                per stage;
+//   warp 1       TMEM allocator + tcgen05.mma issuer (M = 128 over a stage
+//                whose upper 64 rows are left over from earlier stages: those
+//                accumulator rows are never read; N = Epad), two accumulator
+//                stages;
+//   warps 2..17  two router groups of 8 warps; group g owns accumulator g and
+//                the CTA's tiles j = g, g + 2, ...: 4 (Epad 64) / 2 (Epad 32)
+//                of its warps drain the accumulator (tcgen05.ld 32x32b.x32,
+//                TMEM lanes 0-63) into the group's shared-memory logits tile
+//                (and the fp32 logits buffer that LOGITS_REUSE and the logits
+//                read-back use), then the 8 warps route 8 tokens each, four
+//                lanes per token — quad_route, the arithmetic of
+//                router_quad_kernel — and publish the tile's two 32-token
 //                chunk histograms.
+// 64-token tiles put a CTA on every SM at T = 16384 (256 tiles) and let one
+// group route tile j while the producer / MMA already stream tile j + 1 into
+// the other accumulator: the routing of all but each CTA's last tile hides
+// under the gate's HBM stream.
 // The per-call counters (copies kept whole / half, error flags) are reduced
 // per CTA, accumulated in acc[0..2], and the last CTA to finish (acc[3]
 // counts them) moves them into counters[0..3] and re-zeroes acc: no memset and
 // no zeroing race with the atomics of other CTAs.
 // ---------------------------------------------------------------------------
 constexpr int kGrStages = 7;
-constexpr int kGrRouterWarps = 16;
-constexpr int kGrThreads = (2 + kGrRouterWarps) * 32;
-constexpr int kGrABytes = 128 * 64 * 2;
+constexpr int kGrRows = 64;                 // tokens per tile
+constexpr int kGrGroupWarps = 8;            // router warps per group (64 tokens x 4 lanes)
+constexpr int kGrThreads = (2 + 2 * kGrGroupWarps) * 32;
+constexpr int kGrASlot = 128 * 64 * 2;      // the M = 128 MMA reads a whole 128-row slot
 constexpr int kGrBSlot = 64 * 64 * 2;
+constexpr int kGrChunks = kGrRows / kRouterChunk;
 
 template <int EPAD>
 struct GrGeo {
   static constexpr int LGS = EPAD + 4;  // logits tile row stride (floats; 16-byte rows)
-  static constexpr int RING = kGrStages * (kGrABytes + kGrBSlot);
-  static constexpr int LG = 128 * LGS * 4;
-  static constexpr int HIST = 4 * 128 * 4;
+  static constexpr int RING = kGrStages * (kGrASlot + kGrBSlot);
+  static constexpr int LG = 2 * kGrRows * LGS * 4;          // one logits tile per group
+  static constexpr int HIST = 2 * kGrChunks * 128 * 4;      // per group: its tile's chunk histograms (2E <= 128)
   static constexpr int SMEM = 1024 + RING + LG + HIST + 32 * 8 + (2 * kGrStages + 4) * 8 + 64;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
@@ -552,8 +561,8 @@ struct GateRouteArgs {
   unsigned long long* acc;   // [n1, nh, err, done], all zero between launches
 };
 
-__device__ __forceinline__ void router_bar_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kGrRouterWarps * 32) : "memory");
+__device__ __forceinline__ void group_bar_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kGrGroupWarps * 32) : "memory");
 }
 
 template <int EPAD, int EPT, int KK>
@@ -566,9 +575,9 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* ringA = smem;
-  uint8_t* ringB = smem + NS * kGrABytes;
-  float* lg = reinterpret_cast<float*>(smem + G::RING);
-  int* hist = reinterpret_cast<int*>(smem + G::RING + G::LG);
+  uint8_t* ringB = smem + NS * kGrASlot;
+  float* lg_all = reinterpret_cast<float*>(smem + G::RING);
+  int* hist_all = reinterpret_cast<int*>(smem + G::RING + G::LG);
   uint64_t* tab = reinterpret_cast<uint64_t*>(smem + G::RING + G::LG + G::HIST);
   uint64_t* full = tab + 32;
   uint64_t* empty = full + NS;
@@ -578,8 +587,8 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red + 3);
   const RouterArgs& a = g.r;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kLoaders = EPAD / 32 * 4;  // warps draining the accumulator: 32 columns x 32 lanes each
-  const uint32_t b_bytes = static_cast<uint32_t>(g.epad) * 128;
+  constexpr int kLoaders = 2 * (EPAD / 32);  // warps per group draining TMEM lanes 0-63, 32 columns each
+  const uint32_t tx_bytes = static_cast<uint32_t>(kGrRows * 128 + g.epad * 128);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
@@ -594,7 +603,7 @@ __global__ void __launch_bounds__(kGrThreads, 1)
     tma_prefetch(&mapA);
     tma_prefetch(&mapB);
   }
-  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) hist[i] = 0;
+  for (int i = threadIdx.x; i < 2 * kGrChunks * 128; i += blockDim.x) hist_all[i] = 0;
   if (threadIdx.x < 32) tab[threadIdx.x] = kExp2fTab[threadIdx.x];
   if (warp == 1) {
     tmem_alloc(tmem_slot, 2 * EPAD);
@@ -613,9 +622,14 @@ __global__ void __launch_bounds__(kGrThreads, 1)
       for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x)
         for (int kb = 0; kb < g.nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], kGrABytes + b_bytes);
-          tma_load_2d(ringA + s * kGrABytes, &mapA, &full[s], kb * 64, tile * 128);
+#ifdef DSB_GR_DIAG_NO_B  // diagnostic builds only: gate rows not streamed (wrong logits; timing of the x stream)
+          mbar_expect_tx(&full[s], kGrRows * 128);
+          tma_load_2d(ringA + s * kGrASlot, &mapA, &full[s], kb * 64, tile * kGrRows);
+#else
+          mbar_expect_tx(&full[s], tx_bytes);
+          tma_load_2d(ringA + s * kGrASlot, &mapA, &full[s], kb * 64, tile * kGrRows);
           tma_load_2d(ringB + s * kGrBSlot, &mapB, &full[s], kb * 64, 0);
+#endif
           if (++s == NS) { s = 0; ph ^= 1; }
         }
     }
@@ -632,7 +646,7 @@ __global__ void __launch_bounds__(kGrThreads, 1)
       for (int kb = 0; kb < g.nkb; ++kb) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint64_t adesc = da0 + static_cast<uint64_t>(s * (kGrABytes >> 4));
+        const uint64_t adesc = da0 + static_cast<uint64_t>(s * (kGrASlot >> 4));
         const uint64_t bdesc = db0 + static_cast<uint64_t>(s * (kGrBSlot >> 4));
         if (elect_one()) {
 #pragma unroll
@@ -647,56 +661,67 @@ __global__ void __launch_bounds__(kGrThreads, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else {
-    const int rw = warp - 2;                 // router warp 0..15
-    const int quarter = warp & 3;            // TMEM lane quarter this warp may access
-    const int cb = rw >> 2;                  // loader: accumulator columns [32 cb, 32 cb + 32)
+    const int rw = warp - 2;                   // router warp 0..15
+    const int grp = rw / kGrGroupWarps;        // accumulator / tile parity this warp serves
+    const int gw = rw % kGrGroupWarps;         // warp within the group: tokens [8 gw, 8 gw + 8)
+    const int quarter = warp & 3;              // TMEM lane quarter this warp may access
+    const int cb = gw >> 2;                    // loader: accumulator columns [32 cb, 32 cb + 32)
+    const bool loader = quarter < 2 && cb < EPAD / 32;
     const int ncode = 2 * a.E;
     const int nchunks = (a.T + kRouterChunk - 1) / kRouterChunk;
-    int acc = 0;
+    float* lg = lg_all + grp * kGrRows * LGS;
+    int* hist = hist_all + grp * kGrChunks * 128;
+    const int gtid = threadIdx.x - 64 - grp * kGrGroupWarps * 32;
     uint32_t acc_phase = 0;
     unsigned long long n1 = 0, nh = 0;
     bool bad = false;
-    for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
-      if (rw < kLoaders) {
-        mbar_wait(&tfull[acc], acc_phase);
+    for (int tile = blockIdx.x + grp * gridDim.x; tile < g.ntiles; tile += 2 * gridDim.x) {
+      if (loader) {
+        mbar_wait(&tfull[grp], acc_phase);
         tc_fence_after();
         uint32_t v[32];
-        tmem_ld32(tmem_base + acc * EPAD + (static_cast<uint32_t>(quarter * 32) << 16) + 32 * cb, v);
+        tmem_ld32(tmem_base + grp * EPAD + (static_cast<uint32_t>(quarter * 32) << 16) + 32 * cb, v);
         tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        mbar_arrive(&tempty[grp]);
         const int row = quarter * 32 + lane;
         float4* dst = reinterpret_cast<float4*>(lg + row * LGS + 32 * cb);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]), __uint_as_float(v[4 * i + 2]),
                                __uint_as_float(v[4 * i + 3]));
-        const long long t = static_cast<long long>(tile) * 128 + row;
+        const long long t = static_cast<long long>(tile) * kGrRows + row;
         if (g.logits_out && t < a.T && 32 * cb < g.epad) {
           uint4* o = reinterpret_cast<uint4*>(g.logits_out + t * g.epad + 32 * cb);
 #pragma unroll
           for (int i = 0; i < 8; ++i) o[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         }
       }
-      router_bar_sync();  // the tile's logits are in shared memory
+      acc_phase ^= 1;
+      group_bar_sync(grp);  // the tile's logits are in shared memory
       {
-        const int tk = rw * 8 + (lane >> 2);
-        const int t = tile * 128 + tk;
+        const int tk = gw * 8 + (lane >> 2);
+        const int t = tile * kGrRows + tk;
         const bool tok_ok = t < a.T;
         const int e0 = (lane & 3) * EPT;
         float v[EPT];
         const float* src = lg + tk * LGS + e0;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) v[i] = (tok_ok && e0 + i < a.E) ? src[i] : -INFINITY;
-        bad |= quad_route<EPT, 4, KK>(a, t, tok_ok, v, lane, tab, hist + (rw >> 2) * ncode, n1, nh);
+#ifndef DSB_GR_DIAG_NO_ROUTE  // diagnostic builds only: the gate phase alone
+        bad |= quad_route<EPT, 4, KK>(a, t, tok_ok, v, lane, tab, hist + (gw >> 2) * ncode, n1, nh);
+#else
+        if (v[0] == 12345.f) bad = true;
+        if (tok_ok && (lane & 3) == 0)
+          for (int j = 0; j < a.K; ++j) a.sel_code[static_cast<long long>(t) * a.K + j] = -1;
+#endif
       }
-      router_bar_sync();  // the tile's histograms are complete (and the logits tile is free)
-      for (int i = threadIdx.x - 64; i < 4 * ncode; i += kGrRouterWarps * 32) {
-        const int c = i / ncode, chunk = tile * 4 + c;
+      group_bar_sync(grp);  // the tile's histograms are complete (and the logits tile is free)
+      for (int i = gtid; i < kGrChunks * ncode; i += kGrGroupWarps * 32) {
+        const int c = i / ncode, chunk = tile * kGrChunks + c;
         if (chunk < nchunks) a.cnt_chunk[static_cast<long long>(chunk) * ncode + (i - c * ncode)] = hist[i];
-        hist[i] = 0;  // the next tile's counts start after its first router_bar_sync
+        hist[i] = 0;  // the group's next tile counts after its first group_bar_sync
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -733,10 +758,12 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   }
 }
 
+int gate_route_tile_rows() { return kGrRows; }
+
 int launch_gate_route(const CUtensorMap* mapA, const CUtensorMap* mapB, const RouterArgs& r, int epad, int nkb,
                       float* logits_out, unsigned long long* acc, int num_sms, cudaStream_t stream) {
   if (r.E > 64 || r.K > 16 || r.K < 1 || r.K > r.E || r.nsplit > 1 || (epad != 32 && epad != 64)) return -1;
-  const int ntiles = (r.T + 127) / 128;
+  const int ntiles = (r.T + kGrRows - 1) / kGrRows;
   if (ntiles <= 0) return 0;
   GateRouteArgs g{r, logits_out, epad, nkb, ntiles, acc};
   const int grid = ntiles < num_sms ? ntiles : num_sms;

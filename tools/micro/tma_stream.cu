@@ -1,0 +1,166 @@
+// Micro-benchmark: how fast can TMA stream a row-major bf16 [T x d] token
+// matrix (the gate GEMM's A operand) into shared memory, with the access
+// pattern of the gate kernel (64-column x R-row boxes, k-blocks of one row
+// tile issued back to back)?  One CTA per SM, an NS-stage ring, a consumer
+// warp that only releases stages.  Prints GB/s per (rows, stages, grid).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/micro/tma_stream.cu -o tools/micro/tma_stream
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include "../../paper_2508_18376_b200/csrc/common.cuh"
+using namespace dsb;
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__global__ void __launch_bounds__(64, 1) stream3_kernel(const __grid_constant__ CUtensorMap map, int ntiles, int nkb,
+                                                         int rows, int kbs, int ns) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * 16384);
+  uint64_t* empty = full + ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t bytes = rows * 128 * kbs;
+  if (warp == 0 && lane == 0) {
+    int s = 0; uint32_t ph = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int kb = 0; kb < nkb; kb += kbs) {
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], bytes);
+        tma_load_3d(smem + s * 16384, &map, &full[s], 0, kb, t * rows);
+        if (++s == ns) { s = 0; ph ^= 1; }
+      }
+  } else if (warp == 1 && lane == 0) {
+    int s = 0; uint32_t ph = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int kb = 0; kb < nkb; kb += kbs) {
+        mbar_wait(&full[s], ph);
+        mbar_arrive(&empty[s]);
+        if (++s == ns) { s = 0; ph ^= 1; }
+      }
+  }
+}
+
+__global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap map, int ntiles, int nkb,
+                                                        int rows, int ns) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * 16384);
+  uint64_t* empty = full + ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t bytes = rows * 128;
+  if (warp == 0 && lane == 0) {
+    int s = 0; uint32_t ph = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], bytes);
+        tma_load_2d(smem + s * 16384, &map, &full[s], kb * 64, t * rows);
+        if (++s == ns) { s = 0; ph ^= 1; }
+      }
+  } else if (warp == 1 && lane == 0) {
+    int s = 0; uint32_t ph = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[s], ph);
+        mbar_arrive(&empty[s]);
+        if (++s == ns) { s = 0; ph ^= 1; }
+      }
+  }
+}
+
+int main(int argc, char** argv) {
+  const long long T = argc > 1 ? atoll(argv[1]) : 16384, d = 2048;
+  void* x;
+  cudaMalloc(&x, T * d * 2);
+  cudaMemset(x, 0, T * d * 2);
+  void* flush;
+  const size_t fl = 512ull << 20;
+  cudaMalloc(&flush, fl);
+  PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int rows : {64, 128}) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)T};
+    cuuint64_t strides[1] = {(cuuint64_t)(d * 2)};
+    cuuint32_t box[2] = {64, (cuuint32_t)rows};
+    cuuint32_t es[2] = {1, 1};
+    enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const int ntiles = T / rows;
+    for (int ns : {4, 7, 10, 13}) {
+      for (int grid : {128, 148}) {
+        if (grid > ntiles) continue;
+        const size_t smem = ns * 16384 + 2 * ns * 8 + 1024;
+        float best = 1e9;
+        for (int it = 0; it < 5; ++it) {
+          cudaMemset(flush, it, fl);  // evict x from L2
+          cudaEventRecord(e0);
+          stream_kernel<<<grid, 64, smem>>>(m, ntiles, d / 64, rows, ns);
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (ms < best) best = ms;
+        }
+        printf("rows %3d stages %2d grid %3d: %7.2f us  %6.0f GB/s  (%s)\n", rows, ns, grid, best * 1e3,
+               T * d * 2 / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+  }
+  for (int kbs : {2, 4, 8}) {
+    const int rows = 128 / kbs;  // 16 KB per request
+    CUtensorMap m;
+    cuuint64_t dims[3] = {64, (cuuint64_t)(d / 64), (cuuint64_t)T};
+    cuuint64_t strides[2] = {128, (cuuint64_t)(d * 2)};
+    cuuint32_t box[3] = {64, (cuuint32_t)kbs, (cuuint32_t)rows};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("encode 3d failed %d\n", (int)r); continue; }
+    const int ntiles = T / rows;
+    for (int ns : {7, 10, 13}) {
+      for (int grid : {128, 148}) {
+        const size_t smem = ns * 16384 + 2 * ns * 8 + 1024;
+        cudaFuncSetAttribute(stream3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        float best = 1e9;
+        for (int it = 0; it < 5; ++it) {
+          cudaMemset(flush, it, fl);
+          cudaEventRecord(e0);
+          stream3_kernel<<<grid, 64, smem>>>(m, ntiles, d / 64, rows, kbs, ns);
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          if (ms < best) best = ms;
+        }
+        printf("3d: rows %3d x %d k-blocks (%4d B/row) stages %2d grid %3d: %7.2f us  %6.0f GB/s  (%s)\n", rows, kbs,
+               kbs * 128, ns, grid, best * 1e3, T * d * 2 / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+  }
+  return 0;
+}
