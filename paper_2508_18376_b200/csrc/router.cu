@@ -252,6 +252,47 @@ __device__ __forceinline__ void sort_desc(unsigned long long (&k)[N]) {
 // Returns true when the token's top-K scores sum to <= 0 (normalize_topk
 // throws, dropping.hpp:67).  Shared by the standalone router and the fused
 // gate + router kernel, so both are the same arithmetic.
+// Descending 8-key sort with the 19-comparator, depth-6 network (Batcher /
+// Knuth's optimum for 8 inputs; checked with the 0-1 principle) instead of the
+// 24-comparator bitonic network.
+__device__ __forceinline__ void cex_desc(unsigned long long& a, unsigned long long& b) {
+  const unsigned long long x = a, y = b;
+  const bool sw = x < y;
+  a = sw ? y : x;
+  b = sw ? x : y;
+}
+__device__ __forceinline__ void sort8_desc(unsigned long long* k) {
+  cex_desc(k[0], k[2]); cex_desc(k[1], k[3]); cex_desc(k[4], k[6]); cex_desc(k[5], k[7]);
+  cex_desc(k[0], k[4]); cex_desc(k[1], k[5]); cex_desc(k[2], k[6]); cex_desc(k[3], k[7]);
+  cex_desc(k[0], k[1]); cex_desc(k[2], k[3]); cex_desc(k[4], k[5]); cex_desc(k[6], k[7]);
+  cex_desc(k[2], k[4]); cex_desc(k[3], k[5]);
+  cex_desc(k[1], k[4]); cex_desc(k[3], k[6]);
+  cex_desc(k[1], k[2]); cex_desc(k[3], k[4]); cex_desc(k[5], k[6]);
+}
+// the lane's top KK keys, descending, in key[0..KK).  EPT = 2 KK = 16: sort
+// both halves (2 x 19 comparators), keep max(a[i], b[KK-1-i]) (a bitonic
+// sequence holding the top KK of the union) and merge it (12) — 50
+// comparators + 8 maxima instead of the 80 of a 16-key bitonic sort.
+template <int NS, int EPT, int KK>
+__device__ __forceinline__ void lane_topk(unsigned long long (&key)[NS]) {
+  if constexpr (EPT == 16 && KK == 8 && NS == 16) {
+    sort8_desc(key);
+    sort8_desc(key + 8);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) key[i] = key[i] > key[15 - i] ? key[i] : key[15 - i];
+#pragma unroll
+    for (int j = 4; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int l = i ^ j;
+        if (l > i) cex_desc(key[i], key[l]);
+      }
+    }
+  } else {
+    sort_desc<NS>(key);
+  }
+}
+
 template <int EPT, int LPT, int KK>
 __device__ __forceinline__ bool quad_route(const RouterArgs& a, int t, bool tok_ok, float (&v)[EPT], int lane,
                                            const uint64_t* tab, int* s_hist, unsigned long long& n1,
@@ -293,7 +334,7 @@ __device__ __forceinline__ bool quad_route(const RouterArgs& a, int t, bool tok_
                                       static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<unsigned>(e))
                                 : 0ull;
   }
-  sort_desc<NS>(key);
+  lane_topk<NS, EPT, KK>(key);
 #pragma unroll
   for (int m = 1; m < LPT; m <<= 1) {
     // top KK of (mine U partner's): max(mine[i], theirs[KK-1-i]) is bitonic

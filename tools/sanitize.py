@@ -20,7 +20,8 @@ def layer(d, ffn, E, K, S=0, P=2, dtype="bf16", seed=1):
 
 
 for (d, ffn, E, K, S, T, dt) in [(256, 256, 8, 2, 0, 300, "bf16"), (256, 192, 16, 4, 1, 257, "bf16"),
-                                 (128, 128, 8, 2, 0, 100, "f32")]:
+                                 (128, 128, 8, 2, 0, 100, "f32"),
+                                 (128, 64, 32, 8, 0, 12000, "bf16")]:  # gate_route: two tiles per CTA
     L, dl = layer(d, ffn, E, K, S, dtype=dt)
     x = torch.from_numpy(O.generate_tokens(T, d, 5)).cuda()
     if dt == "bf16":
