@@ -571,6 +571,11 @@ struct dsmoe_b200_ctx {
       scalars;
   DevBuf tiles1, tiles2, tiles_gate, xperm, H, Y, frac_ws, vseg, vseg_unit;
   DevBuf rate_norm, rate_cnt, rate_tunit, rate_result;  // rate-targeted drop (dsmoe_b200_forward_rate)
+  // superchunk histograms of the fused gate + router (2 x kScCap x kScCodes,
+  // zero at allocation, double-buffered by counters[12]); sc_T = token count of
+  // the last routing that filled them, -1 when cnt_chunk came from elsewhere
+  DevBuf sc_hist;
+  int sc_T = -1;
   // EP with one row per (token, rank): last ep_pack's layout on this context
   DevBuf ep_pos_td, ep_send_token, ep_cnt, ep_tot, ep_owner, ep_base;
   int ep_N = 0, ep_T = -1;
@@ -664,6 +669,10 @@ struct dsmoe_b200_ctx {
                         // [8..11] the fused gate + router's accumulators (zero between launches)
       counters.ensure(16 * sizeof(unsigned long long));
       cuda_check(cudaMemsetAsync(counters.p, 0, counters.bytes, stream), "memset");
+    }
+    if (!sc_hist.p) {
+      sc_hist.ensure(2ull * kScCap * kScCodes * sizeof(int));
+      cuda_check(cudaMemsetAsync(sc_hist.p, 0, sc_hist.bytes, stream), "memset");
     }
     row_token.ensure(static_cast<size_t>(Rcap + kRowSlack) * 4);
     seg.ensure(sizeof(UnitSeg) * L->E);
@@ -936,11 +945,18 @@ void stage_route(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* x, in
   a.logits_sum = nsplit > 1 ? C->logits.as<float>() : nullptr;
   if (fused) {
     const CUtensorMap mx = make_map(x, T, L->d, L->d, gate_route_tile_rows());
+    static const bool sc_env = [] {  // DSMOE_B200_PERMUTE_SC=0: the permutation scans every chunk itself
+      const char* v = std::getenv("DSMOE_B200_PERMUTE_SC");
+      return !(v && std::atoi(v) == 0);
+    }();
     launch_check(launch_gate_route(&mx, &L->map_gate, a, L->Epad, L->d / kTileK, C->logits.as<float>(),
-                                   C->counters.as<unsigned long long>() + 8, num_sms(), s),
+                                   C->counters.as<unsigned long long>() + 8, num_sms(), s,
+                                   sc_env ? C->sc_hist.as<int>() : nullptr),
                  "gate + router");
+    C->sc_T = sc_env ? T : -1;
   } else {
     launch_check(launch_router(a, s), "router");
+    C->sc_T = -1;
   }
   count_launch(1);
   // after the router: with a split-K gate the summed logits exist only now
@@ -981,12 +997,15 @@ void stage_permute(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, int T, bool pla
     return v && std::string(v) == "split";
   }();
   if (!split) {
+    // after the fused gate + router: chunk offsets from its superchunk sums
+    const bool sc = C->sc_T == T && L->E <= 64;
     launch_check(launch_permute_fused(C->cnt_chunk.as<int>(), nchunks, L->E, C->chunk_off.as<int>(),
                                       C->code_base.as<int>(), C->seg.as<UnitSeg>(), r_total,
                                       C->code_base.as<int>() + 2 * L->E, C->sel_code.as<int32_t>(),
                                       C->sel_raw.as<float>(), T, L->K, C->row_token.as<int32_t>(),
                                       C->row_scale.as<float>(), C->slot_pos.as<int32_t>(), plan ? &pa : nullptr,
-                                      num_sms(), s),
+                                      num_sms(), s, sc ? C->sc_hist.as<int>() : nullptr,
+                                      sc ? C->counters.as<unsigned long long>() + 12 : nullptr),
                  "permute");
     count_launch(1);
     return;
@@ -1325,6 +1344,7 @@ int dsmoe_b200_moe_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
     a.sel_raw = C->sel_raw.as<float>();
     a.cnt_chunk = C->cnt_chunk.as<int>();
     a.counters = C->counters.as<unsigned long long>();
+    C->sc_T = -1;
     launch_check(launch_import_routing(a, s), "import routing");
     count_launch(1);
     unsigned long long h[5];
@@ -1357,6 +1377,7 @@ int dsmoe_b200_moe_forward(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const v
     b.sel_code = C->sel_code.as<int32_t>();
     b.sel_raw = C->sel_raw.as<float>();
     b.cnt_chunk = C->cnt_chunk.as<int>();
+    C->sc_T = -1;
     launch_check(launch_import_routing(b, s), "import routing (block view)");
     count_launch(1);
     stage_ffn(C, B, x, T, out);
@@ -1654,6 +1675,7 @@ void ep_expert_impl(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* ro
                                static_cast<size_t>(nranks + 1) * 8, cudaMemcpyHostToDevice, s), "H2D");
     const int nchunks = (Ti + kRouterChunk - 1) / kRouterChunk;
     cuda_check(cudaMemsetAsync(C->sel_code.p, 0xFF, static_cast<size_t>(Ti) * L->K * 4, s), "memset");
+    C->sc_T = -1;
     cuda_check(cudaMemsetAsync(C->cnt_chunk.p, 0, static_cast<size_t>(nchunks) * 2 * L->E * 4, s), "memset");
     const long long* b = C->ep_base.as<long long>();
     launch_check(launch_ep_local_routing(rec_code, rec_row, rec_raw, S, rec_stride, b, b + nranks + 1, nranks, L->K,
@@ -2184,6 +2206,7 @@ int dsmoe_b200_profile_importance(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, 
     a.sel_raw = C->sel_raw.as<float>();
     a.cnt_chunk = C->cnt_chunk.as<int>();
     a.counters = C->counters.as<unsigned long long>();
+    C->sc_T = -1;
     launch_check(launch_import_routing(a, s), "import routing");
     stage_permute(C, L, T, false);
     unsigned long long flags[5];

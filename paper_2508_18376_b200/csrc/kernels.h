@@ -45,9 +45,16 @@ constexpr int kRouterChunk = 32;  // tokens per router block (one warp each) / s
 int launch_router(const RouterArgs& a, cudaStream_t stream);
 // K0 + K1 fused (bf16, E <= 64, K <= 16, no split): mapA = x (gate_route_tile_rows()-row boxes),
 // mapB = the layer's gate rows (Epad-row boxes); acc = 4 zeroed u64 per context
+// sc (optional): 2 x kScCap x kScCodes ints, zero at allocation — the launch adds
+// every tile's histogram into its superchunk (gate_route_sc_chunks(T) chunks) of
+// buffer acc[4] & 1, clears the other buffer and advances acc[4]; the
+// permutation then needs no chunk scan (launch_permute_fused with sc)
+constexpr int kScCap = 64, kScCodes = 128;
 int launch_gate_route(const CUtensorMap* mapA, const CUtensorMap* mapB, const RouterArgs& r, int epad, int nkb,
-                      float* logits_out, unsigned long long* acc, int num_sms, cudaStream_t stream);
+                      float* logits_out, unsigned long long* acc, int num_sms, cudaStream_t stream,
+                      int* sc = nullptr);
 int gate_route_tile_rows();
+int gate_route_sc_chunks(int T);
 int launch_rate_calibrate(const double* norm, int T, int K, int P, int S, int two_t, int keep_top1, double target,
                           double tol, int iters, unsigned long long* cnt, double* t_unit, int E, double* result,
                           int num_sms, cudaStream_t stream);
@@ -76,10 +83,12 @@ int launch_scan_plan(const int* cnt_chunk, int nchunks, int E, int* chunk_off, i
                      int* r_total, int* code_tot, const PlanArgs* plan, int num_sms, cudaStream_t stream);
 int launch_plan(const PlanArgs& a, int num_sms, cudaStream_t stream);
 // scan + segments + ordered scatter (+ work lists) in one cooperative launch
+// sc / sc_epoch (E <= 64, after launch_gate_route with sc): chunk offsets from
+// the superchunk histograms — no chunk scan, no grid-wide barrier
 int launch_permute_fused(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
                          int* r_total, int* code_tot, const int32_t* sel_code, const float* sel_raw, int T, int K,
                          int32_t* row_token, float* row_scale, int32_t* slot_pos, const PlanArgs* plan, int num_sms,
-                         cudaStream_t stream);
+                         cudaStream_t stream, const int* sc = nullptr, const unsigned long long* sc_epoch = nullptr);
 int launch_scatter(const int32_t* sel_code, const float* sel_raw, int T, int K, int E, const int* chunk_off,
                    const int* code_base, int32_t* row_token, float* row_scale, int32_t* slot_pos, cudaStream_t stream);
 int launch_gather(const void* x, void* xp, const int32_t* row_token, const int* r_total,

@@ -22,6 +22,19 @@
 
 namespace dsb {
 
+#ifndef DSB_PERMUTE_PHASES
+#define DSB_PERMUTE_PHASES 0  // 1: blocks 0, 73, last print the phase durations (diagnostic builds only)
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__shared__ unsigned long long s_tq[3];  // diagnostic builds: plan sub-phase timestamps
+__device__ inline bool phase_block() {
+  return DSB_PERMUTE_PHASES && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 73 || blockIdx.x == gridDim.x - 1);
+}
+
 __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 // Block-wide exclusive scan of v[0..n) in shared memory, in place; returns
@@ -74,7 +87,10 @@ constexpr int kPlanMaxUnits = 2048;
 // rows every sub-block's chunks, afterwards only sub-block 0's.  GEMM2 tiles:
 // m-tile major, then d_model tiles.  Minor sub-blocks get tiles only for the
 // full rows, so FLOPs fall with the drop rate (no masks).
-__device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int* off2, UnitInfo* su = nullptr) {
+// su: room for the units' descriptors in shared memory (staged here), or
+// null; su_ready: the caller staged them already (before its griddepcontrol.wait)
+__device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int* off2, UnitInfo* su = nullptr,
+                          bool su_ready = false) {
   const int nu = a.num_routed + a.num_shared;
   const int tm = a.tile_m ? a.tile_m : kTileM;     // GEMM1 rows per tile: 128 (single CTA) or 256 (CTA pair)
   const int tm2 = a.tile_m2 ? a.tile_m2 : tm;      // GEMM2 rows per tile
@@ -86,39 +102,87 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     const int s = u - a.num_routed;
     return UnitSeg{a.shared_row0 + s * a.T, a.T, a.T, 0};
   };
-  // the units' descriptors staged in shared memory when the caller provides
-  // room: the tile builders below read them many times in dependent order
-  if (su) {
-    for (int u = threadIdx.x; u < nu; u += blockDim.x) su[u] = a.units[unit_of(u)];
-    __syncthreads();
-  }
   auto unit_info = [&](int u) -> const UnitInfo& { return su ? su[u] : a.units[unit_of(u)]; };
-  // tile counts per unit, then block-wide exclusive scans
-  for (int u = threadIdx.x; u < nu; u += blockDim.x) {
-    const UnitInfo& ui = unit_info(u);
-    const UnitSeg sg = seg_of(u);
+  // tiles of one unit in each work list
+  auto unit_tiles = [&](const UnitInfo& ui, const UnitSeg& sg, int& c1, int& c2) {
     const int mt_all = cdiv(sg.n_tot, tm), mt_full = cdiv(sg.n_full, tm);
-    int c1 = 0;
+    c1 = 0;
     for (int p = 0; p < ui.nsub; ++p) c1 += cdiv(ui.sub_wpad[p], kChunk) * (p == 0 ? mt_all : mt_full);
-    off1[u] = c1;
     // GEMM2 (unified, tm2 <= tm): tiles over all rows; a tile holding any
     // full row runs K = full width — its major-only rows read minor-sub-block H
     // that GEMM1's straddling minor tile wrote as zeros (rows in [live,
     // m_valid) of a GEMM1 tile store 0, and GEMM1 tiles of tm rows contain the
     // GEMM2 tile).  Otherwise the full rows and the major-only rows tile
     // separately (two tails per unit instead of one).
-    off2[u] = (unified ? cdiv(sg.n_tot, tm2) : cdiv(sg.n_full, tm2) + cdiv(sg.n_tot - sg.n_full, tm2)) * ntd;
+    c2 = (unified ? cdiv(sg.n_tot, tm2) : cdiv(sg.n_full, tm2) + cdiv(sg.n_tot - sg.n_full, tm2)) * ntd;
+  };
+  if (nu <= 64) {
+    // one warp: descriptors staged (when there is room), tile counts and both
+    // exclusive scans in registers — no block-wide scan barriers
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int c1[2] = {0, 0}, c2[2] = {0, 0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = lane + 32 * h;
+        if (u < nu) {
+          const UnitInfo ui = su_ready ? su[u] : a.units[unit_of(u)];
+          if (su && !su_ready) su[u] = ui;
+          unit_tiles(ui, seg_of(u), c1[h], c2[h]);
+        }
+      }
+      int i1[2] = {c1[0], c1[1]}, i2[2] = {c2[0], c2[1]};
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int y1 = __shfl_up_sync(0xffffffffu, i1[h], o), y2 = __shfl_up_sync(0xffffffffu, i2[h], o);
+          if (lane >= o) {
+            i1[h] += y1;
+            i2[h] += y2;
+          }
+        }
+      }
+      const int a1 = __shfl_sync(0xffffffffu, i1[0], 31), a2 = __shfl_sync(0xffffffffu, i2[0], 31);
+      const int b1 = __shfl_sync(0xffffffffu, i1[1], 31), b2 = __shfl_sync(0xffffffffu, i2[1], 31);
+      if (lane < nu) {
+        off1[lane] = i1[0] - c1[0];
+        off2[lane] = i2[0] - c2[0];
+      }
+      if (lane + 32 < nu) {
+        off1[lane + 32] = a1 + i1[1] - c1[1];
+        off2[lane + 32] = a2 + i2[1] - c2[1];
+      }
+      if (lane == 0) {
+        off1[nu] = a1 + b1;
+        off2[nu] = a2 + b2;
+        if (a.n1 && blockIdx.x == 0) *a.n1 = a1 + b1;
+        if (a.n2 && blockIdx.x == 0) *a.n2 = a2 + b2;
+      }
+    }
+    __syncthreads();
+  } else {
+    // the units' descriptors staged in shared memory when the caller provides
+    // room: the tile builders below read them many times in dependent order
+    if (su && !su_ready) {
+      for (int u = threadIdx.x; u < nu; u += blockDim.x) su[u] = a.units[unit_of(u)];
+      __syncthreads();
+    }
+    // tile counts per unit, then block-wide exclusive scans
+    for (int u = threadIdx.x; u < nu; u += blockDim.x) unit_tiles(unit_info(u), seg_of(u), off1[u], off2[u]);
+    __syncthreads();
+    const int tot1 = block_excl_scan(off1, nu);
+    const int tot2 = block_excl_scan(off2, nu);
+    if (threadIdx.x == 0) {
+      off1[nu] = tot1;
+      off2[nu] = tot2;
+      if (a.n1 && blockIdx.x == 0) *a.n1 = tot1;
+      if (a.n2 && blockIdx.x == 0) *a.n2 = tot2;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  const int tot1 = block_excl_scan(off1, nu);
-  const int tot2 = block_excl_scan(off2, nu);
-  if (threadIdx.x == 0) {
-    off1[nu] = tot1;
-    off2[nu] = tot2;
-    if (a.n1 && blockIdx.x == 0) *a.n1 = tot1;
-    if (a.n2 && blockIdx.x == 0) *a.n2 = tot2;
-  }
-  __syncthreads();
+  unsigned long long tq0 = 0, tq1 = 0, tq2 = 0;
+  if (DSB_PERMUTE_PHASES) tq0 = gtimer();
   auto find = [&](const int* off, int i) {  // largest u with off[u] <= i
     int lo = 0, hi = nu - 1;
     while (lo < hi) {
@@ -170,7 +234,11 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     tl.m_live = live | (sh ? kTileAltA : (a.gather ? kTileGatherA : 0));
     a.tiles1[i] = tl;
   }
-  for (int i = gtid; i < off2[nu]; i += gstride) {
+  if (DSB_PERMUTE_PHASES) tq1 = gtimer();
+  // GEMM2 tiles start on the other half of the block's warps: both lists are
+  // built concurrently (each list has ~1 tile per thread of a few warps)
+  const int gtid2 = ((threadIdx.x + (blockDim.x >> 1)) % blockDim.x) * gridDim.x + blockIdx.x;
+  for (int i = gtid2; i < off2[nu]; i += gstride) {
     const int u = find(off2, i);
     const UnitInfo& ui = unit_info(u);
     const UnitSeg sg = seg_of(u);
@@ -190,6 +258,12 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     tl.m_valid = m_valid;
     tl.m_live = m_valid;
     a.tiles2[i] = tl;
+  }
+  if (DSB_PERMUTE_PHASES && threadIdx.x == 0) {
+    tq2 = gtimer();
+    s_tq[0] = tq0;
+    s_tq[1] = tq1;
+    s_tq[2] = tq2;
   }
 }
 
@@ -375,16 +449,21 @@ struct PermuteArgs {
   int32_t* slot_pos;
   PlanArgs plan;
   int do_plan;
+  const int* sc;                          // superchunk histograms (gate_route), or null: phase A
+  int sc_chunks;
+  const unsigned long long* sc_epoch;
 };
 
-#ifndef DSB_PERMUTE_PHASES
-#define DSB_PERMUTE_PHASES 0  // 1: block 0 prints the phase durations (diagnostic builds only)
-#endif
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
+// dynamic shared memory of permute_fused_kernel, in ints: [2E bases | 4 x (2E
+// carry | 8 x 2E warp counts)], then the units' descriptors (plan), then the
+// superchunk prefixes (sc path, kScCap x kScCodes)
+constexpr int kScLd = kScCodes + 1;  // shared-memory row stride of the superchunk prefixes
+static_assert(kScCodes == 128, "superchunk rows are indexed with shifts");
+__host__ __device__ inline int permute_smem_ints(int E) { return (2 * E * (1 + 4 * (1 + 8)) + 3) & ~3; }
+__host__ __device__ inline int permute_units_ints(int nu) {
+  return ((nu * static_cast<int>(sizeof(UnitInfo)) + 15) & ~15) / 4;
 }
+
 
 __global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a) {
   unsigned long long tp[6];
@@ -506,30 +585,237 @@ __global__ void __launch_bounds__(1024) permute_fused_kernel(const PermuteArgs a
   // ---- phase B3: this CTA's share of the GEMM work lists
   if (a.do_plan) {
     // after the scatter's dynamic region: room for the units' descriptors
-    UnitInfo* su = reinterpret_cast<UnitInfo*>(dsm + ((2 * a.E * (1 + 4 * (1 + 8)) + 3) & ~3));
+    UnitInfo* su = reinterpret_cast<UnitInfo*>(dsm + permute_smem_ints(a.E));
     plan_body(a.plan, s_seg, off1, off2, su);
   }
   if (DSB_PERMUTE_PHASES) {
     tp[5] = gtimer();
-    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
-      printf("permute block %d: wait %llu  A %llu  sync %llu  B12 %llu  B3 %llu ns\n", blockIdx.x, tp[1] - tp[0],
-             tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4]);
+    if (phase_block())
+      printf("permute block %d: wait %llu  A %llu  sync/A' %llu  B12 %llu  B3 %llu (prologue %llu tiles1 %llu tiles2 %llu) ns\n",
+             blockIdx.x, tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4],
+             a.do_plan ? s_tq[0] - tp[4] : 0ull, a.do_plan ? s_tq[1] - s_tq[0] : 0ull, a.do_plan ? s_tq[2] - s_tq[1] : 0ull);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Superchunk permutation (after the fused gate + router, E <= 64): that kernel
+// added every 64-token tile's histogram into its superchunk (sc_chunks chunks)
+// of the buffer the device epoch selects.  Every CTA scans the <= kScCap
+// superchunks itself — exclusive prefix per code and per-code totals — so the
+// chunk scan and the grid-wide barrier of permute_fused_kernel disappear; a
+// chunk's offset is its superchunk prefix plus the chunk rows before it in
+// that superchunk.  Loads are issued early: the units' descriptors before
+// griddepcontrol.wait (layer constants), the epoch, the chunk rows and the
+// first scatter pass's selections together after it.  Results are identical
+// to permute_fused_kernel.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) permute_sc_kernel(const PermuteArgs a) {
+  unsigned long long tp[6];
+  if (DSB_PERMUTE_PHASES) tp[0] = gtimer();
+  extern __shared__ int dsm[];
+  __shared__ int off1[kPlanMaxUnits + 1], off2[kPlanMaxUnits + 1];
+  __shared__ UnitSeg s_seg[64];
+  __shared__ int s_ctot[kScCodes], s_rtot;
+  constexpr int kGroups = 4, kGW = 8;  // chunks in flight per CTA, warps per chunk
+  const int ncode = 2 * a.E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int nu_plan = a.do_plan ? a.plan.num_routed + a.plan.num_shared : 0;
+  UnitInfo* su = reinterpret_cast<UnitInfo*>(dsm + permute_smem_ints(a.E));
+  int* scp = dsm + permute_smem_ints(a.E) + permute_units_ints(nu_plan);  // 2 x kScLd superchunk prefixes
+  int* base = dsm;
+  int* carry = dsm + ncode;
+  // layer constants: staged while the router kernel still runs
+  if (a.do_plan)
+    for (int u = threadIdx.x; u < nu_plan; u += blockDim.x)
+      su[u] = a.plan.units[u < a.plan.num_routed ? (a.plan.seg_unit ? a.plan.seg_unit[u] : u)
+                                                  : a.plan.shared_unit0 + (u - a.plan.num_routed)];
+  const int grp = warp / kGW, gwarp = warp % kGW, gtid = threadIdx.x % (kGW * 32);
+  const long long slots_per_chunk = static_cast<long long>(kRouterChunk) * a.K;
+  const int passes = static_cast<int>((slots_per_chunk + kGW * 32 - 1) / (kGW * 32));
+  pdl_wait();
+  pdl_trigger();
+  if (DSB_PERMUTE_PHASES) tp[1] = gtimer();
+  // ---- loads that depend only on the router's outputs, all in flight at once
+  const unsigned long long ep = *reinterpret_cast<const volatile unsigned long long*>(a.sc_epoch);
+  const int chunk0 = blockIdx.x * kGroups + grp;     // this group's first chunk
+  const int cc = gtid & (kScCodes - 1), ch_half = gtid >> 7;
+  int pre = 0;  // rows of code cc in this superchunk's chunks before chunk0 (this thread's half)
+  if (chunk0 < a.nchunks && cc < ncode)
+    for (int ch = (chunk0 / a.sc_chunks) * a.sc_chunks + ch_half; ch < chunk0; ch += 16) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (ch + 2 * j < chunk0) pre += a.cnt_chunk[static_cast<long long>(ch + 2 * j) * ncode + cc];
+    }
+  const long long i_pre = static_cast<long long>(chunk0) * slots_per_chunk + gtid;  // first pass's selection
+  const long long s1_pre = min(static_cast<long long>(a.T) * a.K, static_cast<long long>(chunk0 + 1) * slots_per_chunk);
+  const bool pre_ok = chunk0 < a.nchunks && i_pre < s1_pre;
+  const int code_pre = pre_ok ? a.sel_code[i_pre] : -1;
+  const float raw_pre = pre_ok && code_pre >= 0 ? a.sel_raw[i_pre] : 0.f;
+  // ---- per-code totals over all superchunks and the prefix before this CTA's
+  // superchunk (threads 0..ncode-1, one code each, every load in flight);
+  // threads [512, 512 + ncode): the prefix before the superchunk of the CTA's
+  // last group when its chunks straddle a superchunk boundary
+  const int* buf = a.sc + static_cast<long long>((ep + 1ull) & 1ull) * kScCap * kScCodes;  // = (ep - 1) & 1
+  const int nsc = cdiv(a.nchunks, a.sc_chunks);
+  const int sc_first = min(blockIdx.x * kGroups, a.nchunks - 1) / a.sc_chunks;
+  const int sc_last = min(blockIdx.x * kGroups + kGroups - 1, a.nchunks - 1) / a.sc_chunks;
+  {
+    const int c = threadIdx.x & 511;
+    const int upto = threadIdx.x < 512 ? sc_first : sc_last;
+    if (c < ncode && (threadIdx.x < 512 || sc_last != sc_first)) {
+      int tot = 0, pfx = 0;
+      for (int s0 = 0; s0 < nsc; s0 += 16) {
+        int v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = s0 + j < nsc ? buf[(s0 + j) * kScCodes + c] : 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          tot += v[j];
+          if (s0 + j < upto) pfx += v[j];
+        }
+      }
+      if (threadIdx.x < 512) {
+        s_ctot[c] = tot;
+        scp[c] = pfx;
+      } else {
+        scp[kScLd + c] = pfx;
+      }
+    }
+  }
+  __syncthreads();
+  if (DSB_PERMUTE_PHASES) tp[2] = tp[3] = gtimer();
+  // ---- unit segments (one warp, 2 units per lane)
+  if (warp == 0) {
+    const int r0 = lane < a.E ? s_ctot[2 * lane] + s_ctot[2 * lane + 1] : 0;
+    const int r1 = lane + 32 < a.E ? s_ctot[2 * lane + 64] + s_ctot[2 * lane + 65] : 0;
+    int i0 = r0, i1 = r1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y0 = __shfl_up_sync(0xffffffffu, i0, o), y1 = __shfl_up_sync(0xffffffffu, i1, o);
+      if (lane >= o) {
+        i0 += y0;
+        i1 += y1;
+      }
+    }
+    const int t0 = __shfl_sync(0xffffffffu, i0, 31), t1 = __shfl_sync(0xffffffffu, i1, 31);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int u = lane + 32 * h;
+      if (u < a.E) {
+        const int start = h ? t0 + i1 - r1 : i0 - r0;
+        const int nf = s_ctot[2 * u], nm = s_ctot[2 * u + 1];
+        s_seg[u] = UnitSeg{start, nf, nf + nm, 0};
+        base[2 * u] = start;
+        base[2 * u + 1] = start + nf;
+        if (blockIdx.x == 0) {
+          a.seg[u] = s_seg[u];
+          a.code_base[2 * u] = start;
+          a.code_base[2 * u + 1] = start + nf;
+        }
+      }
+    }
+    if (lane == 0) {
+      s_rtot = t0 + t1;
+      if (blockIdx.x == 0) *a.r_total = t0 + t1;
+    }
+  }
+  if (blockIdx.x == 0)
+    for (int c = threadIdx.x; c < ncode; c += blockDim.x) a.code_tot[c] = s_ctot[c];
+  __syncthreads();
+  // ---- ordered scatter (permute_fused_kernel phase B2), chunk offsets from the prefixes
+  {
+    int* gcarry = carry + grp * (ncode + kGW * ncode);
+    int* gwcnt = gcarry + ncode;
+    bool first = true;
+    for (int c0 = blockIdx.x * kGroups; c0 < a.nchunks; c0 += gridDim.x * kGroups) {
+      const int chunk = c0 + grp;
+      const bool have = chunk < a.nchunks;
+      const int sc0 = have ? chunk / a.sc_chunks : 0;
+      int v = pre;
+      if (!first && have && cc < ncode) {  // later rounds (T > gridDim x kGroups chunks)
+        v = 0;
+        for (int ch = sc0 * a.sc_chunks + ch_half; ch < chunk; ch += 2)
+          v += a.cnt_chunk[static_cast<long long>(ch) * ncode + cc];
+        if (ch_half == 0)
+          for (int q = 0; q < sc0; ++q) v += buf[q * kScCodes + cc];
+      }
+      if (ch_half == 1 && cc < ncode) gwcnt[cc] = v;  // gwcnt is free until the first pass below
+      __syncthreads();
+      if (ch_half == 0 && cc < ncode)
+        gcarry[cc] = have ? (first ? scp[(sc0 == sc_first ? 0 : kScLd) + cc] : 0) + base[cc] + v + gwcnt[cc] : 0;
+      const long long s0 = static_cast<long long>(chunk) * slots_per_chunk;
+      const long long s1 = have ? min(static_cast<long long>(a.T) * a.K, s0 + slots_per_chunk) : s0;
+      for (int ps = 0; ps < passes; ++ps) {
+        const long long p0 = s0 + static_cast<long long>(ps) * kGW * 32;
+        __syncthreads();  // gcarry written / the previous pass's gwcnt readers done
+        for (int i = gtid; i < kGW * ncode; i += kGW * 32) gwcnt[i] = 0;
+        __syncthreads();
+        const long long i = p0 + gtid;
+        const bool use_pre = first && ps == 0;
+        const int code = use_pre ? code_pre : (i < s1 ? a.sel_code[i] : -1);
+        const int c = code < 0 ? -1 : (code >> 2) * 2 + ((code & 3) == 2 ? 0 : 1);
+        const unsigned mg = __match_any_sync(0xffffffffu, c);
+        const int rank_w = __popc(mg & ((1u << lane) - 1u));
+        if (c >= 0 && rank_w == 0) gwcnt[gwarp * ncode + c] = __popc(mg);
+        __syncthreads();
+        for (int q = gtid; q < ncode; q += kGW * 32) {
+          int run = gcarry[q];
+#pragma unroll
+          for (int w = 0; w < kGW; ++w) {
+            const int x = gwcnt[w * ncode + q];
+            gwcnt[w * ncode + q] = run;
+            run += x;
+          }
+          gcarry[q] = run;
+        }
+        __syncthreads();
+        if (i < s1) {
+          if (c >= 0) {
+            const int pos = gwcnt[gwarp * ncode + c] + rank_w;
+            a.row_token[pos] = static_cast<int32_t>(i / a.K);
+            a.row_scale[pos] = use_pre ? raw_pre : a.sel_raw[i];
+            a.slot_pos[i] = pos;
+          } else {
+            a.slot_pos[i] = -1;
+          }
+        }
+      }
+      first = false;
+      __syncthreads();
+    }
+  }
+  if (DSB_PERMUTE_PHASES) tp[4] = gtimer();
+  // ---- this CTA's share of the GEMM work lists (descriptors already staged)
+  if (a.do_plan) plan_body(a.plan, s_seg, off1, off2, su, true);
+  if (DSB_PERMUTE_PHASES) {
+    tp[5] = gtimer();
+    if (phase_block())
+      printf("permute_sc block %d: wait %llu  A' %llu  B12 %llu  B3 %llu (prologue %llu tiles1 %llu tiles2 %llu) ns\n",
+             blockIdx.x, tp[1] - tp[0], tp[2] - tp[1], tp[4] - tp[3], tp[5] - tp[4],
+             a.do_plan ? s_tq[0] - tp[4] : 0ull, a.do_plan ? s_tq[1] - s_tq[0] : 0ull,
+             a.do_plan ? s_tq[2] - s_tq[1] : 0ull);
   }
 }
 
 int launch_permute_fused(const int* cnt_chunk, int nchunks, int E, int* chunk_off, int* code_base, UnitSeg* seg,
                          int* r_total, int* code_tot, const int32_t* sel_code, const float* sel_raw, int T, int K,
                          int32_t* row_token, float* row_scale, int32_t* slot_pos, const PlanArgs* plan, int num_sms,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, const int* sc, const unsigned long long* sc_epoch) {
   if (E > 256) return -1;
+  if (sc && (E > 64 || !sc_epoch || (nchunks + gate_route_sc_chunks(T) - 1) / gate_route_sc_chunks(T) > kScCap))
+    return -1;
   PermuteArgs a{cnt_chunk, nchunks, E, chunk_off, code_tot, code_base, seg, r_total, sel_code, sel_raw, T, K,
-                row_token, row_scale, slot_pos, plan ? *plan : PlanArgs{}, plan != nullptr};
+                row_token, row_scale, slot_pos, plan ? *plan : PlanArgs{}, plan != nullptr,
+                sc, sc ? gate_route_sc_chunks(T) : 0, sc_epoch};
   const int threads = 1024;
-  const size_t smem = static_cast<size_t>((2 * E * (1 + 4 * (1 + 8)) + 3) & ~3) * sizeof(int) +
-                      (plan ? sizeof(UnitInfo) * static_cast<size_t>(plan->num_routed + plan->num_shared) : 0);
-  if (set_max_dyn_smem(permute_fused_kernel, smem) != cudaSuccess) return -2;
+  const size_t smem =
+      static_cast<size_t>(permute_smem_ints(E) + (plan ? permute_units_ints(plan->num_routed + plan->num_shared) : 0) +
+                          (sc ? 2 * kScLd : 0)) *
+      sizeof(int);
+  auto* kern = sc ? permute_sc_kernel : permute_fused_kernel;
+  if (set_max_dyn_smem(kern, smem) != cudaSuccess) return -2;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, permute_fused_kernel, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) return -3;
   const int grid = num_sms;  // one CTA per SM: every CTA is co-resident (cooperative launch checks it)
   cudaLaunchConfig_t cfg{};
@@ -539,12 +825,12 @@ int launch_permute_fused(const int* cnt_chunk, int nchunks, int E, int* chunk_of
   cfg.stream = stream;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
+  at[0].val.cooperative = sc ? 0 : 1;  // the superchunk path has no grid-wide barrier
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, permute_fused_kernel, a);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
   return e == cudaSuccess ? 0 : -2;
 }
 

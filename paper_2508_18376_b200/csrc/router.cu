@@ -567,7 +567,7 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
 //                read-back use), then the 8 warps route 8 tokens each, four
 //                lanes per token — quad_route, the arithmetic of
 //                router_quad_kernel — and publish the tile's two 32-token
-//                chunk histograms.
+//                chunk histograms (+ their sum into the tile's superchunk).
 // 64-token tiles put a CTA on every SM at T = 16384 (256 tiles) and let one
 // group route tile j while the producer / MMA already stream tile j + 1 into
 // the other accumulator: the routing of all but each CTA's last tile hides
@@ -599,7 +599,9 @@ struct GateRouteArgs {
   RouterArgs r;
   float* logits_out;         // T x Epad fp32 (row stride Epad), or null
   int epad, nkb, ntiles;
-  unsigned long long* acc;   // [n1, nh, err, done], all zero between launches
+  unsigned long long* acc;   // [n1, nh, err, done] (zero between launches), [4] superchunk epoch
+  int* sc;                   // 2 x kScCap x 128 superchunk histograms (buffer = epoch parity), or null
+  int sc_chunks;             // 32-token chunks per superchunk (even: a tile never straddles two)
 };
 
 __device__ __forceinline__ void group_bar_sync(int g) {
@@ -628,7 +630,7 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red + 3);
   const RouterArgs& a = g.r;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kLoaders = 2 * (EPAD / 32);  // warps per group draining TMEM lanes 0-63, 32 columns each
+  constexpr int kLoaders = 2 * (EPAD / 32);  // router warps draining TMEM lanes 0-63, 32 columns each
   const uint32_t tx_bytes = static_cast<uint32_t>(kGrRows * 128 + g.epad * 128);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -656,6 +658,17 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();     // x / the previous forward's readers of the routing buffers are done
   pdl_trigger();  // the permutation may launch (it waits for this grid to complete)
+  // superchunk epoch: constant for the whole launch (the last CTA advances it
+  // only after every CTA has arrived)
+  const unsigned long long epoch = g.sc ? *reinterpret_cast<volatile unsigned long long*>(&g.acc[4]) : 0ull;
+  if (g.sc) {
+    // clear the other superchunk buffer for the next launch, a slice per CTA:
+    // its readers (the previous forward's permutation) finished before this
+    // grid's griddepcontrol.wait returned
+    int4* o = reinterpret_cast<int4*>(g.sc + static_cast<long long>((epoch + 1ull) & 1ull) * kScCap * kScCodes);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kScCap * kScCodes / 4; i += gridDim.x * blockDim.x)
+      o[i] = make_int4(0, 0, 0, 0);
+  }
   if (warp == 0) {
     if (lane == 0) {
       int s = 0;
@@ -758,10 +771,23 @@ __global__ void __launch_bounds__(kGrThreads, 1)
 #endif
       }
       group_bar_sync(grp);  // the tile's histograms are complete (and the logits tile is free)
-      for (int i = gtid; i < kGrChunks * ncode; i += kGrGroupWarps * 32) {
-        const int c = i / ncode, chunk = tile * kGrChunks + c;
-        if (chunk < nchunks) a.cnt_chunk[static_cast<long long>(chunk) * ncode + (i - c * ncode)] = hist[i];
-        hist[i] = 0;  // the group's next tile counts after its first group_bar_sync
+      // per-chunk histograms, and their sum added into the tile's superchunk
+      // (the permutation scans superchunks instead of every chunk: no grid-wide
+      // barrier there)
+      int* scb = g.sc ? g.sc + (static_cast<long long>(epoch & 1ull) * kScCap +
+                                (tile * kGrChunks) / g.sc_chunks) * kScCodes
+                      : nullptr;
+      for (int code = gtid; code < ncode; code += kGrGroupWarps * 32) {
+        int sum = 0;
+#pragma unroll
+        for (int c = 0; c < kGrChunks; ++c) {
+          const int chunk = tile * kGrChunks + c;
+          const int v = hist[c * ncode + code];
+          if (chunk < nchunks) a.cnt_chunk[static_cast<long long>(chunk) * ncode + code] = v;
+          sum += v;
+          hist[c * ncode + code] = 0;  // the group's next tile counts after its first group_bar_sync
+        }
+        if (scb && sum) atomicAdd(scb + code, sum);
       }
     }
 #pragma unroll
@@ -795,18 +821,28 @@ __global__ void __launch_bounds__(kGrThreads, 1)
       a.counters[3] = 0ull;
       if (te) atomicOr(&a.counters[4], te);
       atomicExch(&g.acc[3], 0ull);
+      // every CTA has read the epoch and cleared its slice: advance it
+      if (g.sc) *reinterpret_cast<volatile unsigned long long*>(&g.acc[4]) = epoch + 1ull;
     }
   }
 }
 
 int gate_route_tile_rows() { return kGrRows; }
 
+int gate_route_sc_chunks(int T) {
+  const int nchunks = (T + kRouterChunk - 1) / kRouterChunk;
+  // at most kScCap superchunks; >= 16 chunks (512 tokens) each; even
+  const int per = (nchunks + kScCap - 1) / kScCap;
+  return per <= 16 ? 16 : per + (per & 1);
+}
+
 int launch_gate_route(const CUtensorMap* mapA, const CUtensorMap* mapB, const RouterArgs& r, int epad, int nkb,
-                      float* logits_out, unsigned long long* acc, int num_sms, cudaStream_t stream) {
+                      float* logits_out, unsigned long long* acc, int num_sms, cudaStream_t stream, int* sc) {
   if (r.E > 64 || r.K > 16 || r.K < 1 || r.K > r.E || r.nsplit > 1 || (epad != 32 && epad != 64)) return -1;
   const int ntiles = (r.T + kGrRows - 1) / kGrRows;
   if (ntiles <= 0) return 0;
-  GateRouteArgs g{r, logits_out, epad, nkb, ntiles, acc};
+  static_assert(kGrChunks == 2, "superchunks hold whole tiles");
+  GateRouteArgs g{r, logits_out, epad, nkb, ntiles, acc, sc, gate_route_sc_chunks(r.T)};
   const int grid = ntiles < num_sms ? ntiles : num_sms;
   cudaError_t err;
 #define DSB_GR(EP, EPT, KK)                                                                                  \

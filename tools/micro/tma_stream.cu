@@ -85,6 +85,19 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
   }
 }
 
+
+__global__ void __launch_bounds__(512) ldg_kernel(const uint4* __restrict__ x, long long n, unsigned* out) {
+  unsigned acc = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    uint4 a = __ldcs(x + i), b = __ldcs(x + i + stride), c = __ldcs(x + i + 2 * stride), d = __ldcs(x + i + 3 * stride);
+    acc ^= a.x ^ b.y ^ c.z ^ d.w;
+  }
+  for (; i < n; i += stride) { uint4 a = __ldcs(x + i); acc ^= a.x; }
+  if (acc == 0x12345678u) *out = acc;
+}
+
 int main(int argc, char** argv) {
   const long long T = argc > 1 ? atoll(argv[1]) : 16384, d = 2048;
   void* x;
@@ -159,6 +172,57 @@ int main(int argc, char** argv) {
         }
         printf("3d: rows %3d x %d k-blocks (%4d B/row) stages %2d grid %3d: %7.2f us  %6.0f GB/s  (%s)\n", rows, kbs,
                kbs * 128, ns, grid, best * 1e3, T * d * 2 / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+  }
+  {
+    unsigned* out; cudaMalloc(&out, 4);
+    for (int bps : {1, 2, 4}) for (int thr : {256, 512}) {
+      float best = 1e9;
+      for (int it = 0; it < 5; ++it) {
+        cudaMemset(flush, it, fl);
+        cudaEventRecord(e0);
+        ldg_kernel<<<sms * bps, thr>>>((const uint4*)x, T * d * 2 / 16, out);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+      }
+      printf("ldg: %d blocks/SM x %d threads: %7.2f us  %6.0f GB/s\n", bps, thr, best * 1e3, T * d * 2 / (best * 1e-3) / 1e9);
+    }
+    // empty-kernel event overhead
+    float best = 1e9;
+    for (int it = 0; it < 5; ++it) {
+      cudaEventRecord(e0);
+      ldg_kernel<<<sms, 256>>>((const uint4*)x, 0, out);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    printf("empty kernel: %7.2f us\n", best * 1e3);
+    // two CTAs per SM, TMA, 64-row boxes, 6 stages each
+    for (int rows : {64}) {
+      CUtensorMap m;
+      cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)T};
+      cuuint64_t strides[1] = {(cuuint64_t)(d * 2)};
+      cuuint32_t box[2] = {64, (cuuint32_t)rows};
+      cuuint32_t es[2] = {1, 1};
+      enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      for (int ns : {4, 6}) {
+        const size_t smem = ns * 16384 + 2 * ns * 8 + 1024;
+        float best2 = 1e9;
+        for (int it = 0; it < 5; ++it) {
+          cudaMemset(flush, it, fl);
+          cudaEventRecord(e0);
+          stream_kernel<<<2 * sms, 64, smem>>>(m, T / rows, d / 64, rows, ns);
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms; cudaEventElapsedTime(&ms, e0, e1);
+          if (ms < best2) best2 = ms;
+        }
+        printf("2 CTA/SM rows %d stages %d: %7.2f us  %6.0f GB/s (%s)\n", rows, ns, best2 * 1e3, T * d * 2 / (best2 * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
       }
     }
   }
