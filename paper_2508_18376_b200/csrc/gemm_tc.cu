@@ -118,7 +118,8 @@ struct GemmArgs {
   const int* row_token;    // gathered A tiles: token of each permuted row
   const void* gather_src;  // gathered A tiles: X (bf16, gather_ld bytes per row)
   long long gather_ld;
-  int flags;               // DSMOE_B200_GEMM_FLAGS: bit 0 B loads evict-first (fused gather), bit 1 no TMA stores
+  int flags;               // DSMOE_B200_GEMM_FLAGS: bit 0 B loads evict-first (fused gather), bit 1 no TMA stores,
+                           // bit 4 / 5: GEMM1 / GEMM2 output stores evict-first
   int tma_store;           // bf16 outputs leave through mapO
   unsigned long long* zero4;  // gate: the router's 4 counters, zeroed here (saves a memset between launches)
 };
@@ -171,13 +172,18 @@ __device__ __forceinline__ void warp_slot_acquire(int lane) {
 }
 
 // slot -> out rows [row0, row0 + min(32, nvalid)), columns [col0, col0 + kBoxCols)
+// st_pol != 0: the TMA store carries that L2 policy (DSMOE_B200_GEMM_FLAGS bits 4 / 5)
 __device__ __forceinline__ void warp_store(const uint8_t* slot, const CUtensorMap* mapO, const GemmArgs& args,
-                                           int row0, int col0, int nvalid, bool full, int lane) {
+                                           int row0, int col0, int nvalid, bool full, int lane,
+                                           uint64_t st_pol = 0) {
   if (full && args.tma_store) {
     fence_proxy_async();  // generic smem writes -> async-proxy (TMA) reads
     __syncwarp();
     if (lane == 0) {
-      tma_store_2d(mapO, smem_u32(slot), col0, row0);
+      if (st_pol)
+        tma_store_2d_hint(mapO, smem_u32(slot), col0, row0, st_pol);
+      else
+        tma_store_2d(mapO, smem_u32(slot), col0, row0);
       bulk_commit();
     }
   } else {
@@ -503,6 +509,9 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     // rows per CTA, quarters q and q + 2 hold the same rows (other N half)
     auto row_base = [&](const GemmTile& t) { return half_m(t) ? 32 * (q & 1) : 32 * q; };
     uint8_t* wslot = stage_buf + (warp - kEpiWarp0) * kWarpSlot;  // this warp's staging slot
+    uint64_t st_pol = 0;  // A/B: output stores evict-first (H / Y must not push x / weights out of L2)
+    if ((MODE == kEpiSwiGLU && (args.flags & 16)) || (MODE == kEpiScale && (args.flags & 32)))
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(st_pol));
     int acc = 0;
     uint32_t acc_phase = 0;
     // accumulator drained: MMA may reuse it (pair: one release-arrive per warp
@@ -593,7 +602,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
           }
           if (kStageOut && kBoxCols == 32) {
             warp_put(wslot, lane, 0, pk);
-            warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + ocol, tl.m_valid - rb, rows_full, lane);
+            warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + ocol, tl.m_valid - rb, rows_full, lane, st_pol);
           } else if (kStageOut)
             warp_put(wslot, lane, 32 * gi, pk);
           else if (valid)
@@ -601,7 +610,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
         }
         release_acc(acc);
         if (kStageOut && kBoxCols == 64 && c0 < nc)
-          warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + c0, tl.m_valid - rb, rows_full, lane);
+          warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + c0, tl.m_valid - rb, rows_full, lane, st_pol);
       } else if constexpr (MODE == kEpiScale) {
         // y = acc * raw score -> bf16, 64 output columns per x64 TMEM load.
         // M = 256 / single: columns 128 p + 64 half (p = 0, 1) at the same
@@ -628,14 +637,14 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
             warp_slot_acquire(lane);
             warp_put(wslot, lane, 0, pk);
             warp_put(wslot, lane, 32, pk + 16);
-            warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + c, tl.m_valid - rb, rows_full, lane);
+            warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + c, tl.m_valid - rb, rows_full, lane, st_pol);
           } else if (have && kStageOut) {
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               warp_slot_acquire(lane);
               warp_put(wslot, lane, 0, pk + 16 * hh);
               warp_store(wslot, &mapO, args, tl.out_row + rb, tl.out_col + c + 32 * hh, tl.m_valid - rb, rows_full,
-                         lane);
+                         lane, st_pol);
             }
           } else if (have && valid) {
             row_put(args, orow, tl.out_col + c, pk);

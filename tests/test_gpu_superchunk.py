@@ -27,10 +27,10 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-D_MODEL, E, K, P = 256, 64, 8, 2
+D_MODEL = 256
 
 
-def _setup():
+def _setup(E=64, K=8, P=2):
     import paper_2508_18376_b200 as pkg
     from test_gpu_parity import rand_layer
     L = rand_layer(D_MODEL, 64, E, K, seed=7, P=P)
@@ -51,7 +51,7 @@ SEQ = [(4133, "fwd"), (1, "fwd"), (777, "route"), (40000, "fwd"), (129, "exact")
 
 
 def _check_perm(pkg, ctx, layer, x, pol, mode):
-    T = x.shape[0]
+    T, E, K, P = x.shape[0], layer.E, layer.K, layer.P
     r = pkg.route_and_drop(ctx, layer, x, pol, logits_mode=mode)
     idx, _, _, frac = r.host()
     y = pkg.forward(ctx, layer, x, pol, logits_mode=mode)
@@ -63,10 +63,11 @@ def _check_perm(pkg, ctx, layer, x, pol, mode):
     return y
 
 
-def test_superchunk_permutation_sequence():
-    pkg, L, layer = _setup()
+@pytest.mark.parametrize("E,K,P", [(64, 8, 2), (24, 4, 2), (40, 16, 1)])
+def test_superchunk_permutation_sequence(E, K, P):
+    pkg, L, layer = _setup(E, K, P)
     ctx = pkg.Context()
-    pol = pkg.DropPolicy.two_t_from(0.08)
+    pol = pkg.DropPolicy.two_t_from(0.08) if P == 2 else pkg.DropPolicy.one_t(0.08)  # 2T needs P = 2
     for i, (T, what) in enumerate(SEQ):
         x = _x(T, 50 + i)
         if what == "route":
