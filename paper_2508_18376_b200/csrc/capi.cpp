@@ -576,6 +576,8 @@ struct dsmoe_b200_ctx {
   // the last routing that filled them, -1 when cnt_chunk came from elsewhere
   DevBuf sc_hist;
   int sc_T = -1;
+  // dynamic tile claims of the CTA-pair GEMMs: [GEMM1 claim, done, GEMM2 claim, done], zero between launches
+  DevBuf gsched;
   // EP with one row per (token, rank): last ep_pack's layout on this context
   DevBuf ep_pos_td, ep_send_token, ep_cnt, ep_tot, ep_owner, ep_base;
   int ep_N = 0, ep_T = -1;
@@ -669,6 +671,10 @@ struct dsmoe_b200_ctx {
                         // [8..11] the fused gate + router's accumulators (zero between launches)
       counters.ensure(16 * sizeof(unsigned long long));
       cuda_check(cudaMemsetAsync(counters.p, 0, counters.bytes, stream), "memset");
+    }
+    if (!gsched.p) {
+      gsched.ensure(4 * sizeof(int));
+      cuda_check(cudaMemsetAsync(gsched.p, 0, gsched.bytes, stream), "memset");
     }
     if (!sc_hist.p) {
       sc_hist.ensure(2ull * kScCap * kScCodes * sizeof(int));
@@ -1039,14 +1045,27 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
     // TMA-store targets: 32-row boxes (one per epilogue warp)
     const CUtensorMap my = make_map(y, y_rows, L->d, L->d, 32, gemm_tc_store_box_cols());
     const CUtensorMap mh32 = make_map(C->H.p, h_rows, L->hstride, L->hstride, 32, gemm_tc_store_box_cols());
+    // DSMOE_B200_SCHED=static: the CTA pairs walk their tiles in a fixed
+    // round-robin instead of claiming them (A/B)
+    static const bool dyn_env = [] {
+      const char* v = std::getenv("DSMOE_B200_SCHED");
+      return !(v && std::string(v) == "static");
+    }();
+    static const bool dyn2_env = [] {  // GEMM2 claims too (DSMOE_B200_SCHED=dyn2)
+      const char* v = std::getenv("DSMOE_B200_SCHED");
+      return v && std::string(v) == "dyn2";
+    }();
+    int* gs = dyn_env ? C->gsched.as<int>() : nullptr;
     C->mark(4);
     launch_check(launch_gemm_tc(1, &mxp, &mx, p1 ? &L->map_w13_h : &L->map_w13, C->tiles1.as<GemmTile>(), n1, mt1,
                                 C->H.p, L->hstride, nullptr, p1 ? 128 : 256, num_sms(), s, row_token,
-                                row_token ? x : nullptr, static_cast<long long>(L->d) * 2, &mh32, p1 ? 1 : 0),
+                                row_token ? x : nullptr, static_cast<long long>(L->d) * 2, &mh32, p1 ? 1 : 0,
+                                nullptr, gs),
                  "gemm1");
     C->mark(5);
     launch_check(launch_gemm_tc(2, &mh, &mh, p2 ? &L->map_w2t_h : &L->map_w2t, C->tiles2.as<GemmTile>(), n2, mt2, y,
-                                L->d, row_scale, p2 ? 128 : 256, num_sms(), s, nullptr, nullptr, 0, &my, p2 ? 1 : 0),
+                                L->d, row_scale, p2 ? 128 : 256, num_sms(), s, nullptr, nullptr, 0, &my, p2 ? 1 : 0,
+                                nullptr, (gs && dyn2_env) ? gs + 2 : nullptr),
                  "gemm2");
   } else {
     SimtArgs g1{};

@@ -250,6 +250,15 @@ __device__ __forceinline__ void pair_arrive_leader_cta(uint64_t* bar) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// CTA pair: store one int into the peer CTA's shared memory at the same offset
+// (rank 1 - own), then arrive on the peer's barrier with cluster-scope release
+__device__ __forceinline__ void pair_store_arrive_peer(int* slot, int v, uint64_t* bar, uint32_t peer) {
+  uint32_t rs, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rs) : "r"(smem_u32(slot)), "r"(peer));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(peer));
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(rs), "r"(v) : "memory");
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+}
 // wait with cluster-scope acquire (writes released by the peer CTA become visible)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);

@@ -89,6 +89,15 @@ enum { kEpiF32 = 0, kEpiSwiGLU = 1, kEpiScale = 2, kEpiF32Wide = 3 };
 // the fused gather runs (GEMM1).  Gate logits (N = Epad <= 64): 8 KB B slots,
 // so both rings can be 8 deep — the gate GEMM is a 64 MB stream of x with
 // little math, and in-flight bytes are what bound it.
+// dynamic tile claims: id ring slots.  No reader ever lags the leader's
+// producer by more than a few tiles (the B ring bounds the producer's lead
+// over the MMA, the two accumulators the MMA's over the epilogue, and every
+// peer walker is paced by the leader's barriers), so a slot is never
+// rewritten before all walkers read it and no "slot free" barrier is needed —
+// per-tile remote release-arrives from 15 peer warps cost 5-10% of the GEMMs.
+constexpr int kSeq = 32;
+constexpr int kLook = 3;  // ids claimed ahead of the tile the leader's producer loads (gather warps read 2 ahead)
+
 template <int MODE, bool PAIR = false>
 struct Geo {
   static constexpr bool kGate = MODE == kEpiF32;
@@ -104,8 +113,9 @@ struct Geo {
   static constexpr int THREADS = (EPI0 + 8) * 32;
   static constexpr int RING = NA * kABytes + NB * BSLOT;
   static constexpr int STAGE = (MODE == kEpiF32 || MODE == kEpiF32Wide) ? 0 : kStageSmem;
-  static constexpr int SMEM = RING + STAGE + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int SMEM = RING + STAGE + 1024 /*align*/ + 1024 /*barriers, tile-id ring*/;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert((2 * NA + 2 * NB + 4 + kSeq) * 8 + kSeq * 4 + 4 <= 1024, "barrier area");
 };
 
 struct GemmArgs {
@@ -122,6 +132,8 @@ struct GemmArgs {
                            // bit 4 / 5: GEMM1 / GEMM2 output stores evict-first
   int tma_store;           // bf16 outputs leave through mapO
   unsigned long long* zero4;  // gate: the router's 4 counters, zeroed here (saves a memset between launches)
+  int* sched;              // CTA pairs: [claim counter, done counter], zero between launches ->
+                           // tiles are claimed dynamically (atomic counter) instead of t0 + k gs
 };
 
 // swish(g) = g * sigmoid(g) = 0.5 g (1 + tanh(g / 2)): one MUFU op (tanh.approx,
@@ -234,7 +246,9 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   uint64_t* emptyB = fullB + kBStages;
   uint64_t* tfull = emptyB + kBStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;  // dynamic tile claims: id ring slot written (both CTAs)
+  int* sring = reinterpret_cast<int*>(sfull + kSeq);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sring + kSeq);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -254,6 +268,15 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   auto row_off_of = [&](const GemmTile& t) { return half_m(t) ? 64 * rank : 128 * rank; };
 
   const bool fused = MODE == kEpiSwiGLU && kGatherWarps > 0 && args.gather_src != nullptr;
+  // Tile schedule.  Static: this CTA (pair) walks tiles t0, t0 + gs, ...
+  // Dynamic (CTA pairs with args.sched): the leader's producer thread claims
+  // tile ids from a global counter, kLook positions ahead of the tile it loads,
+  // and publishes them in a kSeq-slot ring in both CTAs' shared memory; every
+  // walker (producers, gather warps, MMA warp, epilogue warps) reads the ids in
+  // order and releases each slot on the leader's barrier.  A pair that runs
+  // slow (its SM clock, its memory latency, its tiles' costs) claims fewer
+  // tiles, so all pairs finish together.
+  const bool dyn = PAIR && args.sched != nullptr;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kAStages; ++s) {
       // TMA-fed stages: one arrive.expect_tx (pair: the leader's, for both CTAs'
@@ -270,6 +293,8 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], PAIR ? 16 : kEpiThreads);  // pair: one arrive per epilogue warp of both CTAs
     }
+    if (dyn)
+      for (int s = 0; s < kSeq; ++s) mbar_init(&sfull[s], 1);
     fence_mbar_init();
     tma_prefetch(&mapA);
     tma_prefetch(&mapA2);
@@ -324,6 +349,29 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     }
   };
 
+  // the next tile id of this pair's sequence (reader state rd / rend), -1 at
+  // the end; warp_wide: the whole warp calls it (lane 0 releases the slot)
+  auto next_id = [&](int& rd, bool& rend, bool warp_wide) -> int {
+    if (rend) return -1;
+    int v;
+    if (!dyn) {
+      v = t0 + rd * gs;
+      if (v >= ntiles) v = -1;
+    } else {
+      const int s = rd % kSeq;
+      const uint32_t ph = static_cast<uint32_t>(rd / kSeq) & 1u;
+      if (leader)
+        mbar_wait(&sfull[s], ph);
+      else
+        mbar_wait_cluster(&sfull[s], ph);
+      v = *reinterpret_cast<volatile int*>(&sring[s]);
+      (void)warp_wide;
+    }
+    ++rd;
+    if (v < 0) rend = true;
+    return v;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer: B always; A too unless the gather warps own it
@@ -331,10 +379,62 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       uint32_t pa = 0, pb = 0;
       uint64_t pol_b;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_b));
-      GemmTile nxt = t0 < ntiles ? args.tiles[t0] : GemmTile{};
-      for (int t = t0; t < ntiles; t += gs) {
+      // the leader's claims: sequence positions [0, claimed) are published.
+      // The atomic of the next claim is issued one tile before its value is
+      // published, so its latency never stalls the loads.
+      int claimed = 0, pend = 0;
+      bool ended = false, have_pend = false;
+      auto publish = [&](int t) {
+        const int s = claimed % kSeq;
+        if (t >= ntiles) {
+          t = -1;
+          ended = true;
+          // every pair publishes exactly one claim past the end: the last one re-arms the counters
+          if (atomicAdd(args.sched + 1, 1) == gs - 1) {
+            atomicExch(args.sched, 0);
+            atomicExch(args.sched + 1, 0);
+          }
+        }
+        sring[s] = t;
+        mbar_arrive(&sfull[s]);
+        pair_store_arrive_peer(&sring[s], t, &sfull[s], 1);
+        ++claimed;
+      };
+#ifdef DSB_SCHED_RING_STATIC  // diagnostic: the ring protocol with the static order (t0 + k gs)
+      int kstat = 0;
+      auto claim1 = [&]() { return t0 + (kstat++) * gs; };
+#else
+      auto claim1 = [&]() { return atomicAdd(args.sched, 1); };
+#endif
+      if (dyn && leader) {
+#ifdef DSB_SCHED_RING_STATIC
+        for (int k = 0; k <= kLook && !ended; ++k) publish(claim1());
+#else
+        const int base = atomicAdd(args.sched, kLook + 1);  // the first kLook + 1 positions: one atomic
+        for (int k = 0; k <= kLook && !ended; ++k) publish(base + k);
+#endif
+        if (!ended) {
+          pend = claim1();
+          have_pend = true;
+        }
+      }
+      int rd = 0, j = 0;
+      bool rend = false;
+      int id = next_id(rd, rend, false);
+      GemmTile nxt = id >= 0 ? args.tiles[id] : GemmTile{};
+      while (id >= 0) {
         const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
-        if (t + gs < ntiles) nxt = args.tiles[t + gs];
+        if (have_pend && claimed <= j + 1 + kLook) {  // keep kLook ids published past this tile
+          have_pend = false;
+          publish(pend);
+          if (!ended) {
+            pend = claim1();
+            have_pend = true;
+          }
+        }
+        id = next_id(rd, rend, false);
+        if (id >= 0) nxt = args.tiles[id];
+        ++j;
         const bool alt = (tl.m_live & kTileAltA) != 0;
         const void* ma = alt ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
         const int brow = tl.b_row + (PAIR ? rank * (tl.n_mma >> 1) : 0);
@@ -385,14 +485,21 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
           tok[j] = rt[i < tl.m_valid ? i : 0];
         }
       };
-      GemmTile cur = t0 < ntiles ? args.tiles[t0] : GemmTile{};
-      GemmTile nxt = t0 + gs < ntiles ? args.tiles[t0 + gs] : GemmTile{};
+      int rd = 0;
+      bool rend = false;
+      int id_cur = next_id(rd, rend, true);
+      int id_nxt = next_id(rd, rend, true);
+      GemmTile cur = id_cur >= 0 ? args.tiles[id_cur] : GemmTile{};
+      GemmTile nxt = id_nxt >= 0 ? args.tiles[id_nxt] : GemmTile{};
       int tok[4] = {0, 0, 0, 0};
-      if (t0 < ntiles) load_tok(cur, tok);
-      for (int t = t0; t < ntiles; t += gs) {
+      if (id_cur >= 0) load_tok(cur, tok);
+      while (id_cur >= 0) {
         int tok_n[4] = {0, 0, 0, 0};
-        if (t + gs < ntiles) load_tok(nxt, tok_n);
-        const GemmTile nxt2 = t + 2 * gs < ntiles ? args.tiles[t + 2 * gs] : GemmTile{};
+        if (id_nxt >= 0) load_tok(nxt, tok_n);
+        const int id_nxt2 = next_id(rd, rend, true);
+        const GemmTile nxt2 = id_nxt2 >= 0 ? args.tiles[id_nxt2] : GemmTile{};
+        id_cur = id_nxt;
+        id_nxt = id_nxt2;
         const GemmTile& tl = cur;
         const bool gather = (tl.m_live & kTileGatherA) != 0;
         const void* ma = (tl.m_live & kTileAltA) ? static_cast<const void*>(&mapA2) : static_cast<const void*>(&mapA);
@@ -451,10 +558,14 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     uint32_t acc_phase = 0;
     const uint64_t da0 = sdesc_sw128(smem_u32(ringA));  // + (bytes >> 4) moves the start address
     const uint64_t db0 = sdesc_sw128(smem_u32(ringB));
-    GemmTile nxt = t0 < ntiles ? args.tiles[t0] : GemmTile{};
-    for (int t = t0; t < ntiles && leader; t += gs) {
+    int rd = 0;
+    bool rend = !leader;  // the peer's MMA warp does not walk the tiles
+    int id = next_id(rd, rend, true);
+    GemmTile nxt = id >= 0 ? args.tiles[id] : GemmTile{};
+    while (id >= 0) {
       const GemmTile tl = nxt;  // descriptor prefetched one tile ahead
-      if (t + gs < ntiles) nxt = args.tiles[t + gs];
+      id = next_id(rd, rend, true);
+      if (id >= 0) nxt = args.tiles[id];
       const uint32_t idesc = idesc_bf16(PAIR ? (half_m(tl) ? kTileM : 2 * kTileM) : kTileM, tl.n_mma);
       const uint32_t dtmem = tmem_base + acc * kAccCols;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -530,18 +641,22 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
         mbar_arrive(&tempty[a]);
       }
     };
-    GemmTile nxt = t0 < ntiles ? args.tiles[t0] : GemmTile{};
+    int rd = 0;
+    bool rend = false;
+    int id = next_id(rd, rend, true);
+    GemmTile nxt = id >= 0 ? args.tiles[id] : GemmTile{};
     float sc_nxt = 0.f;  // kEpiScale: this thread's row score, loaded a tile ahead
     auto load_score = [&](const GemmTile& t) {
       const int rr = row_off_of(t) + row_base(t) + lane;
       return rr < t.m_valid ? args.row_scale[t.out_row + rr] : 0.f;
     };
-    if (MODE == kEpiScale && t0 < ntiles) sc_nxt = load_score(nxt);
-    for (int t = t0; t < ntiles; t += gs) {
+    if (MODE == kEpiScale && id >= 0) sc_nxt = load_score(nxt);
+    while (id >= 0) {
       GemmTile tl = nxt;  // descriptor prefetched one tile ahead
       const float sc_cur = sc_nxt;
-      if (t + gs < ntiles) {
-        nxt = args.tiles[t + gs];
+      id = next_id(rd, rend, true);
+      if (id >= 0) {
+        nxt = args.tiles[id];
         if (MODE == kEpiScale) sc_nxt = load_score(nxt);
       }
       const bool hm = half_m(tl);
@@ -687,14 +802,14 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
                    int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token,
                    const void* gather_src, long long gather_ld, const CUtensorMap* mapO, int pair,
-                   unsigned long long* zero4) {
+                   unsigned long long* zero4, int* sched) {
   static const int flags = [] {
     const char* v = std::getenv("DSMOE_B200_GEMM_FLAGS");
     return v ? std::atoi(v) : 0;
   }();
   GemmArgs a{tiles, num_tiles, out, ldo, row_scale, static_cast<uint32_t>(b_box_rows * 128), row_token,
              gather_src, gather_ld, flags, mapO != nullptr && mode != kEpiF32 && mode != kEpiF32Wide && !(flags & 2) ? 1 : 0,
-             zero4};
+             zero4, pair ? sched : nullptr};
   // gate logits with more than 64 output columns need the wide B slots
   if (mode == kEpiF32 && b_box_rows > 64) mode = kEpiF32Wide;
   const CUtensorMap* mo = mapO ? mapO : mapB;

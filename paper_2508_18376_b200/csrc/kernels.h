@@ -105,7 +105,8 @@ int launch_gemm_tc(int mode, const CUtensorMap* mapA, const CUtensorMap* mapA2,
                    int max_tiles, void* out, long long ldo, const float* row_scale,
                    int b_box_rows, int num_sms, cudaStream_t stream, const int* row_token = nullptr,
                    const void* gather_src = nullptr, long long gather_ld = 0,
-                   const CUtensorMap* mapO = nullptr, int pair = 0, unsigned long long* zero4 = nullptr);
+                   const CUtensorMap* mapO = nullptr, int pair = 0, unsigned long long* zero4 = nullptr,
+                   int* sched = nullptr);  // CTA pairs: 2 zeroed ints -> tiles claimed dynamically
 
 int gemm_tc_store_box_cols();  // TMA-store box width the gemm_tc build expects (64: SW128, 32: SW64)
 
