@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(1024) permute_sc_kernel(const PermuteArgs a) {
   extern __shared__ int dsm[];
   __shared__ int off1[kPlanMaxUnits + 1], off2[kPlanMaxUnits + 1];
   __shared__ UnitSeg s_seg[64];
-  __shared__ int s_ctot[kScCodes], s_rtot;
+  __shared__ int s_ctot[kScCodes];
   constexpr int kGroups = 4, kGW = 8;  // chunks in flight per CTA, warps per chunk
   const int ncode = 2 * a.E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -714,10 +714,7 @@ __global__ void __launch_bounds__(1024) permute_sc_kernel(const PermuteArgs a) {
         }
       }
     }
-    if (lane == 0) {
-      s_rtot = t0 + t1;
-      if (blockIdx.x == 0) *a.r_total = t0 + t1;
-    }
+    if (lane == 0 && blockIdx.x == 0) *a.r_total = t0 + t1;
   }
   if (blockIdx.x == 0)
     for (int c = threadIdx.x; c < ncode; c += blockDim.x) a.code_tot[c] = s_ctot[c];
