@@ -24,6 +24,8 @@
 // operation rounds exactly where the reference's (-ffp-contract=off) does.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+
 #include "kernels.h"
 
 namespace dsb {
@@ -577,6 +579,14 @@ int launch_router(const RouterArgs& a, cudaStream_t stream) {
 // counts them) moves them into counters[0..3] and re-zeroes acc: no memset and
 // no zeroing race with the atomics of other CTAs.
 // ---------------------------------------------------------------------------
+#ifndef DSB_GR_TIMES
+#define DSB_GR_TIMES 0  // diagnostic builds: CTAs 0, 100, last print their tile timeline (globaltimer, ns)
+#endif
+__device__ __forceinline__ unsigned long long gr_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int kGrStages = 7;
 constexpr int kGrRows = 64;                 // tokens per tile
 constexpr int kGrGroupWarps = 8;            // router warps per group (64 tokens x 4 lanes)
@@ -656,8 +666,10 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  __shared__ unsigned long long s_gt[8];  // diagnostic timeline: start, [acc ready, routed] x 2 tiles, end
   pdl_wait();     // x / the previous forward's readers of the routing buffers are done
   pdl_trigger();  // the permutation may launch (it waits for this grid to complete)
+  if (DSB_GR_TIMES && threadIdx.x == 0) s_gt[0] = gr_now();
   // superchunk epoch: constant for the whole launch (the last CTA advances it
   // only after every CTA has arrived)
   const unsigned long long epoch = g.sc ? *reinterpret_cast<volatile unsigned long long*>(&g.acc[4]) : 0ull;
@@ -753,6 +765,8 @@ __global__ void __launch_bounds__(kGrThreads, 1)
       }
       acc_phase ^= 1;
       group_bar_sync(grp);  // the tile's logits are in shared memory
+      const int lt = (tile - blockIdx.x) / gridDim.x;  // this CTA's tile index (diagnostics)
+      if (DSB_GR_TIMES && gtid == 0 && lt < 3) s_gt[1 + 2 * lt] = gr_now();
       {
         const int tk = gw * 8 + (lane >> 2);
         const int t = tile * kGrRows + tk;
@@ -771,6 +785,7 @@ __global__ void __launch_bounds__(kGrThreads, 1)
 #endif
       }
       group_bar_sync(grp);  // the tile's histograms are complete (and the logits tile is free)
+      if (DSB_GR_TIMES && gtid == 0 && lt < 3) s_gt[2 + 2 * lt] = gr_now();
       // per-chunk histograms, and their sum added into the tile's superchunk
       // (the permutation scans superchunks instead of every chunk: no grid-wide
       // barrier there)
@@ -804,6 +819,11 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (DSB_GR_TIMES && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 100 || blockIdx.x == gridDim.x - 1)) {
+    const unsigned long long t0 = s_gt[0], te = gr_now();
+    printf("gate_route cta %d: tile0 acc %llu routed %llu | tile1 acc %llu routed %llu | end %llu ns\n", blockIdx.x,
+           s_gt[1] - t0, s_gt[2] - t0, s_gt[3] > t0 ? s_gt[3] - t0 : 0ull, s_gt[4] > t0 ? s_gt[4] - t0 : 0ull, te - t0);
+  }
   if (warp == 1) tmem_dealloc(tmem_base, 2 * EPAD);
   if (threadIdx.x == 0) {
     if (red[0]) atomicAdd(&g.acc[0], red[0]);
