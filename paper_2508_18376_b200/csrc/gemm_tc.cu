@@ -38,6 +38,7 @@
 //               bf16 store into H (K3);
 //   kEpiScale   y = acc * row_scale[row] (the raw gate score, moe.hpp:235-237),
 //               bf16 store into Y (K4).
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -96,6 +97,16 @@ enum { kEpiF32 = 0, kEpiSwiGLU = 1, kEpiScale = 2, kEpiF32Wide = 3 };
 // rewritten before all walkers read it and no "slot free" barrier is needed —
 // per-tile remote release-arrives from 15 peer warps cost 5-10% of the GEMMs.
 constexpr int kSeq = 32;
+
+#ifndef DSB_GEMM_TIMES
+#define DSB_GEMM_TIMES 0  // diagnostic builds: per-launch min / max of CTA entry, post-wait and exit times
+#endif
+__device__ unsigned long long g_gemm_times[4][8];  // [mode][entry min, max, wait min, max, end min, max, count, -]
+__device__ __forceinline__ unsigned long long gemm_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int kLook = 3;  // ids claimed ahead of the tile the leader's producer loads (gather warps read 2 ahead)
 
 template <int MODE, bool PAIR = false>
@@ -236,6 +247,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   constexpr int kStageOutBytes = G::STAGE;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
+  const unsigned long long t_entry = DSB_GEMM_TIMES ? gemm_now() : 0ull;
   uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   uint8_t* ringA = smem;                              // kAStages x 16 KB
   uint8_t* ringB = smem + kAStages * kABytes;         // kBStages x kBSlot
@@ -319,6 +331,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // the predecessor's outputs (tile lists, A rows) are complete from here on
+  const unsigned long long t_wait = DSB_GEMM_TIMES ? gemm_now() : 0ull;
   if (MODE == kEpiF32 || MODE == kEpiF32Wide) pdl_trigger();  // gate: the router may launch
   if (MODE == kEpiScale) pdl_trigger_tail();
 #ifdef DSB_PDL_TRIGGER_G1  // experiment: GEMM1 -> GEMM2 (GEMM2 CTAs take SMs as GEMM1 CTAs exit)
@@ -786,6 +799,25 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     }
   }
   if (warp >= kEpiWarp0 && lane == 0) bulk_wait0();  // this lane's TMA stores still read its staging slot
+  if (DSB_GEMM_TIMES && PAIR && threadIdx.x == 0 && MODE >= 1 && MODE <= 2) {
+    unsigned long long* g = g_gemm_times[MODE];
+    const unsigned long long t_end = gemm_now();
+    atomicMin(&g[0], t_entry); atomicMax(&g[1], t_entry);
+    atomicMin(&g[2], t_wait); atomicMax(&g[3], t_wait);
+    atomicMin(&g[4], t_end); atomicMax(&g[5], t_end);
+    __threadfence();
+    if (atomicAdd(&g[6], 1ull) == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long e0 = atomicAdd(&g[0], 0ull);
+      if (e0 != 0ull)
+        printf("gemm%d: entry spread %llu, wait at +%llu..+%llu, end at +%llu..+%llu ns (from first entry)\n", MODE,
+               atomicAdd(&g[1], 0ull) - e0, atomicAdd(&g[2], 0ull) - e0, atomicAdd(&g[3], 0ull) - e0,
+               atomicAdd(&g[4], 0ull) - e0, atomicAdd(&g[5], 0ull) - e0);
+      g[0] = g[2] = g[4] = ~0ull;
+      g[1] = g[3] = g[5] = 0ull;
+      g[6] = 0ull;
+    }
+  }
   tc_fence_before();
   if constexpr (PAIR) {
     pair_sync();  // the leader's MMAs read the peer's smem until its last commit
