@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   // order and releases each slot on the leader's barrier.  A pair that runs
   // slow (its SM clock, its memory latency, its tiles' costs) claims fewer
   // tiles, so all pairs finish together.
-  const bool dyn = PAIR && args.sched != nullptr;
+  const bool dyn_ok = PAIR && args.sched != nullptr;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kAStages; ++s) {
       // TMA-fed stages: one arrive.expect_tx (pair: the leader's, for both CTAs'
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], PAIR ? 16 : kEpiThreads);  // pair: one arrive per epilogue warp of both CTAs
     }
-    if (dyn)
+    if (dyn_ok)
       for (int s = 0; s < kSeq; ++s) mbar_init(&sfull[s], 1);
     fence_mbar_init();
     tma_prefetch(&mapA);
@@ -338,6 +338,10 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
   if (MODE == kEpiSwiGLU) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
   const int ntiles = *args.num_tiles;
+  // claims pay off only with many tiles per pair (tail balance); with a few
+  // (small batches) claiming ahead would pile several tiles on some pairs
+  // while others idle — there the round-robin order is already balanced
+  const bool dyn = dyn_ok && ntiles >= 16 * gs;
   if ((MODE == kEpiF32 || MODE == kEpiF32Wide) && args.zero4 && blockIdx.x == 0 && threadIdx.x < 4) args.zero4[threadIdx.x] = 0ull;
   // "operand ready": own barrier (single CTA) / the leader's (pair)
   auto ready_arrive = [&](uint64_t* bar) {
