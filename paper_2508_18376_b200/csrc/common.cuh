@@ -259,6 +259,18 @@ __device__ __forceinline__ void pair_store_arrive_peer(int* slot, int v, uint64_
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(rs), "r"(v) : "memory");
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
 }
+// CTA pair: one int into the peer CTA's shared memory with st.async, counted
+// as 4 transaction bytes on the peer's barrier (arrive.expect_tx issued
+// first): the peer waits on its own barrier with a CTA-scope acquire, as for
+// TMA data — no cluster-scope acquire on the consumer side
+__device__ __forceinline__ void pair_store_async_peer(int* slot, int v, uint64_t* bar, uint32_t peer) {
+  uint32_t rs, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rs) : "r"(smem_u32(slot)), "r"(peer));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(bar)), "r"(peer));
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], 4;" ::"r"(rb) : "memory");
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(rs), "r"(v), "r"(rb)
+               : "memory");
+}
 // wait with cluster-scope acquire (writes released by the peer CTA become visible)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);

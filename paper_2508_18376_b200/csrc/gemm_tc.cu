@@ -377,10 +377,14 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
     } else {
       const int s = rd % kSeq;
       const uint32_t ph = static_cast<uint32_t>(rd / kSeq) & 1u;
+#ifdef DSB_SCHED_CLUSTER_ACQ  // A/B: plain remote store + cluster-scope acquire on the peer
       if (leader)
         mbar_wait(&sfull[s], ph);
       else
         mbar_wait_cluster(&sfull[s], ph);
+#else  // the peer's slot arrives by st.async, tracked on its own barrier
+      mbar_wait(&sfull[s], ph);
+#endif
       v = *reinterpret_cast<volatile int*>(&sring[s]);
       (void)warp_wide;
     }
@@ -414,7 +418,11 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
         }
         sring[s] = t;
         mbar_arrive(&sfull[s]);
+#ifdef DSB_SCHED_CLUSTER_ACQ
         pair_store_arrive_peer(&sring[s], t, &sfull[s], 1);
+#else
+        pair_store_async_peer(&sring[s], t, &sfull[s], 1);
+#endif
         ++claimed;
       };
 #ifdef DSB_SCHED_RING_STATIC  // diagnostic: the ring protocol with the static order (t0 + k gs)
