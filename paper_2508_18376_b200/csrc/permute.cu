@@ -89,8 +89,14 @@ constexpr int kPlanMaxUnits = 2048;
 // full rows, so FLOPs fall with the drop rate (no masks).
 // su: room for the units' descriptors in shared memory (staged here), or
 // null; su_ready: the caller staged them already (before its griddepcontrol.wait)
+// pcta / npcta: this block's index among the npcta blocks that build the
+// lists (default: every block of the grid)
 __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int* off2, UnitInfo* su = nullptr,
-                          bool su_ready = false) {
+                          bool su_ready = false, int pcta = -1, int npcta = 0) {
+  if (npcta <= 0) {
+    pcta = blockIdx.x;
+    npcta = gridDim.x;
+  }
   const int nu = a.num_routed + a.num_shared;
   const int tm = a.tile_m ? a.tile_m : kTileM;     // GEMM1 rows per tile: 128 (single CTA) or 256 (CTA pair)
   const int tm2 = a.tile_m2 ? a.tile_m2 : tm;      // GEMM2 rows per tile
@@ -156,8 +162,8 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
       if (lane == 0) {
         off1[nu] = a1 + b1;
         off2[nu] = a2 + b2;
-        if (a.n1 && blockIdx.x == 0) *a.n1 = a1 + b1;
-        if (a.n2 && blockIdx.x == 0) *a.n2 = a2 + b2;
+        if (a.n1 && pcta == 0) *a.n1 = a1 + b1;
+        if (a.n2 && pcta == 0) *a.n2 = a2 + b2;
       }
     }
     __syncthreads();
@@ -176,8 +182,8 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
     if (threadIdx.x == 0) {
       off1[nu] = tot1;
       off2[nu] = tot2;
-      if (a.n1 && blockIdx.x == 0) *a.n1 = tot1;
-      if (a.n2 && blockIdx.x == 0) *a.n2 = tot2;
+      if (a.n1 && pcta == 0) *a.n1 = tot1;
+      if (a.n2 && pcta == 0) *a.n2 = tot2;
     }
     __syncthreads();
   }
@@ -193,7 +199,7 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
   };
   // tiles interleaved over the blocks (tile i -> block i % grid) so every
   // block builds a few instead of the first ones building them all
-  const int gtid = threadIdx.x * gridDim.x + blockIdx.x, gstride = gridDim.x * blockDim.x;
+  const int gtid = threadIdx.x * npcta + pcta, gstride = npcta * blockDim.x;
   for (int i = gtid; i < off1[nu]; i += gstride) {
     const int u = find(off1, i);
     const UnitInfo& ui = unit_info(u);
@@ -237,7 +243,7 @@ __device__ void plan_body(const PlanArgs& a, const UnitSeg* seg, int* off1, int*
   if (DSB_PERMUTE_PHASES) tq1 = gtimer();
   // GEMM2 tiles start on the other half of the block's warps: both lists are
   // built concurrently (each list has ~1 tile per thread of a few warps)
-  const int gtid2 = ((threadIdx.x + (blockDim.x >> 1)) % blockDim.x) * gridDim.x + blockIdx.x;
+  const int gtid2 = ((threadIdx.x + (blockDim.x >> 1)) % blockDim.x) * npcta + pcta;
   for (int i = gtid2; i < off2[nu]; i += gstride) {
     const int u = find(off2, i);
     const UnitInfo& ui = unit_info(u);
@@ -458,6 +464,7 @@ struct PermuteArgs {
 // carry | 8 x 2E warp counts)], then the units' descriptors (plan), then the
 // superchunk prefixes (sc path, kScCap x kScCodes)
 constexpr int kScLd = kScCodes + 1;  // shared-memory row stride of the superchunk prefixes
+constexpr int kPlanCtasMin = 8;      // permute_sc: blocks without chunks that take the work lists alone
 static_assert(kScCodes == 128, "superchunk rows are indexed with shifts");
 __host__ __device__ inline int permute_smem_ints(int E) { return (2 * E * (1 + 4 * (1 + 8)) + 3) & ~3; }
 __host__ __device__ inline int permute_units_ints(int nu) {
@@ -782,8 +789,20 @@ __global__ void __launch_bounds__(1024) permute_sc_kernel(const PermuteArgs a) {
     }
   }
   if (DSB_PERMUTE_PHASES) tp[4] = gtimer();
-  // ---- this CTA's share of the GEMM work lists (descriptors already staged)
-  if (a.do_plan) plan_body(a.plan, s_seg, off1, off2, su, true);
+  // ---- GEMM work lists (descriptors already staged).  When enough blocks
+  // have no chunk to scatter (T <= 18944 at 148 SMs: 20+ idle blocks at
+  // T = 16384) they build the lists while the others scatter; otherwise every
+  // block builds its share after its scatter.
+  if (a.do_plan) {
+    const int scatter_ctas = min(static_cast<int>(gridDim.x), cdiv(a.nchunks, kGroups));
+    const int idle = static_cast<int>(gridDim.x) - scatter_ctas;
+    if (idle >= kPlanCtasMin) {
+      if (static_cast<int>(blockIdx.x) >= scatter_ctas)
+        plan_body(a.plan, s_seg, off1, off2, su, true, blockIdx.x - scatter_ctas, idle);
+    } else {
+      plan_body(a.plan, s_seg, off1, off2, su, true);
+    }
+  }
   if (DSB_PERMUTE_PHASES) {
     tp[5] = gtimer();
     if (phase_block())
