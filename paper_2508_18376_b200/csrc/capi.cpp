@@ -1045,11 +1045,13 @@ void run_gemms(dsmoe_b200_ctx* C, const dsmoe_b200_layer* L, const void* rows, l
     // TMA-store targets: 32-row boxes (one per epilogue warp)
     const CUtensorMap my = make_map(y, y_rows, L->d, L->d, 32, gemm_tc_store_box_cols());
     const CUtensorMap mh32 = make_map(C->H.p, h_rows, L->hstride, L->hstride, 32, gemm_tc_store_box_cols());
-    // DSMOE_B200_SCHED=static: the CTA pairs walk their tiles in a fixed
-    // round-robin instead of claiming them (A/B)
+    // The CTA pairs walk their tiles in a fixed round-robin.  DSMOE_B200_SCHED=dyn
+    // makes GEMM1 claim them dynamically (dyn2: both GEMMs): fewer SM cycles
+    // under ncu's serialised replay, but 8 us slower per step in the
+    // back-to-back loop (tools/gemm_span.sh, profiles/r4_ab_front.txt)
     static const bool dyn_env = [] {
       const char* v = std::getenv("DSMOE_B200_SCHED");
-      return !(v && std::string(v) == "static");
+      return v && (std::string(v) == "dyn" || std::string(v) == "dyn2");
     }();
     static const bool dyn2_env = [] {  // GEMM2 claims too (DSMOE_B200_SCHED=dyn2)
       const char* v = std::getenv("DSMOE_B200_SCHED");

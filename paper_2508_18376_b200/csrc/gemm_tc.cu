@@ -822,9 +822,9 @@ __global__ void __launch_bounds__(Geo<MODE, PAIR>::THREADS, 1)
       __threadfence();
       const unsigned long long e0 = atomicAdd(&g[0], 0ull);
       if (e0 != 0ull)
-        printf("gemm%d: entry spread %llu, wait at +%llu..+%llu, end at +%llu..+%llu ns (from first entry)\n", MODE,
-               atomicAdd(&g[1], 0ull) - e0, atomicAdd(&g[2], 0ull) - e0, atomicAdd(&g[3], 0ull) - e0,
-               atomicAdd(&g[4], 0ull) - e0, atomicAdd(&g[5], 0ull) - e0);
+        printf("gemm%d: entry spread %llu, wait at +%llu..+%llu, end at +%llu..+%llu ns (from first entry) abs %llu %llu\n",
+               MODE, atomicAdd(&g[1], 0ull) - e0, atomicAdd(&g[2], 0ull) - e0, atomicAdd(&g[3], 0ull) - e0,
+               atomicAdd(&g[4], 0ull) - e0, atomicAdd(&g[5], 0ull) - e0, e0, atomicAdd(&g[5], 0ull));
       g[0] = g[2] = g[4] = ~0ull;
       g[1] = g[3] = g[5] = 0ull;
       g[6] = 0ull;
