@@ -821,8 +821,9 @@ __global__ void __launch_bounds__(kGrThreads, 1)
   __syncthreads();
   if (DSB_GR_TIMES && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 100 || blockIdx.x == gridDim.x - 1)) {
     const unsigned long long t0 = s_gt[0], te = gr_now();
-    printf("gate_route cta %d: tile0 acc %llu routed %llu | tile1 acc %llu routed %llu | end %llu ns\n", blockIdx.x,
-           s_gt[1] - t0, s_gt[2] - t0, s_gt[3] > t0 ? s_gt[3] - t0 : 0ull, s_gt[4] > t0 ? s_gt[4] - t0 : 0ull, te - t0);
+    printf("gate_route cta %d: tile0 acc %llu routed %llu | tile1 acc %llu routed %llu | end %llu ns abs %llu\n",
+           blockIdx.x, s_gt[1] - t0, s_gt[2] - t0, s_gt[3] > t0 ? s_gt[3] - t0 : 0ull, s_gt[4] > t0 ? s_gt[4] - t0 : 0ull,
+           te - t0, t0);
   }
   if (warp == 1) tmem_dealloc(tmem_base, 2 * EPAD);
   if (threadIdx.x == 0) {
