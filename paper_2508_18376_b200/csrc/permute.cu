@@ -806,10 +806,11 @@ __global__ void __launch_bounds__(1024) permute_sc_kernel(const PermuteArgs a) {
   if (DSB_PERMUTE_PHASES) {
     tp[5] = gtimer();
     if (phase_block())
-      printf("permute_sc block %d: wait %llu  A' %llu  B12 %llu  B3 %llu (prologue %llu tiles1 %llu tiles2 %llu) ns\n",
+      printf("permute_sc block %d: wait %llu  A' %llu  B12 %llu  B3 %llu (prologue %llu tiles1 %llu tiles2 %llu) ns"
+             " abs %llu %llu %llu\n",
              blockIdx.x, tp[1] - tp[0], tp[2] - tp[1], tp[4] - tp[3], tp[5] - tp[4],
              a.do_plan ? s_tq[0] - tp[4] : 0ull, a.do_plan ? s_tq[1] - s_tq[0] : 0ull,
-             a.do_plan ? s_tq[2] - s_tq[1] : 0ull);
+             a.do_plan ? s_tq[2] - s_tq[1] : 0ull, tp[0], tp[1], tp[5]);
   }
 }
 
